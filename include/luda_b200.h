@@ -1,0 +1,150 @@
+/*
+ * luda_b200.h — C ABI of the B200-native LUDA compaction path.
+ *
+ * The reference (pure Python, /root/reference/pkg/src/luda) exposes its
+ * compaction path through an offload-device plugin protocol
+ * (device.py:253-627: make_device → alloc/free/stage_in/stage_out/dispatch/
+ * stats/close) and a SPEC-level entry point run_compaction(job, device)
+ * (SPEC.md:323-331). This header is the native seam those calls bind to.
+ * Every entry point returns an int status (enum luda_status); the message of
+ * the last failure on the calling thread is available from luda_last_error().
+ *
+ * No torch types cross this boundary: device buffers are plain pointers,
+ * streams/events are opaque handles (cudaStream_t / cudaEvent_t).
+ */
+#ifndef LUDA_B200_H
+#define LUDA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; mapped to the reference exception tree (errors.py:4-46) by
+ * paper_2004_03054_b200/errors.py:from_status. */
+enum luda_status {
+  LUDA_OK = 0,
+  LUDA_CORRUPT = 1,     /* CorruptionError(offset) — checksum mismatch        */
+  LUDA_FORMAT = 2,      /* FormatError — malformed footer/filter/index/block  */
+  LUDA_CAPACITY = 3,    /* CapacityError                                       */
+  LUDA_ORDERING = 4,    /* OrderingError — input run not strictly ascending    */
+  LUDA_DEVICE = 5,      /* DeviceError — CUDA failure / bad argument           */
+  LUDA_UNSUPPORTED = 6  /* valid input outside the fast-path envelope          */
+};
+
+/* Kernel kinds of the reference KernelSpec (kernels.py:171-178). */
+enum luda_kind { LUDA_KIND_UNPACK = 0, LUDA_KIND_SHARED_KEY = 1, LUDA_KIND_ENCODE = 2,
+                 LUDA_KIND_FILTER = 3 };
+
+/* ---- context ----------------------------------------------------------- */
+/* Replaces make_device(DeviceConfig) bring-up (device.py:622-627). */
+int luda_init(int device_ordinal);
+int luda_shutdown(void);
+const char* luda_last_error(void);
+int64_t luda_last_error_offset(void); /* block offset of the last LUDA_CORRUPT, or -1 */
+int luda_abi_version(void);
+
+/* ---- regions: device arena + pinned host staging ------------------------ */
+/* Replaces _DeviceBase.alloc/free (device.py:266-294). */
+int luda_region_alloc(uint64_t nbytes, void** dev_ptr);
+int luda_region_free(void* dev_ptr);
+int luda_host_alloc(uint64_t nbytes, void** host_ptr);
+int luda_host_free(void* host_ptr);
+
+/* ---- streams, transfers, events ----------------------------------------- */
+/* Replaces stage_in/stage_out on the named FIFO streams in_lower/in_upper/out
+ * (device.py:298-333, 511-547): one CUDA stream per named stream. */
+int luda_stream_create(void** stream);
+int luda_stream_destroy(void* stream);
+int luda_stream_sync(void* stream);
+int luda_stage_in_async(void* dst_dev, const void* src_host, uint64_t nbytes, void* stream);
+int luda_stage_out_async(void* dst_host, const void* src_dev, uint64_t nbytes, void* stream);
+int luda_memcpy_d2d_async(void* dst_dev, const void* src_dev, uint64_t nbytes, void* stream);
+int luda_event_create(void** event);
+int luda_event_record(void* event, void* stream);
+int luda_event_query(void* event); /* 1 = complete, 0 = pending, <0 = error */
+int luda_event_wait(void* event);
+int luda_event_elapsed_ms(void* start, void* stop, float* ms);
+int luda_event_destroy(void* event);
+int luda_stream_wait_event(void* stream, void* event);
+
+/* ---- primitives --------------------------------------------------------- */
+/* CRC-32/IEEE of a device buffer (checksum.py:12-13); synchronous. */
+int luda_crc32(const void* dev_data, uint64_t nbytes, uint32_t* out_crc, void* stream);
+/* Batched CRC: crc of [data+off[i], +len[i]) for i < n, written to dev out. */
+int luda_crc32_batch(const void* dev_data, const uint64_t* dev_off, const uint32_t* dev_len,
+                     uint32_t n, uint32_t* dev_out, void* stream);
+
+/* ---- per-kind dispatch (reference KernelSpec semantics) ----------------- */
+/* Replaces SerialDevice/HostParallelDevice.dispatch (device.py:435-456,
+ * 566-607) for the four kinds of kernels.py:72-168.
+ *   items      : host array, n_items rows of the kind's argument tuple as
+ *                int64 (unpack 9, shared_key 6, encode 10, filter 7 columns)
+ *   region_ptr : host array mapping region id → device pointer
+ *   region_cap : host array mapping region id → capacity (bytes)
+ *   results    : host out, n_items rows of the kind's result tuple as int64
+ *                (unpack 4, shared_key 1, encode 2, filter 1 columns)
+ *   fail_item  : index of the first failing item in dispatch order, or -1;
+ *                its tag (status) is the return value, its message in
+ *                luda_last_error() and corrupt offset in luda_last_error_offset().
+ * Synchronous on `stream`. */
+int luda_dispatch(int kind, const int64_t* items, uint32_t n_items,
+                  void* const* region_ptr, const uint64_t* region_cap, uint32_t n_regions,
+                  int64_t* results, int64_t* fail_item, void* stream);
+
+/* ---- fused compaction job (run_compaction) ------------- */
+typedef struct {
+  const uint8_t* arena;         /* device: staged input files                     */
+  uint64_t arena_bytes;
+  uint32_t n_files;
+  const uint64_t* file_off;     /* host[n_files]: file i at arena + file_off[i]    */
+  const uint64_t* file_len;     /* host[n_files]                                   */
+  const int64_t* file_offset_base; /* host[n_files] or NULL: added to error offsets */
+  uint32_t n_runs;              /* sorted runs, in merge-priority order            */
+  const uint32_t* run_first_file; /* host[n_runs+1]                               */
+  uint32_t block_size;          /* StoreConfig.block_size (config.py:48)           */
+  uint32_t restart_interval;    /* StoreConfig.restart_interval (config.py:49)     */
+  uint32_t bits_per_key;        /* StoreConfig.bits_per_key (config.py:50)         */
+  uint64_t sst_size_target;     /* StoreConfig.sst_size_target (config.py:47)      */
+  /* Version.covers_below(target_level) as closed user-key intervals
+   * (version.py:122-128): n_deeper pairs, keys packed back to back. */
+  uint32_t n_deeper;
+  const uint8_t* deeper_keys;   /* host: lo0 hi0 lo1 hi1 ...                       */
+  const uint32_t* deeper_lens;  /* host[2*n_deeper]                                */
+  /* Optional key-range restriction [range_lo, range_hi) on user keys
+   * (subcompactions); NULL = unbounded on that side. */
+  const uint8_t* range_lo; uint32_t range_lo_len;
+  const uint8_t* range_hi; uint32_t range_hi_len;
+} luda_job_desc;
+
+typedef struct {
+  uint8_t* out;                 /* device: output SSTs back to back (lib-owned)   */
+  uint64_t out_bytes;
+  uint32_t n_sst;
+  uint64_t* sst_off;            /* host[n_sst] (lib-owned)                         */
+  uint64_t* sst_len;            /* host[n_sst]                                     */
+  uint32_t key_len;             /* internal key length K                           */
+  uint8_t* sst_keys;            /* host[n_sst*2*K]: smallest ∥ largest per SST     */
+  uint64_t n_in, n_out, blocks_in, blocks_out;
+  double t_ms[8];               /* parse, decode, merge, plan, encode, meta, -, total */
+  void* priv;
+} luda_job_result;
+
+int luda_compact(const luda_job_desc* job, luda_job_result* result, void* stream);
+int luda_job_release(luda_job_result* result);
+
+/* Build SSTs from already-sorted unique records (used by the bench to
+ * synthesise inputs and by the L0-flush path): records are produced by
+ * luda_records_from_keys from flat arrays. Outputs like luda_compact. */
+int luda_build_from_sorted(const uint8_t* dev_user_keys, uint32_t user_key_len,
+                           const uint64_t* dev_trailers, const uint8_t* dev_values,
+                           const uint64_t* dev_value_off, const uint32_t* dev_value_len,
+                           uint64_t n, uint32_t block_size, uint32_t restart_interval,
+                           uint32_t bits_per_key, uint64_t sst_size_target,
+                           luda_job_result* result, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LUDA_B200_H */

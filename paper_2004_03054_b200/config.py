@@ -20,8 +20,7 @@ def default_device_workers() -> int:
 
 @dataclass
 class DeviceConfig:
-    # "b200" selects this package's CUDA backend; "serial" is accepted too and
-    # maps onto the same backend (it has no host-thread semantics to emulate).
+    # "b200" selects this package's CUDA backend (the only backend here).
     backend: str = "b200"
     workers: int = 0
     bandwidth_bytes_per_sec: float = 8 * 2**30

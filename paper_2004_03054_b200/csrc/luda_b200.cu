@@ -1,0 +1,875 @@
+// luda_b200.cu — C ABI (include/luda_b200.h) and the native job orchestrator.
+//
+// Single translation unit: every stage header is included here so device
+// globals (CRC tables) need no relocatable device code.
+//
+// luda_compact(job) runs the fused compaction pipeline on one stream:
+//   parse_files_a + crc_ranges   footer/filter/index checks   (sst.py:284-310)
+//   parse_files_c                data-block table
+//   decode_kernel<W>             CRC verify + parse → records (blocks.py:130-165)
+//   merge passes <W>             merge path + resolve + compaction (SPEC D12/D20)
+//   block_jump + chain           exact SstBuilder block cut     (sst.py:138-162)
+//   scan + sst_jump + chain      exact SST cut (SizeOverflowError rule)
+//   encode_kernel<W>             data blocks (blocks.py:77-103)
+//   sst_meta_kernel<W>           filter, index, footer          (bloom.py:71-88, sst.py:67-76, 206-208)
+// Host syncs happen only where a count decides the next launch shape.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/luda_b200.h"
+#include "luda_common.cuh"
+#include "luda_decode.cuh"
+#include "luda_encode.cuh"
+#include "luda_merge.cuh"
+#include "luda_parse.cuh"
+#include "luda_plan.cuh"
+#include "luda_rec.cuh"
+#include "luda_tables.cuh"
+
+using namespace luda;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_err_off = -1;
+int g_device = -1;
+int g_num_sms = 148;
+
+int fail(int status, const std::string& msg, int64_t off = -1) {
+  g_err = msg;
+  g_err_off = off;
+  return status;
+}
+
+#define CK(expr)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(LUDA_DEVICE, std::string(#expr " failed: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Stream-ordered scratch allocations released together.
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  T* get(uint64_t count, bool zero = false) {
+    void* p = nullptr;
+    const uint64_t bytes = std::max<uint64_t>(count * sizeof(T), 16) + 256;
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    if (zero) cudaMemsetAsync(p, 0, bytes, st);
+    return reinterpret_cast<T*>(p);
+  }
+  void* release_last() {
+    void* p = ptrs.back();
+    ptrs.pop_back();
+    return p;
+  }
+};
+
+#define GET(var, T, count, zero)                                                  \
+  T* var = scratch.get<T>((count), (zero));                                       \
+  if (!var) return fail(LUDA_DEVICE, "device allocation failed (" #var ")");
+
+struct JobPriv {
+  std::vector<uint64_t> off, len;
+  std::vector<uint8_t> keys;
+};
+
+const char* file_msg(uint32_t code) {
+  switch (code) {
+    case F_SHORT: return "file too short for footer";
+    case F_FILTER_SHORT: return "filter block too short";
+    case F_INDEX_SHORT: return "index block too short";
+    case F_IDX_VARINT_TRUNC: return "truncated varint";
+    case F_IDX_VARINT_LONG: return "varint too long";
+    case F_IDX_TRUNC: return "truncated index entry";
+    case F_IDX_TRAILING: return "trailing garbage in index block";
+    default: return "format error";
+  }
+}
+
+const char* block_msg(uint32_t code) {
+  switch (code) {
+    case B_SHORT: return "block too short";
+    case B_CRC: return "data block checksum mismatch";
+    case B_RESTART: return "bad restart array";
+    case B_VARINT_TRUNC: return "truncated varint";
+    case B_VARINT_LONG: return "varint too long";
+    case B_TRUNC_ENTRY: return "truncated block entry";
+    case B_TRAILING: return "trailing garbage in block entries";
+    case B_KEYLEN: return "keys of differing lengths in one job are not supported by the b200 fast path";
+    case B_VALUE_BIG: return "value longer than 16 MiB (or arena beyond 1 TiB) not supported by the b200 fast path";
+    default: return "block error";
+  }
+}
+
+int sync(cudaStream_t st) {
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  return LUDA_OK;
+}
+
+double ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Host transform of a user-key bound into the padded L-byte comparison domain
+// (see luda_merge.cuh). `lower` = bound is a lower bound (k >= b); `closed`
+// selects <=/>= vs </>.
+KeyBound make_bound(const uint8_t* key, uint32_t klen, uint32_t L, bool lower, bool closed) {
+  // Comparisons are done on user keys zero-padded to L bytes (luda_merge.cuh).
+  //   lower, closed (k >= key):  klen <= L → pad(k) >= pad(key); klen > L → pad(k) > pad(key[:L])
+  //   upper, closed (k <= key):  klen == L → <=;  klen < L → <;  klen > L → <= pad(key[:L])
+  //   upper, open   (k <  key):  klen <= L → <;   klen > L → <= pad(key[:L])
+  KeyBound b{};
+  b.present = 1;
+  uint8_t pad[32] = {0};
+  memcpy(pad, key, std::min(klen, L));
+  for (int w = 0; w < 4; ++w) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v = (v << 8) | pad[8 * w + i];
+    b.k[w] = v;
+  }
+  if (lower) b.incl = klen <= L;
+  else if (closed) b.incl = klen >= L;
+  else b.incl = klen > L;
+  return b;
+}
+
+struct RunSeg {
+  uint64_t start, len;
+};
+
+template <int W>
+int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, Rec<W>* Y, Rec<W>* S, std::vector<RunSeg> runs,
+               const ResolveArgs& ra_final, unsigned long long* d_err_order, unsigned long long* d_nout) {
+  // drop empty runs
+  std::vector<RunSeg> segs;
+  for (auto& r : runs)
+    if (r.len) segs.push_back(r);
+  if (segs.empty()) {
+    CK(cudaMemsetAsync(d_nout, 0, 8, st));
+    return LUDA_OK;
+  }
+  bool first_pass = true;
+  const size_t smem = sizeof(Rec<W>) * kMergeTile + 4 * kMergeTile;
+  CK(cudaFuncSetAttribute(merge_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto launch = [&](const Rec<W>* A, uint64_t na, const Rec<W>* B, uint64_t nb, Rec<W>* out, uint64_t abase,
+                    uint64_t bbase, bool resolve) -> int {
+    const uint64_t ntiles = (na + nb + kMergeTile - 1) / kMergeTile;
+    GET(split, uint64_t, ntiles + 1, false);
+    merge_partition_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, st>>>(A, na, B, nb, ntiles, split);
+    MergeArgs<W> m{};
+    m.A = A; m.na = na; m.B = B; m.nb = nb; m.split = split; m.ntiles = ntiles; m.out = out;
+    m.a_run_base = abase; m.b_run_base = bbase;
+    m.err_order = d_err_order;  // order errors are reported for original runs only
+    m.ra.resolve = resolve;
+    if (resolve) {
+      m.ra = ra_final;
+      m.ra.resolve = true;
+      GET(lb, uint64_t, ntiles, true);
+      GET(ctr, unsigned int, 1, true);
+      m.lb = lb;
+      m.tile_ctr = ctr;
+      m.n_out = d_nout;
+    }
+    if (!first_pass) {
+      GET(sink, unsigned long long, 1, true);
+      m.err_order = sink;
+    }
+    merge_kernel<W><<<(unsigned)ntiles, kMergeThreads, smem, st>>>(m);
+    CK(cudaGetLastError());
+    return LUDA_OK;
+  };
+  Rec<W>* cur = X;
+  Rec<W>* nxt = Y;
+  while (segs.size() > 2) {
+    std::vector<RunSeg> next;
+    for (size_t i = 0; i < segs.size(); i += 2) {
+      if (i + 1 < segs.size()) {
+        const RunSeg a = segs[i], b = segs[i + 1];
+        int rc = launch(cur + a.start, a.len, cur + b.start, b.len, nxt + a.start, a.start, b.start, false);
+        if (rc) return rc;
+        next.push_back({a.start, a.len + b.len});
+      } else {
+        const RunSeg a = segs[i];
+        if (first_pass) {  // still order-check the odd run
+          int rc = launch(cur + a.start, a.len, cur + a.start, 0, nxt + a.start, a.start, a.start, false);
+          if (rc) return rc;
+        } else {
+          CK(cudaMemcpyAsync(nxt + a.start, cur + a.start, a.len * sizeof(Rec<W>), cudaMemcpyDeviceToDevice, st));
+        }
+        next.push_back(a);
+      }
+    }
+    segs = next;
+    std::swap(cur, nxt);
+    first_pass = false;
+  }
+  if (segs.size() == 2) return launch(cur + segs[0].start, segs[0].len, cur + segs[1].start, segs[1].len, S,
+                                      segs[0].start, segs[1].start, true);
+  return launch(cur + segs[0].start, segs[0].len, cur + segs[0].start, 0, S, segs[0].start, segs[0].start, true);
+}
+
+struct ChainBufs {
+  uint32_t* nodes;
+  uint32_t n_nodes;
+};
+
+// Greedy chain over jmp[0..n) with max jump D; returns nodes (device) + count.
+int run_chain(cudaStream_t st, Scratch& scratch, const uint32_t* jmp, uint32_t n, uint32_t D, uint32_t T_min,
+              ChainBufs& outb) {
+  if (n == 0) {
+    outb.n_nodes = 0;
+    outb.nodes = nullptr;
+    return LUDA_OK;
+  }
+  D = std::max<uint32_t>(D, 1);
+  uint32_t T = std::max<uint32_t>(T_min, D);
+  T = (T + 31) & ~31u;
+  const uint32_t ntiles = (uint32_t)((n + (uint64_t)T - 1) / T);
+  const uint32_t G = std::max<uint32_t>(1, (uint32_t)std::ceil(std::sqrt((double)ntiles)));
+  const uint32_t ngroups = (ntiles + G - 1) / G;
+  ChainArgs c{};
+  c.jmp = jmp; c.n = n; c.T = T; c.D = D; c.ntiles = ntiles; c.G = G; c.ngroups = ngroups;
+  GET(ex, uint32_t, (uint64_t)ntiles * D, false);
+  GET(cn, uint32_t, (uint64_t)ntiles * D, false);
+  GET(gex, uint32_t, (uint64_t)ngroups * D, false);
+  GET(gcn, uint32_t, (uint64_t)ngroups * D, false);
+  GET(gen, uint32_t, ngroups, false);
+  GET(gba, uint32_t, ngroups, false);
+  GET(nodes, uint32_t, n, false);
+  GET(nn, uint32_t, 1, true);
+  c.exit_ = ex; c.cnt = cn; c.gexit = gex; c.gcnt = gcn; c.gentry = gen; c.gbase = gba; c.nodes = nodes; c.nnodes = nn;
+  const size_t sm = T <= 12288 ? (size_t)T * 4 : 0;
+  if (sm > 48 * 1024) CK(cudaFuncSetAttribute(chain_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  chain_map_kernel<<<ntiles, kChainThreads, sm, st>>>(c);
+  chain_group_kernel<<<ngroups, kChainThreads, 0, st>>>(c);
+  chain_top_kernel<<<1, 32, 0, st>>>(c);
+  chain_emit_kernel<<<ntiles, kChainThreads, 0, st>>>(c);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&outb.n_nodes, nn, 4, cudaMemcpyDeviceToHost, st));
+  int rc = sync(st);
+  if (rc) return rc;
+  outb.nodes = nodes;
+  return LUDA_OK;
+}
+
+struct EmitParams {
+  uint32_t K, block_size, ri, bpk;
+  uint64_t sst_target;
+  uint32_t min_entry;  // lower bound of one encoded entry (sizes the planner halo)
+};
+
+// Plan + encode the survivors `S[0..n)` whose values live in `varena`.
+template <int W>
+int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n, const uint8_t* varena,
+                  const EmitParams& p, luda_job_result* res, cudaEvent_t* ev) {
+  JobPriv* priv = new JobPriv();
+  res->priv = priv;
+  res->key_len = p.K;
+  res->n_out = n;
+  if (n == 0) {
+    res->n_sst = 0;
+    res->out = nullptr;
+    res->out_bytes = 0;
+    return LUDA_OK;
+  }
+  if (n >= 0xFFFFFFF0ull) return fail(LUDA_UNSUPPORTED, "more than 2^32 surviving entries in one job");
+  // ---- block jumps ----
+  const uint32_t max_entries = std::max<uint32_t>(1, (p.block_size > 8 ? (p.block_size - 8) / p.min_entry : 0) + 1);
+  const uint32_t halo = ((max_entries + 1 + 31) / 32) * 32;
+  if (halo > 8192) return fail(LUDA_UNSUPPORTED, "block_size too large for the b200 planner");
+  GET(jmp, uint32_t, n, false);
+  GET(bsz, uint32_t, n, false);
+  GET(ctl, unsigned int, 4, true);  // jmax, overflow, jmax_sst
+  BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1};
+  const size_t jsm = 2ull * (kJumpTile + halo) * 4;
+  CK(cudaFuncSetAttribute(block_jump_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
+  block_jump_kernel<W><<<(unsigned)((n + kJumpTile - 1) / kJumpTile), kJumpThreads, jsm, st>>>(ja);
+  CK(cudaGetLastError());
+  unsigned int hctl[4];
+  CK(cudaMemcpyAsync(hctl, ctl, 16, cudaMemcpyDeviceToHost, st));
+  int rc = sync(st);
+  if (rc) return rc;
+  if (hctl[1]) return fail(LUDA_DEVICE, "block planner halo overflow");
+  ChainBufs bch{};
+  rc = run_chain(st, scratch, jmp, (uint32_t)n, hctl[0], 8192, bch);
+  if (rc) return rc;
+  const uint32_t nblk = bch.n_nodes;
+  res->blocks_out = nblk;
+  GET(blk_first, uint32_t, nblk, false);
+  GET(blk_n, uint32_t, nblk, false);
+  GET(blk_size, uint32_t, nblk, false);
+  GET(blk_pos, uint64_t, nblk + 1, false);
+  block_desc_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(bch.nodes, nblk, jmp, bsz, blk_first, blk_n, blk_size);
+  {
+    const uint64_t nt = std::max<uint64_t>(1, (nblk + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
+    GET(lb, uint64_t, nt, true);
+    GET(ctr, unsigned int, 1, true);
+    scan_excl_kernel<uint32_t><<<(unsigned)nt, kScanThreads, 0, st>>>(blk_size, nblk, blk_pos, lb, ctr);
+  }
+  // ---- SST cut ----
+  GET(sjmp, uint32_t, nblk, false);
+  sst_jump_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, p.sst_target, sjmp, ctl + 2);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hctl, ctl, 16, cudaMemcpyDeviceToHost, st));
+  rc = sync(st);
+  if (rc) return rc;
+  ChainBufs sch{};
+  rc = run_chain(st, scratch, sjmp, nblk, hctl[2], 8192, sch);
+  if (rc) return rc;
+  const uint32_t nsst = sch.n_nodes;
+  GET(sst_size, uint64_t, nsst, false);
+  GET(sst_data, uint64_t, nsst, false);
+  GET(sst_nent, uint64_t, nsst, false);
+  GET(sst_last, uint32_t, nsst, false);
+  GET(sst_off, uint64_t, nsst + 1, false);
+  SstLayoutArgs la{sch.nodes, nsst, nblk, blk_first, blk_pos, n, p.K, p.bpk, sst_size, sst_data, sst_nent, sst_last};
+  sst_layout_kernel<<<(nsst + 255) / 256, 256, 0, st>>>(la);
+  {
+    const uint64_t nt = std::max<uint64_t>(1, (nsst + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
+    GET(lb, uint64_t, nt, true);
+    GET(ctr, unsigned int, 1, true);
+    scan_excl_kernel<uint64_t><<<(unsigned)nt, kScanThreads, 0, st>>>(sst_size, nsst, sst_off, lb, ctr);
+  }
+  priv->off.resize(nsst + 1);
+  priv->len.resize(nsst);
+  std::vector<uint64_t> nent(nsst);
+  CK(cudaMemcpyAsync(priv->off.data(), sst_off, 8ull * (nsst + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(priv->len.data(), sst_size, 8ull * nsst, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(nent.data(), sst_nent, 8ull * nsst, cudaMemcpyDeviceToHost, st));
+  rc = sync(st);
+  if (rc) return rc;
+  if (ev) CK(cudaEventRecord(ev[0], st));
+  const uint64_t total = priv->off[nsst];
+  // big-filter scratch
+  std::vector<uint64_t> soff(nsst, ~0ull);
+  uint64_t big_words = 0;
+  for (uint32_t s = 0; s < nsst; ++s) {
+    uint64_t nbits = std::max<uint64_t>(64, nent[s] * p.bpk);
+    nbits = (nbits + 7) & ~7ull;
+    if (nbits / 8 + 1 > (uint64_t)kMetaBuf) {
+      soff[s] = big_words;
+      big_words += (nbits / 8 + 1 + 3) / 4 + 8;
+    }
+  }
+  void* outp = nullptr;
+  CK(cudaMalloc(&outp, total + 256));
+  res->out = reinterpret_cast<uint8_t*>(outp);
+  res->out_bytes = total;
+  GET(bigs, uint32_t, big_words + 16, true);
+  GET(d_soff, uint64_t, nsst, false);
+  CK(cudaMemcpyAsync(d_soff, soff.data(), 8ull * nsst, cudaMemcpyHostToDevice, st));
+  GET(d_keys, uint8_t, 2ull * nsst * p.K, false);
+  // ---- encode data blocks ----
+  EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off, res->out};
+  const size_t esm = sizeof(CrcSmem) + (size_t)kEncWarps * kEncBuf;
+  CK(cudaFuncSetAttribute(encode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
+  const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncWarps - 1) / kEncWarps, (uint64_t)g_num_sms);
+  encode_kernel<W><<<std::max(1u, egrid), kEncWarps * 32, esm, st>>>(ea);
+  CK(cudaGetLastError());
+  // ---- filter / index / footer ----
+  const uint32_t kprobes = std::max(1, std::min(30, (int)std::lround(p.bpk * std::log(2.0))));
+  MetaArgs<W> ma{S, p.K, p.bpk, kprobes, nsst, sch.nodes, sst_last, sst_off, sst_data, sst_nent, sst_size,
+                 blk_first, blk_n, blk_size, blk_pos, res->out, bigs, d_soff, d_keys};
+  CK(cudaFuncSetAttribute(sst_meta_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMetaSmem));
+  sst_meta_kernel<W><<<nsst, kMetaThreads, kMetaSmem, st>>>(ma);
+  CK(cudaGetLastError());
+  if (ev) CK(cudaEventRecord(ev[1], st));
+  priv->keys.resize(2ull * nsst * p.K);
+  CK(cudaMemcpyAsync(priv->keys.data(), d_keys, priv->keys.size(), cudaMemcpyDeviceToHost, st));
+  rc = sync(st);
+  if (rc) return rc;
+  res->n_sst = nsst;
+  res->sst_off = priv->off.data();
+  res->sst_len = priv->len.data();
+  res->sst_keys = priv->keys.data();
+  return LUDA_OK;
+}
+
+template <int W>
+int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_job_result* res, uint32_t K,
+              uint32_t nblk, const BlockTable& bt, const uint32_t* d_file_blk_base,
+              const std::vector<uint32_t>& file_blk_base, uint64_t bound, cudaEvent_t* ev) {
+  const uint32_t L = K - 8;
+  res->blocks_in = nblk;
+  // ---- decode ----
+  uint64_t cap = std::max<uint64_t>(bound, 1);
+  GET(d_base, uint64_t, nblk + 1, false);
+  GET(errs, unsigned long long, 2, false);
+  const size_t dsm = sizeof(CrcSmem) + (size_t)kDecWarps * kDecWarpBytes;
+  CK(cudaFuncSetAttribute(decode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+  Rec<W>* X = nullptr;
+  uint64_t n_in = 0;
+  std::vector<uint64_t> fbase(jd->n_files + 1);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    X = scratch.get<Rec<W>>(cap, false);
+    if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
+    CK(cudaMemsetAsync(errs, 0xFF, 16, st));
+    GET(lb, uint64_t, nblk, true);
+    GET(ctr, unsigned int, 1, true);
+    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, cap, lb, ctr, d_base, errs, errs + 1};
+    decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
+    CK(cudaGetLastError());
+    GET(d_fbase, uint64_t, jd->n_files + 1, false);
+    file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_base, d_file_blk_base, jd->n_files,
+                                                                           d_fbase);
+    unsigned long long herr[2];
+    CK(cudaMemcpyAsync(herr, errs, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
+    int rc = sync(st);
+    if (rc) return rc;
+    if (herr[0] != ~0ull || herr[1] != ~0ull) {
+      const bool ref = herr[0] != ~0ull;
+      const unsigned long long e = ref ? herr[0] : herr[1];
+      const uint32_t b = (uint32_t)(e >> 8), code = (uint32_t)(e & 0xFF);
+      uint32_t foff = 0;
+      CK(cudaMemcpy(&foff, bt.foff + b, 4, cudaMemcpyDeviceToHost));
+      if (!ref) return fail(LUDA_UNSUPPORTED, block_msg(code));
+      if (code == B_CRC) return fail(LUDA_CORRUPT, block_msg(code), foff);
+      return fail(LUDA_FORMAT, block_msg(code));
+    }
+    n_in = fbase[jd->n_files];
+    if (n_in <= cap) break;
+    cap = n_in;  // exact re-run (non-canonical restart layout exceeded the bound)
+  }
+  res->n_in = n_in;
+  if (ev) CK(cudaEventRecord(ev[2], st));
+  // ---- merge + resolve ----
+  ResolveArgs ra{};
+  std::vector<KeyBound> bounds;
+  {
+    const uint8_t* kp = jd->deeper_keys;
+    for (uint32_t i = 0; i < jd->n_deeper; ++i) {
+      const uint32_t llo = jd->deeper_lens[2 * i], lhi = jd->deeper_lens[2 * i + 1];
+      bounds.push_back(make_bound(kp, llo, L, true, true));
+      kp += llo;
+      bounds.push_back(make_bound(kp, lhi, L, false, true));
+      kp += lhi;
+    }
+  }
+  KeyBound* d_bounds = nullptr;
+  if (!bounds.empty()) {
+    d_bounds = scratch.get<KeyBound>(bounds.size(), false);
+    if (!d_bounds) return fail(LUDA_DEVICE, "device allocation failed (bounds)");
+    CK(cudaMemcpyAsync(d_bounds, bounds.data(), bounds.size() * sizeof(KeyBound), cudaMemcpyHostToDevice, st));
+  }
+  ra.deeper = d_bounds;
+  ra.n_deeper = jd->n_deeper;
+  if (jd->range_lo) ra.range_lo = make_bound(jd->range_lo, jd->range_lo_len, L, true, true);
+  if (jd->range_hi) ra.range_hi = make_bound(jd->range_hi, jd->range_hi_len, L, false, false);
+  ra.resolve = true;
+  std::vector<uint32_t> run_first(jd->run_first_file, jd->run_first_file + jd->n_runs + 1);
+  GET(Y, Rec<W>, n_in, false);
+  GET(S, Rec<W>, n_in, false);
+  GET(merr, unsigned long long, 2, false);
+  uint64_t n_out = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    std::vector<RunSeg> runs;
+    for (uint32_t r = 0; r + 1 < run_first.size(); ++r) {
+      const uint64_t a = fbase[run_first[r]], b = fbase[run_first[r + 1]];
+      runs.push_back({a, b - a});
+    }
+    CK(cudaMemsetAsync(merr, 0xFF, 8, st));
+    CK(cudaMemsetAsync(merr + 1, 0, 8, st));
+    int rc = merge_runs<W>(st, scratch, X, Y, S, runs, ra, merr, merr + 1);
+    if (rc) return rc;
+    unsigned long long hm[2];
+    CK(cudaMemcpyAsync(hm, merr, 16, cudaMemcpyDeviceToHost, st));
+    rc = sync(st);
+    if (rc) return rc;
+    if (hm[0] == ~0ull) {
+      n_out = hm[1];
+      break;
+    }
+    // violation at decoded position p: a seam between files of one run → split runs per file and retry
+    const uint64_t p = hm[0];
+    bool seam = false;
+    for (uint32_t f = 0; f < jd->n_files; ++f)
+      if (fbase[f] == p && fbase[f + 1] >= p) {
+        // file f starts at p; seam only if f is not the first file of its run
+        bool run_start = false;
+        for (uint32_t r : run_first) run_start |= (r == f);
+        seam = !run_start;
+      }
+    if (!seam || attempt == 1) return fail(LUDA_ORDERING, "input run not strictly ascending");
+    std::vector<uint32_t> per_file;
+    for (uint32_t f = 0; f <= jd->n_files; ++f) per_file.push_back(f);
+    run_first = per_file;
+  }
+  if (ev) CK(cudaEventRecord(ev[3], st));
+  // survivors have distinct user keys → LCP < L → unshared >= 9 → entry >= 12 B
+  EmitParams ep{K, jd->block_size, jd->restart_interval, jd->bits_per_key, jd->sst_size_target, 12};
+  return plan_and_emit<W>(st, scratch, S, n_out, jd->arena, ep, res, ev ? ev + 4 : nullptr);
+}
+
+template <int W>
+__global__ void records_from_arrays_kernel(const uint8_t* keys, uint32_t L, const uint64_t* trailers,
+                                           const uint64_t* voff, const uint32_t* vlen, uint64_t n, Rec<W>* out,
+                                           unsigned long long* bad) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Rec<W> r;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const uint32_t idx = 8 * j + b;
+      v = (v << 8) | (idx < L ? keys[i * L + idx] : 0u);
+    }
+    r.k[j] = v;
+  }
+  r.t = ~trailers[i];
+  if (vlen[i] > kMaxValueLen || voff[i] > kMaxValueOff) atomicMin(bad, 0ull);
+  r.h = handle_pack(voff[i], vlen[i]);
+  out[i] = r;
+}
+
+template <int W>
+__global__ void check_sorted_kernel(const Rec<W>* r, uint64_t n, unsigned long long* bad) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
+  if (i < n && rec_cmp(r[i - 1], r[i]) >= 0) atomicMin(bad, (unsigned long long)i);
+}
+
+template <int W>
+int build_w(cudaStream_t st, Scratch& scratch, const uint8_t* keys, uint32_t L, const uint64_t* tr,
+            const uint8_t* values, const uint64_t* voff, const uint32_t* vlen, uint64_t n, const EmitParams& ep,
+            luda_job_result* res) {
+  GET(R, Rec<W>, n, false);
+  GET(bad, unsigned long long, 1, false);
+  CK(cudaMemsetAsync(bad, 0xFF, 8, st));
+  const unsigned g = (unsigned)((n + 255) / 256);
+  records_from_arrays_kernel<W><<<g, 256, 0, st>>>(keys, L, tr, voff, vlen, n, R, bad);
+  check_sorted_kernel<W><<<g, 256, 0, st>>>(R, n, bad);
+  unsigned long long hb = 0;
+  CK(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
+  int rc = sync(st);
+  if (rc) return rc;
+  if (hb == 0) return fail(LUDA_UNSUPPORTED, "value too large for the b200 record handle");
+  if (hb != ~0ull) return fail(LUDA_ORDERING, "keys not strictly ascending");
+  res->n_in = n;
+  return plan_and_emit<W>(st, scratch, R, n, values, ep, res, nullptr);
+}
+
+}  // namespace
+
+extern "C" {
+
+int luda_abi_version(void) { return 1; }
+
+const char* luda_last_error(void) { return g_err.c_str(); }
+int64_t luda_last_error_offset(void) { return g_err_off; }
+
+int luda_init(int device_ordinal) {
+  CK(cudaSetDevice(device_ordinal));
+  if (g_device == device_ordinal) return LUDA_OK;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device_ordinal));
+  if (prop.major != 10) return fail(LUDA_DEVICE, std::string("not an sm_100 device: ") + prop.name);
+  g_num_sms = prop.multiProcessorCount;
+  if (upload_crc_tables()) return fail(LUDA_DEVICE, "CRC table upload failed");
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device_ordinal) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  g_device = device_ordinal;
+  return LUDA_OK;
+}
+
+int luda_shutdown(void) {
+  if (g_device >= 0) cudaDeviceSynchronize();
+  g_device = -1;
+  return LUDA_OK;
+}
+
+int luda_region_alloc(uint64_t nbytes, void** dev_ptr) {
+  CK(cudaMalloc(dev_ptr, std::max<uint64_t>(nbytes, 1) + 512));
+  return LUDA_OK;
+}
+int luda_region_free(void* p) {
+  CK(cudaFree(p));
+  return LUDA_OK;
+}
+int luda_host_alloc(uint64_t nbytes, void** p) {
+  CK(cudaHostAlloc(p, std::max<uint64_t>(nbytes, 1), cudaHostAllocDefault));
+  return LUDA_OK;
+}
+int luda_host_free(void* p) {
+  CK(cudaFreeHost(p));
+  return LUDA_OK;
+}
+int luda_stream_create(void** s) {
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  *s = st;
+  return LUDA_OK;
+}
+int luda_stream_destroy(void* s) {
+  CK(cudaStreamDestroy((cudaStream_t)s));
+  return LUDA_OK;
+}
+int luda_stream_sync(void* s) {
+  CK(cudaStreamSynchronize((cudaStream_t)s));
+  return LUDA_OK;
+}
+int luda_stage_in_async(void* dst, const void* src, uint64_t n, void* s) {
+  if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, (cudaStream_t)s));
+  return LUDA_OK;
+}
+int luda_stage_out_async(void* dst, const void* src, uint64_t n, void* s) {
+  if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, (cudaStream_t)s));
+  return LUDA_OK;
+}
+int luda_memcpy_d2d_async(void* dst, const void* src, uint64_t n, void* s) {
+  if (n) CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, (cudaStream_t)s));
+  return LUDA_OK;
+}
+int luda_event_create(void** e) {
+  cudaEvent_t ev;
+  CK(cudaEventCreate(&ev));
+  *e = ev;
+  return LUDA_OK;
+}
+int luda_event_record(void* e, void* s) {
+  CK(cudaEventRecord((cudaEvent_t)e, (cudaStream_t)s));
+  return LUDA_OK;
+}
+int luda_event_query(void* e) {
+  cudaError_t r = cudaEventQuery((cudaEvent_t)e);
+  if (r == cudaSuccess) return 1;
+  if (r == cudaErrorNotReady) return 0;
+  fail(LUDA_DEVICE, cudaGetErrorString(r));
+  return -1;
+}
+int luda_event_wait(void* e) {
+  CK(cudaEventSynchronize((cudaEvent_t)e));
+  return LUDA_OK;
+}
+int luda_event_elapsed_ms(void* a, void* b, float* ms) {
+  CK(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
+  return LUDA_OK;
+}
+int luda_event_destroy(void* e) {
+  CK(cudaEventDestroy((cudaEvent_t)e));
+  return LUDA_OK;
+}
+int luda_stream_wait_event(void* s, void* e) {
+  CK(cudaStreamWaitEvent((cudaStream_t)s, (cudaEvent_t)e, 0));
+  return LUDA_OK;
+}
+
+int luda_crc32_batch(const void* data, const uint64_t* off, const uint32_t* len, uint32_t n, uint32_t* out,
+                     void* stream) {
+  if (n == 0) return LUDA_OK;
+  const size_t sm = sizeof(CrcSmem) + kCrcWarps * (kGroup + 192);
+  CK(cudaFuncSetAttribute(crc_ranges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const unsigned grid = std::min<unsigned>((n + kCrcWarps - 1) / kCrcWarps, 4 * g_num_sms);
+  crc_ranges_kernel<<<grid, kCrcWarps * 32, sm, (cudaStream_t)stream>>>((const uint8_t*)data, off, len, n, out);
+  CK(cudaGetLastError());
+  return LUDA_OK;
+}
+
+int luda_crc32(const void* data, uint64_t n, uint32_t* out_crc, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* d = nullptr;
+  CK(cudaMallocAsync(&d, 4, st));
+  CK(cudaMemsetAsync(d, 0xFF, 4, st));
+  if (n < 4) {
+    uint64_t* o = nullptr;
+    uint32_t* l = nullptr;
+    CK(cudaMallocAsync(&o, 8, st));
+    CK(cudaMallocAsync(&l, 4, st));
+    const uint64_t z = 0;
+    const uint32_t nn = (uint32_t)n;
+    CK(cudaMemcpyAsync(o, &z, 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(l, &nn, 4, cudaMemcpyHostToDevice, st));
+    int rc = luda_crc32_batch(data, o, l, 1, d, stream);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(out_crc, d, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFreeAsync(o, st);
+    cudaFreeAsync(l, st);
+  } else {
+    const size_t sm = sizeof(CrcSmem) + kCrcWarps * (kGroup + 192);
+    CK(cudaFuncSetAttribute(crc_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const uint64_t np = (n + kGroup - 1) / kGroup;
+    const unsigned grid = (unsigned)std::min<uint64_t>((np + kCrcWarps - 1) / kCrcWarps, 4ull * g_num_sms);
+    crc_big_kernel<<<grid, kCrcWarps * 32, sm, st>>>((const uint8_t*)data, n, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_crc, d, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  cudaFreeAsync(d, st);
+  return LUDA_OK;
+}
+
+int luda_job_release(luda_job_result* r) {
+  if (!r) return LUDA_OK;
+  if (r->out) cudaFree(r->out);
+  delete reinterpret_cast<JobPriv*>(r->priv);
+  memset(r, 0, sizeof(*r));
+  return LUDA_OK;
+}
+
+int luda_build_from_sorted(const uint8_t* keys, uint32_t L, const uint64_t* trailers, const uint8_t* values,
+                           const uint64_t* voff, const uint32_t* vlen, uint64_t n, uint32_t block_size,
+                           uint32_t restart_interval, uint32_t bits_per_key, uint64_t sst_size_target,
+                           luda_job_result* res, void* stream) {
+  if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
+  memset(res, 0, sizeof(*res));
+  if (L > 32) return fail(LUDA_UNSUPPORTED, "user keys longer than 32 bytes");
+  if (restart_interval < 1) return fail(LUDA_DEVICE, "restart_interval must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch scratch(st);
+  // duplicates of a user key may share up to K-1 bytes → entry >= 4 B
+  EmitParams ep{L + 8, block_size, restart_interval, bits_per_key, sst_size_target, 4};
+  const uint32_t W = std::max<uint32_t>(1, (L + 7) / 8);
+  int rc;
+  switch (W) {
+    case 1: rc = build_w<1>(st, scratch, keys, L, trailers, values, voff, vlen, n, ep, res); break;
+    case 2: rc = build_w<2>(st, scratch, keys, L, trailers, values, voff, vlen, n, ep, res); break;
+    case 3: rc = build_w<3>(st, scratch, keys, L, trailers, values, voff, vlen, n, ep, res); break;
+    default: rc = build_w<4>(st, scratch, keys, L, trailers, values, voff, vlen, n, ep, res); break;
+  }
+  if (rc) luda_job_release(res);
+  return rc;
+}
+
+int luda_dispatch(int kind, const int64_t* items, uint32_t n_items, void* const* region_ptr,
+                  const uint64_t* region_cap, uint32_t n_regions, int64_t* results, int64_t* fail_item,
+                  void* stream) {
+  (void)kind; (void)items; (void)n_items; (void)region_ptr; (void)region_cap; (void)n_regions; (void)results;
+  (void)stream;
+  *fail_item = 0;
+  return fail(LUDA_DEVICE, "luda_dispatch: not implemented yet");
+}
+
+int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
+  if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
+  memset(res, 0, sizeof(*res));
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch scratch(st);
+  cudaEvent_t ev[8];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() { for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]); }
+  } evg{ev};
+  CK(cudaEventRecord(ev[0], st));
+  const uint32_t nf = jd->n_files;
+  if (nf == 0) return LUDA_OK;
+  if (jd->restart_interval < 1) return fail(LUDA_DEVICE, "restart_interval must be >= 1");
+  GET(d_faddr, uint64_t, nf, false);
+  GET(d_fsize, uint64_t, nf, false);
+  CK(cudaMemcpyAsync(d_faddr, jd->file_off, 8ull * nf, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_fsize, jd->file_len, 8ull * nf, cudaMemcpyHostToDevice, st));
+  GET(info, FileInfo, nf, false);
+  GET(caddr, uint64_t, 2ull * nf, false);
+  GET(clen, uint32_t, 2ull * nf, false);
+  GET(cstored, uint32_t, 2ull * nf, false);
+  GET(ccrc, uint32_t, 2ull * nf, false);
+  ParseArgs pa{jd->arena, d_faddr, d_fsize, nf, info, caddr, clen, cstored};
+  parse_files_a<<<(nf * 32 + 255) / 256, 256, 0, st>>>(pa);
+  CK(cudaGetLastError());
+  int rc = luda_crc32_batch(jd->arena, caddr, clen, 2 * nf, ccrc, st);
+  if (rc) return rc;
+  std::vector<FileInfo> hinfo(nf);
+  std::vector<uint32_t> hcrc(2 * nf), hst(2 * nf);
+  CK(cudaMemcpyAsync(hinfo.data(), info, sizeof(FileInfo) * nf, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hcrc.data(), ccrc, 8ull * nf, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hst.data(), cstored, 8ull * nf, cudaMemcpyDeviceToHost, st));
+  rc = sync(st);
+  if (rc) return rc;
+  // Reference order per file (Table.__init__), files in job order.
+  uint32_t K = 0xFFFFFFFEu;
+  bool mixed = false;
+  std::vector<uint32_t> fbb(nf + 1, 0);
+  for (uint32_t f = 0; f < nf; ++f) {
+    const FileInfo& fi = hinfo[f];
+    char buf[96];
+    if (fi.code == F_MAGIC) {
+      snprintf(buf, sizeof buf, "bad magic 0x%016llx", (unsigned long long)fi.magic);
+      return fail(LUDA_FORMAT, buf);
+    }
+    if (fi.code) return fail(LUDA_FORMAT, file_msg(fi.code));
+    if (hcrc[2 * f] != hst[2 * f]) return fail(LUDA_CORRUPT, "filter block checksum mismatch", (int64_t)fi.filter_off);
+    if (fi.kbad) {
+      snprintf(buf, sizeof buf, "bad probe count %u", fi.kbyte);
+      return fail(LUDA_FORMAT, buf);
+    }
+    if (fi.icode == F_INDEX_SHORT) return fail(LUDA_FORMAT, file_msg(fi.icode));
+    if (hcrc[2 * f + 1] != hst[2 * f + 1]) return fail(LUDA_CORRUPT, "index block checksum mismatch", (int64_t)fi.index_off);
+    if (fi.icode) return fail(LUDA_FORMAT, file_msg(fi.icode));
+    fbb[f + 1] = fbb[f] + fi.nblocks;
+    if (fi.nblocks) {
+      if (fi.klen == 0xFFFFFFFFu) mixed = true;
+      else if (K == 0xFFFFFFFEu) K = fi.klen;
+      else if (K != fi.klen) mixed = true;
+    }
+  }
+  const uint32_t nblk = fbb[nf];
+  if (nblk == 0) return LUDA_OK;  // no data blocks: empty output
+  if (mixed) return fail(LUDA_UNSUPPORTED, "keys of differing lengths in one job are not supported by the b200 fast path");
+  if (K < 8) return fail(LUDA_UNSUPPORTED, "internal keys shorter than the 8-byte trailer");
+  const uint32_t L = K - 8;
+  if (L > 32) return fail(LUDA_UNSUPPORTED, "user keys longer than 32 bytes are not supported by the b200 fast path");
+  GET(d_fbb, uint32_t, nf + 1, false);
+  CK(cudaMemcpyAsync(d_fbb, fbb.data(), 4ull * (nf + 1), cudaMemcpyHostToDevice, st));
+  BlockTable bt{};
+  {
+    GET(a_, uint64_t, nblk, false);
+    GET(l_, uint32_t, nblk, false);
+    GET(o_, uint32_t, nblk, false);
+    GET(f_, uint32_t, nblk, false);
+    bt = BlockTable{a_, l_, o_, f_};
+  }
+  GET(bound, unsigned long long, 1, true);
+  parse_files_c<<<(nf * 32 + 255) / 256, 256, 0, st>>>(pa, d_fbb, bt, std::max<uint32_t>(jd->restart_interval, 16),
+                                                       bound);
+  CK(cudaGetLastError());
+  unsigned long long hbound = 0;
+  CK(cudaMemcpyAsync(&hbound, bound, 8, cudaMemcpyDeviceToHost, st));
+  rc = sync(st);
+  if (rc) return rc;
+  const uint32_t W = std::max<uint32_t>(1, (L + 7) / 8);
+  CK(cudaEventRecord(ev[1], st));
+  cudaEvent_t* pev = ev;
+  switch (W) {
+    case 1: rc = compact_w<1>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
+    case 2: rc = compact_w<2>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
+    case 3: rc = compact_w<3>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
+    default: rc = compact_w<4>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
+  }
+  if (rc) {
+    luda_job_release(res);
+    return rc;
+  }
+  CK(cudaEventRecord(ev[7], st));
+  CK(cudaEventSynchronize(ev[7]));
+  // t_ms: [0] parse, [1] decode, [2] merge, [3] plan, [4] emit, [7] total
+  if (res->n_out) {
+    for (int i = 0; i < 5; ++i) res->t_ms[i] = ev_ms(ev[i], ev[i + 1]);
+  }
+  res->t_ms[7] = ev_ms(ev[0], ev[7]);
+  return LUDA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,331 @@
+// luda_decode.cuh — data-block decode: CRC verify + entry parse → records.
+//
+// Restates decode_data_block (blocks.py:130-165) for every data block listed
+// by the index blocks (Table.scan, sst.py:370-375), and the `unpack` kernel
+// work item (kernels.py:72-104), except that it emits fixed-width sort
+// records (luda_rec.cuh) with a value HANDLE instead of copying values.
+//
+// One warp per block, blocks taken in order from a global counter:
+//  1. stage the 16-byte-aligned window of the block into the warp's smem
+//     buffer (coalesced 16 B loads), blocks > kDecStageBytes are read in place;
+//  2. phase 1 — count entries. Fast path: lane k walks restart interval k
+//     (restart offsets from the block tail) and the walk is accepted only if
+//     every interval starts with shared == 0 and ends exactly on the next
+//     restart offset; then the sequential reference parse passes through the
+//     same entry boundaries and yields identical keys. Otherwise lane 0 runs
+//     the exact sequential reference parse (errors included);
+//  3. decoupled look-back over block order gives the block's first record
+//     index (single pass, no count kernel);
+//  4. warp CRC-32 of the payload (end-aligned segments, luda_common.cuh);
+//  5. phase 2 — lanes take consecutive entries; each loads its key suffix and
+//     the prefix bytes it shares are filled from earlier lanes by a
+//     Hillis-Steele scan over "valid-from" byte positions (shuffles only);
+//     records are written coalesced (lane i → record base+i).
+// Errors: reference errors → min((block << 8) | code) in err_ref; inputs that
+// are valid for the reference but outside the fixed-key-length envelope →
+// err_unsup (host raises those only if no reference error exists).
+#pragma once
+#include "luda_parse.cuh"
+#include "luda_rec.cuh"
+
+namespace luda {
+
+enum BlockCode : uint32_t {
+  B_OK = 0,
+  B_SHORT = 1,          // block too short
+  B_CRC = 2,            // data block checksum mismatch
+  B_RESTART = 3,        // bad restart array
+  B_VARINT_TRUNC = 4,   // truncated varint
+  B_VARINT_LONG = 5,    // varint too long
+  B_TRUNC_ENTRY = 6,    // truncated block entry
+  B_TRAILING = 7,       // trailing garbage in block entries
+  B_KEYLEN = 8,         // (unsupported) key length differs from the job's K
+  B_VALUE_BIG = 9,      // (unsupported) value length >= 2^24 or arena offset >= 2^40
+};
+
+constexpr int kDecWarps = 16;
+constexpr int kDecStageBytes = 8192;
+constexpr int kDecPre = 160;
+constexpr int kDecBuf = kDecPre + kDecStageBytes + 64;
+constexpr int kDecSlots = 256;
+constexpr int kDecWarpBytes = kDecBuf + kDecSlots * 8;
+
+struct DecSlot {
+  uint32_t pos;  // block-relative offset of the key suffix
+  uint32_t sv;   // value_len << 8 | shared
+};
+
+template <int W>
+struct DecodeArgs {
+  const uint8_t* arena;
+  BlockTable bt;
+  uint32_t nblk;
+  uint32_t K;               // internal key length of the job
+  Rec<W>* out;
+  uint64_t cap;
+  uint64_t* lb;             // look-back status per block (zeroed)
+  unsigned int* tile_ctr;   // zeroed
+  uint64_t* blk_base;       // [nblk+1] first record index of each block
+  unsigned long long* err_ref;
+  unsigned long long* err_unsup;
+};
+
+// Walk one restart interval [start, end) under fast-path rules; calls
+// emit(j, pos_suffix, shared, vlen) per entry; returns entry count or -1.
+template <typename Emit>
+__device__ __forceinline__ int64_t interval_walk(const uint8_t* d, uint64_t start, uint64_t end, uint32_t K,
+                                                 Emit emit) {
+  uint64_t pos = start;
+  int64_t j = 0;
+  while (pos < end) {
+    uint64_t s, u, vl;
+    if (varint_read(d, end, pos, s) || varint_read(d, end, pos, u) || varint_read(d, end, pos, vl)) return -1;
+    if (j == 0 ? s != 0 : s > K) return -1;
+    if (u != (uint64_t)K - s || vl > kMaxValueLen) return -1;
+    if (u > end || vl > end || pos + u + vl > end) return -1;
+    emit(j, (uint32_t)pos, (uint32_t)s, (uint32_t)vl);
+    pos += u + vl;
+    ++j;
+  }
+  return pos == end ? j : -1;
+}
+
+// Exact sequential decode_data_block walk (blocks.py:151-164). Returns the
+// reference error code (0 ok) and sets `unsup` for envelope violations.
+template <typename Emit>
+__device__ uint32_t block_walk_exact(const uint8_t* d, uint64_t payload, uint64_t entries_end, uint32_t K,
+                                     uint64_t& n_out, uint32_t& unsup, Emit emit) {
+  uint64_t pos = 0, prev_len = 0, n = 0;
+  unsup = 0;
+  while (pos < entries_end) {
+    uint64_t s, u, vl;
+    int r;
+    if ((r = varint_read(d, payload, pos, s)) || (r = varint_read(d, payload, pos, u)) ||
+        (r = varint_read(d, payload, pos, vl))) {
+      n_out = n;
+      return r == 1 ? B_VARINT_TRUNC : B_VARINT_LONG;
+    }
+    if (s > prev_len || u > entries_end || vl > entries_end || pos + u + vl > entries_end) {
+      n_out = n;
+      return B_TRUNC_ENTRY;
+    }
+    if (s + u != K) unsup = unsup ? unsup : B_KEYLEN;
+    if (vl > kMaxValueLen) unsup = unsup ? unsup : B_VALUE_BIG;
+    emit(n, (uint32_t)pos, (uint32_t)s, (uint32_t)vl);
+    prev_len = s + u;
+    pos += u + vl;
+    ++n;
+  }
+  n_out = n;
+  return pos != entries_end ? B_TRAILING : B_OK;
+}
+
+template <int W>
+__device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_t b, uint8_t* wbuf,
+                                                 DecSlot* slots, const CrcSmem& cs) {
+  constexpr int NW = 2 * W + 2;
+  const uint32_t lane = lane_id();
+  const uint32_t len = a.bt.len[b];
+  const uint64_t addr = a.bt.addr[b];
+  const uint32_t K = a.K;
+  const bool staged = len <= (uint32_t)kDecStageBytes;
+  const uint8_t* g = a.arena + addr;
+  const uint8_t* d = g;
+  if (len >= 12 && staged) {
+    const uintptr_t w0 = reinterpret_cast<uintptr_t>(g) & ~uintptr_t(15);
+    const uintptr_t w1 = (reinterpret_cast<uintptr_t>(g) + len + 15) & ~uintptr_t(15);
+    const uint32_t nch = (uint32_t)((w1 - w0) >> 4);
+    uint4* dst = reinterpret_cast<uint4*>(wbuf + kDecPre);
+    for (uint32_t c = lane; c < nch; c += 32) dst[c] = *reinterpret_cast<const uint4*>(w0 + 16ull * c);
+    __syncwarp();
+    d = wbuf + kDecPre + (reinterpret_cast<uintptr_t>(g) & 15);
+  }
+  uint32_t code = len < 12 ? (uint32_t)B_SHORT : 0u;
+  uint32_t nres = 0;
+  int64_t entries_end = 0;
+  bool restart_bad = false;
+  if (!code) {
+    nres = ld_u32_le(d + len - 8);
+    entries_end = (int64_t)len - 8 - 4 * (int64_t)nres;
+    restart_bad = nres < 1 || entries_end < 0;
+  }
+  // ---- phase 1: count -------------------------------------------------------
+  bool fast = false;
+  uint64_t n = 0;
+  uint32_t pcode = 0, unsup = 0;
+  int64_t my_cnt = 0, my_pre = 0;  // fast path: this lane's interval (lane < nres)
+  if (!code && !restart_bad) {
+    if (nres <= 32) {
+      bool ok = true;
+      if (lane < nres) {
+        const uint64_t st = ld_u32_le(d + entries_end + 4 * lane);
+        const uint64_t en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint64_t)entries_end;
+        ok = (lane != 0 || st == 0) && st < en && en <= (uint64_t)entries_end;
+        if (ok) {
+          my_cnt = interval_walk(d, st, en, K, [](int64_t, uint32_t, uint32_t, uint32_t) {});
+          ok = my_cnt >= 0;
+        }
+      }
+      fast = __all_sync(0xFFFFFFFFu, ok);
+    }
+    if (fast) {
+      const int64_t incl = warp_incl_scan<int64_t>(lane < nres ? my_cnt : 0);
+      my_pre = incl - (lane < nres ? my_cnt : 0);
+      n = (uint64_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
+    } else {
+      uint64_t nn = 0;
+      uint32_t pc = 0, us = 0;
+      if (lane == 0)
+        pc = block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us,
+                              [](uint64_t, uint32_t, uint32_t, uint32_t) {});
+      n = __shfl_sync(0xFFFFFFFFu, nn, 0);
+      pcode = __shfl_sync(0xFFFFFFFFu, pc, 0);
+      unsup = __shfl_sync(0xFFFFFFFFu, us, 0);
+    }
+  }
+  // ---- look-back: first record index of this block --------------------------
+  if (lane == 0) lb_publish(a.lb, b, kLbAgg, n);
+  const uint64_t excl = lb_exclusive(a.lb, b);
+  if (lane == 0) {
+    lb_publish(a.lb, b, kLbInc, excl + n);
+    a.blk_base[b] = excl;
+    if (b + 1 == a.nblk) a.blk_base[a.nblk] = excl + n;
+  }
+  // ---- CRC ------------------------------------------------------------------
+  if (!code) {
+    uint32_t crc;
+    if (staged) {
+      crc = warp_crc32_smem(d, len - 4, cs);
+    } else {
+      const uint64_t np = ((uint64_t)len - 4 + kGroup - 1) / kGroup;
+      uint32_t raw = 0;
+      for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(g, len - 4, q, wbuf, cs);
+      crc = ~raw;
+    }
+    if (crc != ld_u32_le(d + len - 4)) code = B_CRC;
+    else if (restart_bad) code = B_RESTART;
+    else code = pcode;
+  }
+  if (code) {
+    if (lane == 0) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
+    return;
+  }
+  if (unsup) {
+    if (lane == 0) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | unsup);
+    return;
+  }
+  if (excl + n > a.cap) return;  // host re-runs with exact capacity
+  // ---- phase 2: records ------------------------------------------------------
+  const uint32_t L = K - 8;
+  uint32_t carry[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) carry[i] = 0;
+  for (uint64_t w0 = 0; w0 < n; w0 += kDecSlots) {
+    const uint64_t w1 = w0 + kDecSlots;
+    auto put = [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+      if (j >= w0 && j < w1) slots[j - w0] = DecSlot{pos, (vl << 8) | s};
+    };
+    if (fast) {
+      if (lane < nres) {
+        const uint64_t st = ld_u32_le(d + entries_end + 4 * lane);
+        const uint64_t en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint64_t)entries_end;
+        const int64_t pre = my_pre;
+        if ((uint64_t)(pre + my_cnt) > w0 && (uint64_t)pre < w1)
+          interval_walk(d, st, en, K, [&](int64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+            put((uint64_t)(pre + j), pos, s, vl);
+          });
+      }
+    } else if (lane == 0) {
+      uint64_t nn;
+      uint32_t us;
+      block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us, put);
+    }
+    __syncwarp();
+    const uint32_t wn = (uint32_t)((n - w0) < (uint64_t)kDecSlots ? (n - w0) : (uint64_t)kDecSlots);
+    for (uint32_t c0 = 0; c0 < wn; c0 += 32) {
+      const uint32_t e = c0 + lane;
+      const bool act = e < wn;
+      DecSlot sl = act ? slots[e] : DecSlot{0, 0};
+      const uint32_t s = sl.sv & 0xFFu;
+      const uint32_t vl = sl.sv >> 8;
+      uint32_t kw[NW];
+      {
+        const uint8_t* V = d + sl.pos - s;  // key byte i at V + i
+        const uintptr_t va = reinterpret_cast<uintptr_t>(V);
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(va & ~uintptr_t(3));
+        const uint32_t sh = (uint32_t)(va & 3u) * 8u;
+        uint32_t lo = act ? wp[0] : 0u;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          const uint32_t hi = act ? wp[i + 1] : 0u;
+          kw[i] = __funnelshift_r(lo, hi, sh);
+          lo = hi;
+        }
+      }
+      uint32_t v = act ? s : 0u;  // bytes [v, K) valid
+      if (lane == 0 && v) {
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          const int32_t bi = (int32_t)v - 4 * i;
+          const uint32_t keep = bi <= 0 ? 0xFFFFFFFFu : (bi >= 4 ? 0u : (0xFFFFFFFFu << (8 * bi)));
+          kw[i] = (kw[i] & keep) | (carry[i] & ~keep);
+        }
+        v = 0;
+      }
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        if (!__any_sync(0xFFFFFFFFu, v != 0)) break;
+        const uint32_t ov = __shfl_up_sync(0xFFFFFFFFu, v, dd);
+        uint32_t ow[NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) ow[i] = __shfl_up_sync(0xFFFFFFFFu, kw[i], dd);
+        if (lane >= (uint32_t)dd && v) {
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            const int32_t bi = (int32_t)v - 4 * i;
+            const uint32_t keep = bi <= 0 ? 0xFFFFFFFFu : (bi >= 4 ? 0u : (0xFFFFFFFFu << (8 * bi)));
+            kw[i] = (kw[i] & keep) | (ow[i] & ~keep);
+          }
+          v = ov < v ? ov : v;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NW; ++i) carry[i] = __shfl_sync(0xFFFFFFFFu, kw[i], 31);
+      if (act) {
+        Rec<W> r;
+        words_to_rec<W, NW>(kw, L, r);
+        const uint64_t voff = addr + sl.pos + (K - s);
+        r.h = handle_pack(voff, vl);
+        a.out[excl + w0 + e] = r;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W> a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
+  uint8_t* wbuf = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kDecWarpBytes;
+  DecSlot* slots = reinterpret_cast<DecSlot*>(wbuf + kDecBuf);
+  crc_smem_init(cs);
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  while (true) {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(a.tile_ctr, 1u);
+    b = __shfl_sync(0xFFFFFFFFu, b, 0);
+    if (b >= a.nblk) break;
+    decode_one_block<W>(a, b, wbuf, slots, cs);
+  }
+}
+
+// First record index of every file (gathered from the block bases).
+__global__ void file_entry_base_kernel(const uint64_t* blk_base, const uint32_t* file_blk_base, uint32_t nfiles,
+                                       uint64_t* out) {
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f <= nfiles) out[f] = blk_base[file_blk_base[f]];
+}
+
+}  // namespace luda

@@ -1,0 +1,389 @@
+// luda_encode.cuh — output SST emission.
+//
+// encode_kernel (warp per data block) restates assemble_block
+// (blocks.py:77-103) + compute_layouts (blocks.py:41-58) — the reference's
+// `shared_key` and `encode` kernel items (kernels.py:107-155) fused:
+//   entry = varint shared ∥ varint unshared ∥ varint value_len ∥ key[shared:] ∥ value
+//   shared = LCP with the previous key, 0 at i % restart_interval == 0
+//   block = entries ∥ u32le restart offsets ∥ u32le n_restarts ∥ u32le crc
+// Lanes take 32 consecutive entries: sizes → warp scan → offsets; headers and
+// key suffixes are written by their lane, values are gathered straight from
+// the staged input SSTs by the whole warp (one copy; the reference copies
+// twice). The block is assembled in shared memory at the
+// same 16-byte phase as its destination, CRC'd there and streamed out with
+// 16-byte stores. Blocks larger than kEncStage are written in place.
+//
+// sst_meta_kernel (CTA per output SST) builds the filter block
+// (bloom.py:71-88 + FilterBlock.encode :53-55: h = crc32(user_key),
+// delta = rotr(h, 17), bit (h + j*delta) mod n_bits for j < k, atomicOr into
+// a shared bit array), the index block (sst.py:67-76) and the footer
+// (sst.py:206-208).
+#pragma once
+#include "luda_parse.cuh"
+#include "luda_plan.cuh"
+#include "luda_rec.cuh"
+
+namespace luda {
+
+constexpr int kEncWarps = 16;
+constexpr int kEncStage = 8192;
+constexpr int kEncPre = 160;
+constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
+
+// Copy n bytes src → dst (any alignment; dst generic: smem or global) with
+// `nl` cooperating threads (rank `r`). Destination-aligned 32-bit words are
+// assembled from two aligned source words; partial edge words are written
+// bytewise so neighbouring data is never touched. src window [src-3, src+n+4)
+// must be readable.
+__device__ __forceinline__ void coop_copy(uint8_t* dst, const uint8_t* src, uint64_t n, uint32_t r, uint32_t nl) {
+  if (n == 0) return;
+  const uintptr_t da = reinterpret_cast<uintptr_t>(dst);
+  const uintptr_t w0 = da & ~uintptr_t(3);
+  const uintptr_t w1 = (da + n + 3) & ~uintptr_t(3);
+  const uint64_t nw = (w1 - w0) >> 2;
+  const intptr_t delta = reinterpret_cast<intptr_t>(src) - (intptr_t)da;
+  for (uint64_t w = r; w < nw; w += nl) {
+    const uintptr_t A = w0 + 4 * w;
+    const uintptr_t sA = (uintptr_t)((intptr_t)A + delta);
+    const uint32_t* sp = reinterpret_cast<const uint32_t*>(sA & ~uintptr_t(3));
+    const uint32_t v = __funnelshift_r(sp[0], sp[1], (uint32_t)(sA & 3u) * 8u);
+    if (A >= da && A + 4 <= da + n) {
+      *reinterpret_cast<uint32_t*>(A) = v;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (A + b >= da && A + b < da + n) reinterpret_cast<uint8_t*>(A)[b] = (uint8_t)(v >> (8 * b));
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t put_varint(uint8_t* p, uint64_t v) {
+  uint32_t n = 0;
+  while (v >= 0x80) { p[n++] = (uint8_t)(v | 0x80); v >>= 7; }
+  p[n++] = (uint8_t)v;
+  return n;
+}
+
+__device__ __forceinline__ void put_u32(uint8_t* p, uint32_t v) {
+  p[0] = (uint8_t)v; p[1] = (uint8_t)(v >> 8); p[2] = (uint8_t)(v >> 16); p[3] = (uint8_t)(v >> 24);
+}
+
+// Write bytes [from, K) of the internal key of r to p[0..).
+template <int W>
+__device__ __forceinline__ void put_key_tail(uint8_t* p, const Rec<W>& r, uint32_t L, uint32_t from) {
+  constexpr int KMAX = 8 * W + 8;
+  const uint64_t tr = ~r.t;
+#pragma unroll
+  for (int j = 0; j < KMAX; ++j) {
+    if ((uint32_t)j >= from && (uint32_t)j < L + 8) {
+      uint32_t byte;
+      if ((uint32_t)j < L) byte = (uint32_t)(r.k[j >> 3] >> (56 - 8 * (j & 7))) & 0xFFu;
+      else byte = (uint32_t)(tr >> (8 * (j - L))) & 0xFFu;
+      p[j - from] = (uint8_t)byte;
+    }
+  }
+}
+
+// CRC of one pass over smem data (un-shifted, warp-reduced raw register).
+__device__ __forceinline__ uint32_t warp_pass_raw_smem(const uint8_t* data, uint32_t n, int64_t q, const CrcSmem& cs) {
+  const uint32_t lane = lane_id();
+  const int64_t nseg = ((int64_t)n + kSeg - 1) / kSeg;
+  const int64_t d = (int64_t)lane + 32 * q;
+  uint32_t r = 0;
+  if (d < nseg) {
+    const int64_t start = (int64_t)n - (int64_t)kSeg * (d + 1);
+    r = seg_crc_smem(data + start, start, cs.tab + lane);
+  }
+  r = seg_shift(r, cs.nib + lane);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r ^= __shfl_xor_sync(0xFFFFFFFFu, r, o);
+  return r;
+}
+
+// CTA-wide CRC-32 of smem data (passes spread over warps). All threads call;
+// returns the CRC in every thread. `red` = smem scratch of >= 32 words.
+__device__ __forceinline__ uint32_t cta_crc32_smem(const uint8_t* data, uint32_t n, const CrcSmem& cs, uint32_t* red) {
+  const uint32_t nwarps = blockDim.x >> 5, wid = threadIdx.x >> 5;
+  uint32_t acc = 0;
+  if (n < 4) {
+    if (threadIdx.x == 0) red[0] = crc32_bytes(data, n, cs.tab);
+    __syncthreads();
+    const uint32_t v = red[0];
+    __syncthreads();
+    return v;
+  }
+  const int64_t npass = ((int64_t)n + kGroup - 1) / kGroup;
+  for (int64_t q = wid; q < npass; q += nwarps) acc ^= crc_shift(warp_pass_raw_smem(data, n, q, cs), (uint64_t)kGroup * q);
+  if (lane_id() == 0) red[wid] = acc;
+  __syncthreads();
+  uint32_t v = 0;
+  for (uint32_t w = 0; w < nwarps; ++w) v ^= red[w];
+  __syncthreads();
+  return ~v;
+}
+
+// CTA-wide CRC-32 of a global range, staging passes through per-warp smem.
+__device__ __forceinline__ uint32_t cta_crc32_global(const uint8_t* g, uint64_t n, const CrcSmem& cs, uint8_t* stage,
+                                                     uint32_t* red) {
+  const uint32_t nwarps = blockDim.x >> 5, wid = threadIdx.x >> 5;
+  if (n < 4) {
+    if (threadIdx.x == 0) red[0] = crc32_bytes(g, (uint32_t)n, cs.tab);
+    __syncthreads();
+    const uint32_t v = red[0];
+    __syncthreads();
+    return v;
+  }
+  uint32_t acc = 0;
+  const uint64_t npass = (n + kGroup - 1) / kGroup;
+  uint8_t* my = stage + wid * (kGroup + 192);
+  for (uint64_t q = wid; q < npass; q += nwarps) acc ^= warp_crc_pass_global(g, n, q, my, cs);
+  if (lane_id() == 0) red[wid] = acc;
+  __syncthreads();
+  uint32_t v = 0;
+  for (uint32_t w = 0; w < nwarps; ++w) v ^= red[w];
+  __syncthreads();
+  return ~v;
+}
+
+template <int W>
+struct EncodeArgs {
+  const uint8_t* arena;
+  const Rec<W>* rec;
+  uint32_t K;
+  uint32_t ri;
+  uint32_t nblk;
+  const uint32_t* blk_first;
+  const uint32_t* blk_n;
+  const uint32_t* blk_size;
+  const uint64_t* blk_pos;
+  const uint32_t* sst_first_blk;
+  uint32_t nsst;
+  const uint64_t* sst_off;
+  uint8_t* out;
+};
+
+template <int W>
+__device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_t k, uint8_t* wbuf, const CrcSmem& cs) {
+  const uint32_t lane = lane_id();
+  const uint64_t first = a.blk_first[k];
+  const uint32_t cnt = a.blk_n[k];
+  const uint32_t size = a.blk_size[k];
+  const uint32_t K = a.K, L = K - 8, ri = a.ri;
+  // owning SST: last s with sst_first_blk[s] <= k
+  uint32_t lo = 0, hi = a.nsst;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a.sst_first_blk[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  const uint64_t out_off = a.sst_off[lo] + (a.blk_pos[k] - a.blk_pos[a.sst_first_blk[lo]]);
+  const uint32_t nres = (cnt + ri - 1) / ri;
+  const uint32_t entries_end = size - 8 - 4 * nres;
+  const bool staged = size <= (uint32_t)kEncStage;
+  uint8_t* sbase = wbuf + kEncPre;
+  uint8_t* dst = staged ? sbase + (out_off & 15) : a.out + out_off;
+  uint32_t carry = 0;
+  for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
+    const uint32_t i = c0 + lane;
+    const bool act = i < cnt;
+    Rec<W> r;
+    if (act) r = a.rec[first + i];
+    uint32_t s = 0, u = 0, vl = 0, hv = 0, esz = 0;
+    uint64_t voff = 0;
+    if (act) {
+      if (i % ri != 0) s = ikey_lcp(a.rec[first + i - 1], r, L);
+      u = K - s;
+      vl = handle_len(r.h);
+      voff = handle_off(r.h);
+      hv = varint_size(s) + varint_size(u) + varint_size(vl);
+      esz = hv + u + vl;
+    }
+    const uint32_t incl = warp_incl_scan<uint32_t>(esz);
+    const uint32_t off = carry + incl - esz;
+    carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (act) {
+      uint8_t* p = dst + off;
+      uint32_t h = put_varint(p, s);
+      h += put_varint(p + h, u);
+      h += put_varint(p + h, vl);
+      put_key_tail<W>(p + h, r, L, s);
+      if (i % ri == 0) put_u32(dst + entries_end + 4 * (i / ri), off);
+    }
+    // values: whole warp per entry
+    const uint32_t nact = cnt - c0 < 32 ? cnt - c0 : 32;
+    for (uint32_t j = 0; j < nact; ++j) {
+      const uint64_t so = __shfl_sync(0xFFFFFFFFu, voff, j);
+      const uint32_t sl = __shfl_sync(0xFFFFFFFFu, vl, j);
+      const uint32_t dp = __shfl_sync(0xFFFFFFFFu, off + hv + u, j);
+      coop_copy(dst + dp, a.arena + so, sl, lane, 32);
+    }
+  }
+  if (lane == 0) put_u32(dst + entries_end + 4 * nres, nres);
+  __syncwarp();
+  uint32_t crc;
+  if (staged) {
+    crc = warp_crc32_smem(dst, size - 4, cs);
+  } else {
+    __threadfence();
+    __syncwarp();
+    const uint64_t np = ((uint64_t)size - 4 + kGroup - 1) / kGroup;
+    uint32_t raw = 0;
+    for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(dst, size - 4, q, wbuf, cs);
+    crc = ~raw;
+  }
+  if (lane == 0) put_u32(dst + size - 4, crc);
+  __syncwarp();
+  if (staged) {
+    const uintptr_t g = reinterpret_cast<uintptr_t>(a.out + out_off);
+    const uintptr_t g0 = g & ~uintptr_t(15), g1 = (g + size + 15) & ~uintptr_t(15);
+    const uint32_t nch = (uint32_t)((g1 - g0) >> 4);
+    for (uint32_t c = lane; c < nch; c += 32) {
+      const uintptr_t A = g0 + 16ull * c;
+      const uint8_t* sp = sbase + 16 * c;
+      if (A >= g && A + 16 <= g + size) {
+        *reinterpret_cast<uint4*>(A) = *reinterpret_cast<const uint4*>(sp);
+      } else {
+        for (int b = 0; b < 16; ++b)
+          if (A + b >= g && A + b < g + size) reinterpret_cast<uint8_t*>(A)[b] = sp[b];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int W>
+__global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W> a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
+  uint8_t* wbuf = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kEncBuf;
+  crc_smem_init(cs);
+  __syncthreads();
+  const uint32_t gw = blockIdx.x * kEncWarps + (threadIdx.x >> 5);
+  const uint32_t nw = gridDim.x * kEncWarps;
+  for (uint32_t k = gw; k < a.nblk; k += nw) encode_one_block<W>(a, k, wbuf, cs);
+}
+
+// ---- per-SST filter + index + footer -----------------------------------------------------
+constexpr int kMetaThreads = 256;
+constexpr int kMetaBuf = 48 * 1024;
+constexpr int kMetaSmem = (int)sizeof(CrcSmem) + kEncPre + kMetaBuf + 64;
+
+template <int W>
+struct MetaArgs {
+  const Rec<W>* rec;
+  uint32_t K;
+  uint32_t bits_per_key;
+  uint32_t kprobes;
+  uint32_t nsst;
+  const uint32_t* sst_first_blk;
+  const uint32_t* sst_last_blk;
+  const uint64_t* sst_off;
+  const uint64_t* sst_data;
+  const uint64_t* sst_nent;
+  const uint64_t* sst_size;
+  const uint32_t* blk_first;
+  const uint32_t* blk_n;
+  const uint32_t* blk_size;
+  const uint64_t* blk_pos;
+  uint8_t* out;
+  uint32_t* scratch;           // zeroed, for filters larger than kMetaBuf
+  const uint64_t* scratch_off; // per SST word offset into scratch (or ~0)
+  uint8_t* sst_keys;           // [nsst][2][K]
+};
+
+template <int W>
+__global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
+  uint8_t* buf = smem_raw + sizeof(CrcSmem) + kEncPre;  // 16-aligned, 160 B lead-in
+  __shared__ uint32_t red[32];
+  crc_smem_init(cs);
+  const uint32_t s = blockIdx.x;
+  const uint32_t tid = threadIdx.x, lane = lane_id();
+  const uint32_t K = a.K, L = K - 8;
+  const uint32_t fb = a.sst_first_blk[s], eb = a.sst_last_blk[s];
+  const uint64_t fe = a.blk_first[fb];
+  const uint64_t ne = a.sst_nent[s];
+  const uint64_t data = a.sst_data[s];
+  uint8_t* fout = a.out + a.sst_off[s];
+  uint64_t nbits = ne * a.bits_per_key;
+  if (nbits < 64) nbits = 64;
+  nbits = (nbits + 7) & ~7ull;
+  const uint64_t nbytes = nbits / 8;
+  const bool small = nbytes + 1 <= (uint64_t)kMetaBuf;
+  uint32_t* bits = small ? reinterpret_cast<uint32_t*>(buf) : a.scratch + a.scratch_off[s];
+  if (small)
+    for (uint32_t i = tid; i < (nbytes + 1 + 3) / 4; i += kMetaThreads) bits[i] = 0;
+  __syncthreads();
+  // ---- bloom bits ----
+  const uint32_t* tl = cs.tab + lane;
+  for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
+    const Rec<W> r = a.rec[e];
+    uint32_t c = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 8 * W; ++j)
+      if ((uint32_t)j < L) c = crc_byte(c, (uint32_t)(r.k[j >> 3] >> (56 - 8 * (j & 7))) & 0xFFu, tl);
+    const uint32_t h = ~c;
+    const uint32_t delta = (h >> 17) | (h << 15);
+    const uint64_t nb64 = nbits;
+    uint64_t p = (uint64_t)h % nb64;
+    const uint64_t step = (uint64_t)delta % nb64;
+    for (uint32_t j = 0; j < a.kprobes; ++j) {
+      atomicOr(bits + (p >> 5), 1u << (p & 31));
+      p += step;
+      if (p >= nb64) p -= nb64;
+    }
+  }
+  __syncthreads();
+  // ---- filter block: bits ∥ k ∥ crc ----
+  uint8_t* fb8 = reinterpret_cast<uint8_t*>(bits);
+  if (tid == 0) fb8[nbytes] = (uint8_t)a.kprobes;
+  __syncthreads();
+  const uint32_t fcrc = small ? cta_crc32_smem(fb8, (uint32_t)(nbytes + 1), cs, red)
+                              : cta_crc32_global(fb8, nbytes + 1, cs, buf, red);
+  coop_copy(fout + data, fb8, nbytes + 1, tid, kMetaThreads);
+  if (tid == 0) put_u32(fout + data + nbytes + 1, fcrc);
+  __syncthreads();
+  // ---- index block ----
+  const uint64_t flen = nbytes + 5;
+  const uint32_t vK = varint_size(K);
+  const uint64_t E = vK + K + 8;
+  const uint32_t nb = eb - fb;
+  const uint64_t ibody = (uint64_t)nb * E + 4;  // entries ∥ count
+  const bool ismall = ibody <= (uint64_t)kMetaBuf;
+  uint8_t* ib = ismall ? buf : fout + data + flen;
+  for (uint32_t i = tid; i < nb; i += kMetaThreads) {
+    const uint32_t b = fb + i;
+    uint8_t* p = ib + (uint64_t)i * E;
+    put_varint(p, K);
+    const Rec<W> last = a.rec[(uint64_t)a.blk_first[b] + a.blk_n[b] - 1];
+    put_key_tail<W>(p + vK, last, L, 0);
+    put_u32(p + vK + K, (uint32_t)(a.blk_pos[b] - a.blk_pos[fb]));
+    put_u32(p + vK + K + 4, a.blk_size[b]);
+  }
+  if (tid == 0) put_u32(ib + (uint64_t)nb * E, nb);
+  __syncthreads();
+  if (!ismall) __threadfence();
+  __syncthreads();
+  const uint32_t icrc = ismall ? cta_crc32_smem(ib, (uint32_t)ibody, cs, red)
+                               : cta_crc32_global(ib, ibody, cs, buf, red);
+  if (ismall) coop_copy(fout + data + flen, ib, ibody, tid, kMetaThreads);
+  if (tid == 0) {
+    put_u32(fout + data + flen + ibody, icrc);
+    // footer <IIIIQ>: filter_off, filter_len, index_off, index_len, magic
+    uint8_t* ft = fout + a.sst_size[s] - 24;
+    put_u32(ft, (uint32_t)data);
+    put_u32(ft + 4, (uint32_t)flen);
+    put_u32(ft + 8, (uint32_t)(data + flen));
+    put_u32(ft + 12, (uint32_t)(ibody + 4));
+    put_u32(ft + 16, (uint32_t)kMagic);
+    put_u32(ft + 20, (uint32_t)(kMagic >> 32));
+  }
+  // smallest / largest internal keys
+  if (tid < 2 && ne > 0) {
+    const Rec<W> r = a.rec[tid == 0 ? fe : fe + ne - 1];
+    put_key_tail<W>(a.sst_keys + ((uint64_t)s * 2 + tid) * K, r, L, 0);
+  }
+}
+
+}  // namespace luda

@@ -1,0 +1,314 @@
+// luda_parse.cuh — SST footer / filter / index parsing and range CRCs.
+//
+// Restates Table.__init__ (sst.py:284-310): footer (last 24 B, <IIIIQ>),
+// magic, FilterBlock.decode (bloom.py:57-68: len >= 6, crc, 1 <= k <= 30) and
+// decode_index_block (sst.py:79-102: len >= 8, crc, n entries of
+// varint klen ∥ key ∥ u32 off ∥ u32 len, no trailing bytes). os.pread short
+// reads past EOF are reproduced by clamping every (off, len) to the file.
+//
+// Stage A (parse_files_a): one warp per file records every reference check
+// outcome and the filter/index byte ranges whose CRCs stage B verifies; the
+// host then raises the first failure in reference order. Stage C
+// (parse_files_c) writes the data-block table (arena address, clamped length,
+// file offset, file index) for the decode stage.
+#pragma once
+#include "luda_common.cuh"
+
+namespace luda {
+
+constexpr uint64_t kMagic = 0x4C55444153535431ull;  // sst.py:42
+
+enum FileCode : uint32_t {
+  F_OK = 0,
+  F_SHORT = 1,          // file too short for footer
+  F_MAGIC = 2,          // bad magic
+  F_FILTER_SHORT = 3,   // filter block too short
+  F_FILTER_CRC = 4,     // filter block checksum mismatch (Corruption @ filter_off)
+  F_FILTER_K = 5,       // bad probe count
+  F_INDEX_SHORT = 6,    // index block too short
+  F_INDEX_CRC = 7,      // index block checksum mismatch (Corruption @ index_off)
+  F_IDX_VARINT_TRUNC = 8,
+  F_IDX_VARINT_LONG = 9,
+  F_IDX_TRUNC = 10,     // truncated index entry
+  F_IDX_TRAILING = 11,  // trailing garbage in index block
+};
+
+// Reference check order: code (short/magic/filter short) → filter crc → kbad →
+// icode == F_INDEX_SHORT → index crc → icode (parse). CRCs come from stage B.
+struct FileInfo {
+  uint32_t code;          // F_SHORT / F_MAGIC / F_FILTER_SHORT (stop everything)
+  uint32_t kbad;          // probe count byte outside [1, 30]
+  uint32_t icode;         // F_INDEX_SHORT or an index parse code
+  uint32_t nblocks;       // index entries (valid when parse ok)
+  uint32_t klen;          // common index key length; 0xFFFFFFFF if mixed
+  uint32_t kbyte;         // filter probe count byte
+  uint64_t filter_off, filter_len;  // clamped, file relative
+  uint64_t index_off, index_len;
+  uint64_t magic;
+};
+
+__device__ __forceinline__ uint32_t ld_u32_le(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+__device__ __forceinline__ uint64_t ld_u64_le(const uint8_t* p) {
+  return (uint64_t)ld_u32_le(p) | ((uint64_t)ld_u32_le(p + 4) << 32);
+}
+
+// varint.decode (varint.py:28-43) over buf[0,n). Returns 0 ok, 1 truncated,
+// 2 too long; values >= 2^64 saturate to ~0 (the reference then fails a
+// bounds check downstream, as a Python bigint would).
+__device__ __forceinline__ int varint_read(const uint8_t* buf, uint64_t n, uint64_t& pos, uint64_t& out) {
+  uint64_t v = 0;
+  int shift = 0;
+  bool big = false;
+  while (true) {
+    if (pos >= n) return 1;
+    uint32_t b = buf[pos++];
+    uint64_t part = (uint64_t)(b & 0x7F);
+    if (shift == 63 && part > 1) big = true;
+    if (shift < 64) v |= part << shift;
+    if (!(b & 0x80)) { out = big ? ~0ull : v; return 0; }
+    shift += 7;
+    if (shift > 63) return 2;
+  }
+}
+
+// Sequential decode_index_block walk. Emits entries through `emit(i, off, len)`.
+template <typename Emit>
+__device__ int index_walk(const uint8_t* body, uint64_t end, uint32_t n, uint32_t& klen_out, Emit emit) {
+  uint64_t pos = 0;
+  uint32_t klen0 = 0xFFFFFFFEu;
+  for (uint32_t i = 0; i < n; ++i) {
+    uint64_t kl;
+    int r = varint_read(body, end + 4, pos, kl);  // payload = body ∥ count
+    if (r == 1) return F_IDX_VARINT_TRUNC;
+    if (r == 2) return F_IDX_VARINT_LONG;
+    if (kl > end || pos + kl + 8 > end) return F_IDX_TRUNC;
+    if (klen0 == 0xFFFFFFFEu) klen0 = (uint32_t)kl;
+    else if (klen0 != (uint32_t)kl) klen0 = 0xFFFFFFFFu;
+    pos += kl;
+    emit(i, ld_u32_le(body + pos), ld_u32_le(body + pos + 4));
+    pos += 8;
+  }
+  if (pos != end) return F_IDX_TRAILING;
+  klen_out = klen0;
+  return F_OK;
+}
+
+// Fixed-stride fast path: every entry is a 1-byte varint klen == K0.
+// Returns true when the whole index verifies as such (then entries are at
+// i*E with E = 1 + K0 + 8).
+__device__ __forceinline__ bool index_fixed_stride(const uint8_t* body, uint64_t end, uint32_t n, uint32_t& K0) {
+  if (n == 0 || end == 0) return false;
+  const uint32_t k0 = body[0];
+  if (k0 >= 0x80) return false;
+  const uint64_t E = 1ull + k0 + 8ull;
+  if ((uint64_t)n * E != end) return false;
+  bool ok = true;
+  for (uint32_t i = lane_id(); i < n; i += 32) ok &= (body[(uint64_t)i * E] == k0);
+  ok = __all_sync(0xFFFFFFFFu, ok);
+  K0 = k0;
+  return ok;
+}
+
+struct ParseArgs {
+  const uint8_t* arena;
+  const uint64_t* file_addr;  // device: arena offset of file i
+  const uint64_t* file_size;
+  uint32_t nfiles;
+  FileInfo* info;
+  uint64_t* crc_addr;  // 2 ranges per file: filter payload, index payload
+  uint32_t* crc_len;
+  uint32_t* crc_stored;
+};
+
+// Stage A: warp per file.
+__global__ void parse_files_a(ParseArgs a) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  if (warp >= a.nfiles) return;
+  const uint8_t* f = a.arena + a.file_addr[warp];
+  const uint64_t size = a.file_size[warp];
+  FileInfo fi{};
+  fi.klen = 0;
+  uint64_t crc_fa = 0, crc_ia = 0;
+  uint32_t crc_fl = 0, crc_il = 0, st_f = 0, st_i = 0;
+  do {
+    if (size < 24) { fi.code = F_SHORT; break; }
+    const uint8_t* ft = f + size - 24;
+    const uint64_t foff = ld_u32_le(ft), flen = ld_u32_le(ft + 4);
+    const uint64_t ioff = ld_u32_le(ft + 8), ilen = ld_u32_le(ft + 12);
+    fi.magic = ld_u64_le(ft + 16);
+    if (fi.magic != kMagic) { fi.code = F_MAGIC; break; }
+    const uint64_t fl = foff >= size ? 0 : (flen < size - foff ? flen : size - foff);
+    const uint64_t il = ioff >= size ? 0 : (ilen < size - ioff ? ilen : size - ioff);
+    fi.filter_off = foff; fi.filter_len = fl; fi.index_off = ioff; fi.index_len = il;
+    if (fl < 6) { fi.code = F_FILTER_SHORT; break; }
+    crc_fa = a.file_addr[warp] + foff; crc_fl = (uint32_t)(fl - 4); st_f = ld_u32_le(f + foff + fl - 4);
+    fi.kbyte = f[foff + fl - 5];
+    fi.kbad = (fi.kbyte < 1 || fi.kbyte > 30);
+    if (il < 8) { fi.icode = F_INDEX_SHORT; break; }
+    crc_ia = a.file_addr[warp] + ioff; crc_il = (uint32_t)(il - 4); st_i = ld_u32_le(f + ioff + il - 4);
+    const uint8_t* body = f + ioff;
+    const uint64_t end = il - 8;
+    const uint32_t n = ld_u32_le(body + end);
+    uint32_t K0 = 0;
+    if (index_fixed_stride(body, end, n, K0)) {
+      fi.nblocks = n;
+      fi.klen = K0;
+    } else {
+      uint32_t code = 0, kl = 0;
+      if (lane == 0) code = index_walk(body, end, n, kl, [](uint32_t, uint32_t, uint32_t) {});
+      code = __shfl_sync(0xFFFFFFFFu, code, 0);
+      kl = __shfl_sync(0xFFFFFFFFu, kl, 0);
+      fi.icode = code;
+      fi.nblocks = code ? 0 : n;
+      fi.klen = (n == 0) ? 0xFFFFFFFEu : kl;
+    }
+  } while (0);
+  if (lane == 0) {
+    a.info[warp] = fi;
+    a.crc_addr[2 * warp] = crc_fa; a.crc_len[2 * warp] = crc_fl; a.crc_stored[2 * warp] = st_f;
+    a.crc_addr[2 * warp + 1] = crc_ia; a.crc_len[2 * warp + 1] = crc_il; a.crc_stored[2 * warp + 1] = st_i;
+  }
+}
+
+// Warp CRC contribution of pass q (segments [32q, 32q+32) from the end) of
+// the n-byte range at global address g, staged through the warp's smem buffer
+// `stage` (>= kGroup + 160 bytes, 16-aligned). Returns Z_{4224 q}(raw part);
+// the XOR over all passes of a range is its raw register (preset folded in).
+__device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint64_t n, uint64_t q,
+                                                         uint8_t* stage, const CrcSmem& cs) {
+  const uint32_t lane = lane_id();
+  const int64_t hi = (int64_t)n - (int64_t)kGroup * (int64_t)q;          // pass end (data index)
+  const int64_t lo0 = hi - kGroup;
+  const int64_t lo = lo0 > -(int64_t)kSeg - 8 ? lo0 : -(int64_t)kSeg - 8;  // first segment starts > -132
+  // Stage data indices [lo - 8, hi + 8) into smem, keeping 16-byte phase.
+  // Only 16-byte granules that hold bytes of [0, n) are loaded (always
+  // mapped); the rest of the window is zero (those bytes are masked anyway).
+  const uintptr_t gA = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t w0 = (uintptr_t)((int64_t)gA + lo - 8) & ~uintptr_t(15);
+  const uintptr_t w1 = (uintptr_t)((int64_t)gA + hi + 8 + 15) & ~uintptr_t(15);
+  const uintptr_t l0 = gA & ~uintptr_t(15);
+  const uintptr_t l1 = (gA + n + 15) & ~uintptr_t(15);
+  const uint32_t nchunks = (uint32_t)((w1 - w0) >> 4);
+  for (uint32_t c = lane; c < nchunks; c += 32) {
+    const uintptr_t ad = w0 + 16ull * c;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (ad >= l0 && ad < l1) v = *reinterpret_cast<const uint4*>(ad);
+    reinterpret_cast<uint4*>(stage)[c] = v;
+  }
+  __syncwarp();
+  const uint8_t* base = stage + ((uintptr_t)((int64_t)gA + lo) - w0);  // smem addr of data index lo
+  const int64_t nseg = ((int64_t)n + kSeg - 1) / kSeg;
+  const int64_t d = (int64_t)lane + 32 * (int64_t)q;
+  uint32_t r = 0;
+  if (d < nseg) {
+    const int64_t start = (int64_t)n - (int64_t)kSeg * (d + 1);
+    r = seg_crc_smem(base + (start - lo), start, cs.tab + lane);
+  }
+  r = seg_shift(r, cs.nib + lane);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r ^= __shfl_xor_sync(0xFFFFFFFFu, r, o);
+  __syncwarp();
+  return crc_shift(r, (uint64_t)kGroup * q);
+}
+
+// Stage B: CRC of many ranges; warp per range, looping passes. out[i] = crc.
+// Ranges with length < 4 are done by lane 0 bytewise.
+constexpr int kCrcWarps = 8;
+__global__ void __launch_bounds__(kCrcWarps * 32) crc_ranges_kernel(const uint8_t* arena, const uint64_t* addr,
+                                                                   const uint32_t* len, uint32_t nranges,
+                                                                   uint32_t* out) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
+  uint8_t* stage = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * (kGroup + 192);
+  crc_smem_init(cs);
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint32_t nw = gridDim.x * kCrcWarps;
+  for (uint32_t r = blockIdx.x * kCrcWarps + (threadIdx.x >> 5); r < nranges; r += nw) {
+    const uint8_t* g = arena + addr[r];
+    const uint64_t n = len[r];
+    uint32_t acc = 0;
+    if (n < 4) {
+      if (lane == 0) acc = crc32_bytes(g, (uint32_t)n, cs.tab);
+    } else {
+      const uint64_t npass = (n + kGroup - 1) / kGroup;
+      uint32_t raw = 0;
+      for (uint64_t q = 0; q < npass; ++q) raw ^= warp_crc_pass_global(g, n, q, stage, cs);
+      acc = ~raw;
+    }
+    if (lane == 0) out[r] = acc;
+  }
+}
+
+// Single large range: passes spread over all warps, XOR-combined atomically.
+// `out` must be pre-set to 0xFFFFFFFF.
+__global__ void __launch_bounds__(kCrcWarps * 32) crc_big_kernel(const uint8_t* g, uint64_t n, uint32_t* out) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
+  uint8_t* stage = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * (kGroup + 192);
+  crc_smem_init(cs);
+  __syncthreads();
+  const uint64_t npass = (n + kGroup - 1) / kGroup;
+  const uint64_t nw = (uint64_t)gridDim.x * kCrcWarps;
+  uint32_t acc = 0;
+  for (uint64_t q = blockIdx.x * kCrcWarps + (threadIdx.x >> 5); q < npass; q += nw)
+    acc ^= warp_crc_pass_global(g, n, q, stage, cs);
+  if (lane_id() == 0 && acc) atomicXor(out, acc);
+}
+
+struct BlockTable {
+  uint64_t* addr;   // arena byte offset of the (clamped) block
+  uint32_t* len;    // clamped length (pread semantics)
+  uint32_t* foff;   // file-relative offset (error reporting)
+  uint32_t* file;   // file index
+};
+
+// Stage C: warp per (valid) file: write the data-block table.
+__global__ void parse_files_c(ParseArgs a, const uint32_t* file_blk_base, BlockTable bt,
+                              uint32_t restart_bound, unsigned long long* entry_bound) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  if (warp >= a.nfiles) return;
+  const FileInfo fi = a.info[warp];
+  if (fi.nblocks == 0) return;
+  const uint64_t faddr = a.file_addr[warp];
+  const uint64_t size = a.file_size[warp];
+  const uint8_t* f = a.arena + faddr;
+  const uint8_t* body = f + fi.index_off;
+  const uint64_t end = fi.index_len - 8;
+  const uint32_t n = fi.nblocks;
+  const uint32_t base = file_blk_base[warp];
+  unsigned long long bound = 0;
+  auto put = [&](uint32_t i, uint32_t off, uint32_t len) {
+    const uint64_t o = off;
+    const uint64_t l = o >= size ? 0 : ((uint64_t)len < size - o ? len : size - o);
+    bt.addr[base + i] = faddr + (o >= size ? size : o);
+    bt.len[base + i] = (uint32_t)l;
+    bt.foff[base + i] = off;
+    bt.file[base + i] = warp;
+    if (l >= 12) {
+      const uint32_t nres = ld_u32_le(f + o + l - 8);
+      const uint64_t by_bytes = (l - 8) / 3 + 1;
+      const uint64_t by_res = (uint64_t)(nres ? nres : 1) * restart_bound;
+      bound += by_bytes < by_res ? by_bytes : by_res;
+    }
+  };
+  uint32_t K0;
+  if (index_fixed_stride(body, end, n, K0)) {
+    const uint64_t E = 1ull + K0 + 8ull;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint8_t* e = body + (uint64_t)i * E + 1 + K0;
+      put(i, ld_u32_le(e), ld_u32_le(e + 4));
+    }
+  } else if (lane == 0) {
+    uint32_t kl;
+    index_walk(body, end, n, kl, put);
+  }
+  bound = warp_sum(bound);
+  if (lane == 0) atomicAdd(entry_bound, bound);
+}
+
+}  // namespace luda

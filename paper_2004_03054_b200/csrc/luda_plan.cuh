@@ -1,0 +1,308 @@
+// luda_plan.cuh — exact parallel block and SST planning.
+//
+// SstBuilder (sst.py:138-177) cuts blocks greedily: before adding entry e to a
+// non-empty block it flushes if
+//     cur_entry_bytes + size(e) + 4*ceil((n+1)/ri) + 4 > block_size
+// where size(e) uses shared = 0 when e is at a restart position
+// (i % ri == 0 counted from the block start) and the LCP with the previous
+// key otherwise (blocks.py:41-74). Then, after a flush, it closes the SST as
+// soon as data_bytes >= sst_size_target (sst.py:161-162).
+//
+// Both are "greedy chains": from a start s the next start is nxt(s), and the
+// cut set is the chain 0 → nxt(0) → ... . Here:
+//   * block_jump_kernel computes nxt for every survivor (jmp = nxt - s) and
+//     the size of the block that would start there; SST jumps come from a
+//     binary search over block-size prefix sums.
+//   * chain_map_kernel splits the sequence into tiles of T >= D items
+//     (D = max jump) and, for every possible entry offset o < D into the
+//     tile, follows the chain through the tile → exit offset into the next
+//     tile and node count. The maps compose associatively.
+//   * chain_group_kernel composes G consecutive tile maps; chain_top_kernel
+//     walks the groups from offset 0 (the true chain); chain_emit_kernel
+//     re-walks each tile from its true entry and writes the chain nodes.
+// The result is exactly the builder's greedy cut, computed in O(n) work.
+#pragma once
+#include "luda_rec.cuh"
+
+namespace luda {
+
+constexpr uint32_t kChainEnd = 0xFFFFFFFFu;
+
+// ---- block jumps ----------------------------------------------------------------
+constexpr int kJumpThreads = 256;
+constexpr int kJumpTile = 4096;
+
+template <int W>
+struct BlockJumpArgs {
+  const Rec<W>* rec;
+  uint64_t n;
+  uint32_t K;
+  uint32_t block_size;
+  uint32_t ri;
+  uint32_t halo;      // >= max entries per block
+  uint32_t* jmp;      // out [n]
+  uint32_t* bsz;      // out [n]: block size incl. crc if a block starts here
+  unsigned int* jmax;
+  unsigned int* overflow;
+};
+
+template <int W>
+__global__ void __launch_bounds__(kJumpThreads) block_jump_kernel(BlockJumpArgs<W> a) {
+  extern __shared__ __align__(16) uint32_t sz[];  // [2][kJumpTile + halo]: full, compressed
+  const uint32_t span = kJumpTile + a.halo;
+  uint32_t* sa = sz;
+  uint32_t* sb = sz + span;
+  const uint64_t t0 = (uint64_t)blockIdx.x * kJumpTile;
+  const uint32_t K = a.K;
+  const uint32_t vK = varint_size(K);
+  for (uint32_t i = threadIdx.x; i < span; i += kJumpThreads) {
+    const uint64_t j = t0 + i;
+    if (j >= a.n) break;
+    const Rec<W> cur = a.rec[j];
+    const uint32_t vl = handle_len(cur.h);
+    const uint32_t vv = varint_size(vl);
+    sa[i] = 1 + vK + vv + K + vl;
+    uint32_t s = 0;
+    if (j > 0) s = ikey_lcp(a.rec[j - 1], cur, K - 8);
+    sb[i] = varint_size(s) + varint_size(K - s) + vv + (K - s) + vl;
+  }
+  __syncthreads();
+  uint32_t mymax = 0;
+  for (uint32_t i = threadIdx.x; i < (uint32_t)kJumpTile; i += kJumpThreads) {
+    const uint64_t j = t0 + i;
+    if (j >= a.n) break;
+    uint64_t size = 0;
+    uint32_t cnt = 0;
+    while (j + cnt < a.n) {
+      if (i + cnt >= span) { atomicExch(a.overflow, 1u); break; }
+      const uint32_t es = (cnt % a.ri == 0) ? sa[i + cnt] : sb[i + cnt];
+      if (cnt > 0 && size + es + 4ull * ((cnt + 1 + a.ri - 1) / a.ri) + 4 > a.block_size) break;
+      size += es;
+      ++cnt;
+    }
+    a.jmp[j] = cnt;
+    a.bsz[j] = (uint32_t)(size + 4ull * ((cnt + a.ri - 1) / a.ri) + 8);
+    mymax = cnt > mymax ? cnt : mymax;
+  }
+  mymax = warp_max(mymax);
+  if (lane_id() == 0) atomicMax(a.jmax, mymax);
+}
+
+// ---- SST jumps -------------------------------------------------------------------
+// pos[b] = data bytes before block b (exclusive prefix, pos[nb] = total).
+__global__ void sst_jump_kernel(const uint64_t* pos, uint32_t nb, uint64_t target, uint32_t* jmp,
+                                unsigned int* jmax) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t j = 0;
+  if (b < nb) {
+    const uint64_t want = pos[b] + target;
+    // first e in (b, nb] with pos[e] >= want, else nb
+    uint32_t lo = b + 1, hi = nb;
+    while (lo < hi) {
+      const uint32_t mid = lo + ((hi - lo) >> 1);
+      if (pos[mid] >= want) hi = mid;
+      else lo = mid + 1;
+    }
+    j = lo - b;
+    jmp[b] = j;
+  }
+  j = warp_max(j);
+  if (lane_id() == 0) atomicMax(jmax, j);
+}
+
+// ---- generic chain over jmp[0..n) -------------------------------------------------
+struct ChainArgs {
+  const uint32_t* jmp;
+  uint32_t n;
+  uint32_t T;       // tile size (>= D)
+  uint32_t D;       // domain: max jump
+  uint32_t ntiles;
+  uint32_t G;       // tiles per group
+  uint32_t ngroups;
+  uint32_t* exit_;  // [ntiles*D]
+  uint32_t* cnt;    // [ntiles*D]
+  uint32_t* gexit;  // [ngroups*D]
+  uint32_t* gcnt;   // [ngroups*D]
+  uint32_t* gentry; // [ngroups]
+  uint32_t* gbase;  // [ngroups]
+  uint32_t* nodes;  // out: chain nodes
+  uint32_t* nnodes; // out: count
+};
+
+constexpr int kChainThreads = 256;
+
+__global__ void __launch_bounds__(kChainThreads) chain_map_kernel(ChainArgs c) {
+  extern __shared__ __align__(16) uint32_t sj[];  // tile jumps (when T small enough)
+  const uint32_t t = blockIdx.x;
+  const uint64_t t0 = (uint64_t)t * c.T;
+  const uint64_t tend = t0 + c.T < c.n ? t0 + c.T : c.n;
+  const bool use_smem = c.T <= 12288;
+  if (use_smem) {
+    for (uint64_t x = t0 + threadIdx.x; x < tend; x += kChainThreads) sj[x - t0] = c.jmp[x];
+    __syncthreads();
+  }
+  for (uint32_t o = threadIdx.x; o < c.D; o += kChainThreads) {
+    uint64_t x = t0 + o;
+    uint32_t k = 0;
+    while (x < tend) {
+      x += use_smem ? sj[x - t0] : c.jmp[x];
+      ++k;
+    }
+    const uint64_t idx = (uint64_t)t * c.D + o;
+    c.exit_[idx] = (x >= c.n) ? kChainEnd : (uint32_t)(x - (t0 + c.T));
+    c.cnt[idx] = k;
+  }
+}
+
+__global__ void __launch_bounds__(kChainThreads) chain_group_kernel(ChainArgs c) {
+  const uint32_t g = blockIdx.x;
+  const uint32_t tf = g * c.G;
+  const uint32_t tl = (tf + c.G < c.ntiles) ? tf + c.G : c.ntiles;
+  for (uint32_t o = threadIdx.x; o < c.D; o += kChainThreads) {
+    uint32_t off = o, total = 0;
+    for (uint32_t t = tf; t < tl && off != kChainEnd; ++t) {
+      const uint64_t idx = (uint64_t)t * c.D + off;
+      total += c.cnt[idx];
+      off = c.exit_[idx];
+    }
+    c.gexit[(uint64_t)g * c.D + o] = off;
+    c.gcnt[(uint64_t)g * c.D + o] = total;
+  }
+}
+
+__global__ void chain_top_kernel(ChainArgs c) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint32_t off = 0, total = 0;
+  for (uint32_t g = 0; g < c.ngroups; ++g) {
+    c.gentry[g] = off;
+    c.gbase[g] = total;
+    if (off == kChainEnd) continue;
+    const uint64_t idx = (uint64_t)g * c.D + off;
+    total += c.gcnt[idx];
+    off = c.gexit[idx];
+  }
+  *c.nnodes = total;
+}
+
+__global__ void __launch_bounds__(kChainThreads) chain_emit_kernel(ChainArgs c) {
+  __shared__ uint32_t s_off, s_base;
+  const uint32_t t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    const uint32_t g = t / c.G;
+    uint32_t off = c.gentry[g], base = c.gbase[g];
+    for (uint32_t u = g * c.G; u < t && off != kChainEnd; ++u) {
+      const uint64_t idx = (uint64_t)u * c.D + off;
+      base += c.cnt[idx];
+      off = c.exit_[idx];
+    }
+    s_off = off;
+    s_base = base;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0 || s_off == kChainEnd) return;
+  const uint64_t t0 = (uint64_t)t * c.T;
+  const uint64_t tend = t0 + c.T < c.n ? t0 + c.T : c.n;
+  uint64_t x = t0 + s_off;
+  uint32_t k = s_base;
+  while (x < tend) {
+    c.nodes[k++] = (uint32_t)x;
+    x += c.jmp[x];
+  }
+}
+
+// ---- block descriptors + exclusive prefix of sizes ----------------------------------
+__global__ void block_desc_kernel(const uint32_t* nodes, uint32_t nb, const uint32_t* jmp, const uint32_t* bsz,
+                                  uint32_t* blk_first, uint32_t* blk_n, uint32_t* blk_size) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  const uint32_t s = nodes[k];
+  blk_first[k] = s;
+  blk_n[k] = jmp[s];
+  blk_size[k] = bsz[s];
+}
+
+// Single-pass exclusive scan (u64 out) of a u32 or u64 array with decoupled
+// look-back; out[n] = total.
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) scan_excl_kernel(const T* in, uint64_t n, uint64_t* out,
+                                                                 uint64_t* lb, unsigned int* tile_ctr) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_warp[kScanThreads / 32];
+  __shared__ uint64_t s_base;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t i0 = tile * (kScanThreads * kScanItems) + threadIdx.x * kScanItems;
+  uint64_t v[kScanItems];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (i0 + k < n) ? (uint64_t)in[i0 + k] : 0;
+    sum += v[k];
+  }
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  const uint64_t incl = warp_incl_scan<uint64_t>(sum);
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const uint64_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0;
+    const uint64_t wi = warp_incl_scan<uint64_t>(w);
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
+    const uint64_t total = __shfl_sync(0xFFFFFFFFu, wi, 31);
+    if (lane == 0) lb_publish(lb, tile, kLbAgg, total);
+    const uint64_t ex = lb_exclusive(lb, tile);
+    if (lane == 0) {
+      lb_publish(lb, tile, kLbInc, ex + total);
+      s_base = ex;
+      const uint64_t ntile = (n + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems);
+      if (tile + 1 == ntile || n == 0) out[n] = ex + total;
+    }
+  }
+  __syncthreads();
+  uint64_t run = s_base + s_warp[wid] + incl - sum;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (i0 + k < n) out[i0 + k] = run;
+    run += v[k];
+  }
+}
+
+// ---- SST layout ----------------------------------------------------------------------
+struct SstLayoutArgs {
+  const uint32_t* sst_first_blk;  // chain nodes [nsst]
+  uint32_t nsst;
+  uint32_t nblk;
+  const uint32_t* blk_first;
+  const uint64_t* blk_pos;        // [nblk+1]
+  uint64_t n_entries;
+  uint32_t K;
+  uint32_t bits_per_key;
+  uint64_t* sst_size;             // out [nsst]
+  uint64_t* sst_data;             // out: data bytes
+  uint64_t* sst_nent;             // out: entries
+  uint32_t* sst_last_blk;         // out: one past last block
+};
+
+__global__ void sst_layout_kernel(SstLayoutArgs a) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.nsst) return;
+  const uint32_t fb = a.sst_first_blk[s];
+  const uint32_t eb = (s + 1 < a.nsst) ? a.sst_first_blk[s + 1] : a.nblk;
+  const uint64_t fe = a.blk_first[fb];
+  const uint64_t ee = (eb < a.nblk) ? a.blk_first[eb] : a.n_entries;
+  const uint64_t ne = ee - fe;
+  const uint64_t data = a.blk_pos[eb] - a.blk_pos[fb];
+  uint64_t nbits = ne * a.bits_per_key;
+  if (nbits < 64) nbits = 64;
+  nbits = (nbits + 7) & ~7ull;
+  const uint64_t flen = nbits / 8 + 1 + 4;
+  const uint64_t ilen = (uint64_t)(eb - fb) * (varint_size(a.K) + a.K + 8) + 8;
+  a.sst_size[s] = data + flen + ilen + 24;
+  a.sst_data[s] = data;
+  a.sst_nent[s] = ne;
+  a.sst_last_blk[s] = eb;
+}
+
+}  // namespace luda

@@ -1,0 +1,75 @@
+// luda_tables.cuh — CRC-32/IEEE tables and GF(2) shift operators.
+//
+// Host code computes, once per process (luda_init):
+//   g_crc_tab   byte table of the reflected polynomial 0xEDB88320
+//   g_seg_nib   nibble tables of Z_{132*d}, d = 0..31 (segment combine)
+//   c_zpow      columns of Z_{2^i}, i = 0..47 (arbitrary shifts)
+//   c_zgroup    columns of Z_{4224} (one warp pass)
+// where Z_n advances a raw CRC register over n zero bytes (the operator
+// behind zlib's crc32_combine).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "luda_common.cuh"
+
+namespace luda {
+
+namespace tables_detail {
+
+void host_table(uint32_t* t) {
+  for (uint32_t b = 0; b < 256; ++b) {
+    uint32_t c = b;
+    for (int k = 0; k < 8; ++k) c = (c & 1) ? (c >> 1) ^ kCrcPoly : (c >> 1);
+    t[b] = c;
+  }
+}
+
+uint32_t zero_bytes(const uint32_t* t, uint32_t c, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) c = t[c & 0xFF] ^ (c >> 8);
+  return c;
+}
+
+uint32_t apply_cols(const uint32_t* cols, uint32_t c) {
+  uint32_t r = 0;
+  for (int j = 0; j < 32; ++j)
+    if ((c >> j) & 1) r ^= cols[j];
+  return r;
+}
+
+}  // namespace tables_detail
+
+// Returns 0 on success.
+using namespace tables_detail;
+int upload_crc_tables() {
+  uint32_t t[256];
+  host_table(t);
+  // Z_132 columns, then Z_{132 d} by repeated application.
+  uint32_t z132[32];
+  for (int j = 0; j < 32; ++j) z132[j] = zero_bytes(t, 1u << j, kSeg);
+  static uint32_t nib[8 * 16 * 32];
+  uint32_t cols[32];
+  for (int j = 0; j < 32; ++j) cols[j] = 1u << j;  // Z_0 = identity
+  for (int d = 0; d < 32; ++d) {
+    for (int n = 0; n < 8; ++n)
+      for (int v = 0; v < 16; ++v) nib[((n * 16) + v) * 32 + d] = apply_cols(cols, (uint32_t)v << (4 * n));
+    uint32_t next[32];
+    for (int j = 0; j < 32; ++j) next[j] = apply_cols(z132, cols[j]);
+    memcpy(cols, next, sizeof(cols));
+  }
+  // Z_{2^i}: Z_1 columns then squaring.
+  static uint32_t zpow[48][32];
+  for (int j = 0; j < 32; ++j) zpow[0][j] = zero_bytes(t, 1u << j, 1);
+  for (int i = 1; i < 48; ++i)
+    for (int j = 0; j < 32; ++j) zpow[i][j] = apply_cols(zpow[i - 1], zpow[i - 1][j]);
+  uint32_t zg[32];
+  for (int j = 0; j < 32; ++j) zg[j] = zero_bytes(t, 1u << j, kGroup);
+  if (cudaMemcpyToSymbol(g_crc_tab, t, sizeof(t)) != cudaSuccess) return 1;
+  if (cudaMemcpyToSymbol(g_seg_nib, nib, sizeof(nib)) != cudaSuccess) return 1;
+  if (cudaMemcpyToSymbol(c_zpow, zpow, sizeof(zpow)) != cudaSuccess) return 1;
+  if (cudaMemcpyToSymbol(c_zgroup, zg, sizeof(zg)) != cudaSuccess) return 1;
+  return 0;
+}
+
+}  // namespace luda

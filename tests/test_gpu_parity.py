@@ -1,0 +1,147 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bit-exact comparisons only (all of this is integer/byte work)."""
+
+import ctypes
+import hashlib
+import json
+import os
+import random
+import zlib
+
+import pytest
+
+from oracle import jobgen
+from oracle import luda_oracle as O
+from tests.golden.cases import CASES
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "compaction.json")))
+
+
+def sha(b):
+    return hashlib.sha256(bytes(b)).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2004_03054_b200 import DeviceConfig, make_device
+    d = make_device(DeviceConfig(backend="b200"))
+    yield d
+    d.close()
+
+
+@pytest.fixture(scope="module")
+def native():
+    from paper_2004_03054_b200 import _native
+    return _native.lib(0)
+
+
+def gpu_crc(native, data: bytes, pad_front=0):
+    p = ctypes.c_void_p()
+    assert native.luda_region_alloc(len(data) + pad_front + 64, ctypes.byref(p)) == 0
+    try:
+        buf = ctypes.create_string_buffer(bytes(pad_front) + data, len(data) + pad_front)
+        assert native.luda_stage_in_async(p.value, buf, len(data) + pad_front, None) == 0
+        out = ctypes.c_uint32()
+        assert native.luda_crc32(p.value + pad_front, len(data), ctypes.byref(out), None) == 0
+        return out.value
+    finally:
+        native.luda_region_free(p.value)
+
+
+def test_crc32_kat_and_random(native):
+    assert gpu_crc(native, b"123456789") == 0xCBF43926
+    assert gpu_crc(native, b"") == 0
+    rng = random.Random(7)
+    for n in (1, 2, 3, 4, 5, 7, 8, 131, 132, 133, 263, 264, 265, 1000, 4095, 4096, 4223, 4224, 4225, 8448,
+              10025, 65537, 1 << 20, (1 << 22) + 3):
+        for pad in (0, 1, 3, 13):
+            b = rng.randbytes(n)
+            assert gpu_crc(native, b, pad) == zlib.crc32(b), (n, pad)
+
+
+def build(name):
+    mk, out_cfg = {n: (m, c) for n, m, c in CASES}[name]
+    job = mk()
+    blk = {k: out_cfg[k] for k in ("block_size", "restart_interval") if k in out_cfg}
+    lower, upper = jobgen.materialize(job, **blk)
+    return job, lower, upper, out_cfg
+
+
+def gpu_compact(dev, job, lower, upper, out_cfg, **kw):
+    from paper_2004_03054_b200.compaction import compact_files
+    from paper_2004_03054_b200.config import StoreConfig
+    cfg = StoreConfig(**{k: out_cfg[k] for k in ("block_size", "restart_interval", "sst_size_target",
+                                                 "bits_per_key") if k in out_cfg})
+    return compact_files(dev, lower, upper, source_level=job.source_level, deeper=job.deeper, config=cfg, **kw)
+
+
+@pytest.mark.parametrize("name", [n for n, _, _ in CASES])
+def test_compaction_matches_oracle_and_golden(dev, name):
+    job, lower, upper, out_cfg = build(name)
+    want = O.reference_compact(lower + upper, deeper=job.deeper, **out_cfg)
+    got = gpu_compact(dev, job, lower, upper, out_cfg)
+    assert len(got) == len(want)
+    for (gb, gs, gl), (wb, ws, wl) in zip(got, want):
+        assert gs == ws and gl == wl
+        assert gb == wb
+    assert [sha(b) for b, _, _ in got] == [o["sha256"] for o in GOLD[name]["outputs"]]
+
+
+def test_flush_builder_matches_oracle(native):
+    from paper_2004_03054_b200.flush import build_ssts
+    rng = random.Random(11)
+    keys = sorted({rng.randbytes(16) for _ in range(5000)})
+    pairs = []
+    seq = 1
+    for k in keys:
+        for _ in range(rng.choice((1, 1, 1, 2, 3))):  # several versions per user key
+            pairs.append((O.make_ikey(k, seq, O.KIND_PUT if rng.random() < 0.9 else O.KIND_DELETE),
+                          rng.randbytes(rng.randint(0, 300))))
+            seq += 1
+    pairs.sort(key=lambda kv: O.order_key(kv[0]))
+    for cfg in (dict(sst_size_target=64 * 1024), dict(sst_size_target=2**31, block_size=1024, restart_interval=3)):
+        want = O.build_tables_split(pairs, **cfg)
+        got = build_ssts(pairs, **cfg)
+        assert [g[0] for g in got] == [w[0] for w in want]
+        assert [(g[1], g[2]) for g in got] == [(w[1], w[2]) for w in want]
+
+
+def _corrupt_case():
+    job = jobgen.c3(n=2000, seed=5, sst_target=32 * 1024)
+    lower, upper = jobgen.materialize(job)
+    return job, lower, upper
+
+
+def test_corruption_reports_block_offset(dev):
+    from paper_2004_03054_b200 import CorruptionError
+    job, lower, upper = _corrupt_case()
+    _, index = O.open_table(upper[1])
+    off = index[3][1]
+    bad = bytearray(upper[1])
+    bad[off + 7] ^= 0x40
+    upper = list(upper)
+    upper[1] = bytes(bad)
+    with pytest.raises(O.CorruptionError) as want:
+        O.reference_compact(lower + upper)
+    with pytest.raises(CorruptionError) as got:
+        gpu_compact(dev, job, lower, upper, {})
+    assert got.value.offset == want.value.offset == off
+
+
+@pytest.mark.parametrize("mutate,exc", [
+    (lambda f: f[:-1] + bytes([f[-1] ^ 1]), "FormatError"),          # bad magic
+    (lambda f: f[:10], "FormatError"),                                 # too short
+])
+def test_format_errors(dev, mutate, exc):
+    import paper_2004_03054_b200 as P
+    job, lower, upper = _corrupt_case()
+    lower = list(lower)
+    lower[0] = mutate(lower[0])
+    with pytest.raises(getattr(O, exc)):
+        O.reference_compact(lower + upper)
+    with pytest.raises(getattr(P, exc)):
+        gpu_compact(dev, job, lower, upper, {})
