@@ -127,7 +127,9 @@ typedef struct {
   uint32_t key_len;             /* internal key length K                           */
   uint8_t* sst_keys;            /* host[n_sst*2*K]: smallest ∥ largest per SST     */
   uint64_t n_in, n_out, blocks_in, blocks_out;
-  double t_ms[8];               /* parse, decode, merge, plan, encode, meta, -, total */
+  double t_ms[8];               /* phases: parse, decode, merge, plan, emit, -, -, total */
+  double k_ms[8];               /* kernels: decode, merge(final), block_jump, encode, meta, -, -, - */
+  uint64_t launches;            /* kernels launched by this job                   */
   void* priv;
 } luda_job_result;
 

@@ -60,6 +60,8 @@ class JobResult(ctypes.Structure):
         ("blocks_in", ctypes.c_uint64),
         ("blocks_out", ctypes.c_uint64),
         ("t_ms", ctypes.c_double * 8),
+        ("k_ms", ctypes.c_double * 8),
+        ("launches", ctypes.c_uint64),
         ("priv", ctypes.c_void_p),
     ]
 

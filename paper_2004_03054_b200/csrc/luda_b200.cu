@@ -86,7 +86,32 @@ struct Scratch {
 struct JobPriv {
   std::vector<uint64_t> off, len;
   std::vector<uint8_t> keys;
+  cudaStream_t st = nullptr;  // stream the output buffer was allocated on
 };
+
+// Event pairs bracketing single kernels (k_ms of luda_job_result).
+struct KTimer {
+  cudaEvent_t a[8], b[8];
+  bool used[8] = {};
+  KTimer() {
+    for (int i = 0; i < 8; ++i) { cudaEventCreate(&a[i]); cudaEventCreate(&b[i]); }
+  }
+  ~KTimer() {
+    for (int i = 0; i < 8; ++i) { cudaEventDestroy(a[i]); cudaEventDestroy(b[i]); }
+  }
+  void start(int i, cudaStream_t s) { cudaEventRecord(a[i], s); used[i] = true; }
+  void stop(int i, cudaStream_t s) { cudaEventRecord(b[i], s); }
+  void read(double* out) {
+    for (int i = 0; i < 8; ++i) {
+      float ms = 0;
+      if (used[i] && cudaEventElapsedTime(&ms, a[i], b[i]) == cudaSuccess) out[i] = ms;
+    }
+  }
+};
+thread_local KTimer* g_kt = nullptr;
+thread_local uint64_t g_launches = 0;
+#define KT_START(i, s) do { if (g_kt) g_kt->start(i, s); } while (0)
+#define KT_STOP(i, s) do { if (g_kt) g_kt->stop(i, s); } while (0)
 
 const char* file_msg(uint32_t code) {
   switch (code) {
@@ -174,6 +199,7 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, Rec<W>* Y, Rec<W>* 
     const uint64_t ntiles = (na + nb + kMergeTile - 1) / kMergeTile;
     GET(split, uint64_t, ntiles + 1, false);
     merge_partition_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, st>>>(A, na, B, nb, ntiles, split);
+    ++g_launches;
     MergeArgs<W> m{};
     m.A = A; m.na = na; m.B = B; m.nb = nb; m.split = split; m.ntiles = ntiles; m.out = out;
     m.a_run_base = abase; m.b_run_base = bbase;
@@ -192,7 +218,10 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, Rec<W>* Y, Rec<W>* 
       GET(sink, unsigned long long, 1, true);
       m.err_order = sink;
     }
+    if (resolve) KT_START(1, st);
     merge_kernel<W><<<(unsigned)ntiles, kMergeThreads, smem, st>>>(m);
+    ++g_launches;
+    if (resolve) KT_STOP(1, st);
     CK(cudaGetLastError());
     return LUDA_OK;
   };
@@ -259,9 +288,13 @@ int run_chain(cudaStream_t st, Scratch& scratch, const uint32_t* jmp, uint32_t n
   const size_t sm = T <= 12288 ? (size_t)T * 4 : 0;
   if (sm > 48 * 1024) CK(cudaFuncSetAttribute(chain_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   chain_map_kernel<<<ntiles, kChainThreads, sm, st>>>(c);
+  ++g_launches;
   chain_group_kernel<<<ngroups, kChainThreads, 0, st>>>(c);
+  ++g_launches;
   chain_top_kernel<<<1, 32, 0, st>>>(c);
+  ++g_launches;
   chain_emit_kernel<<<ntiles, kChainThreads, 0, st>>>(c);
+  ++g_launches;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&outb.n_nodes, nn, 4, cudaMemcpyDeviceToHost, st));
   int rc = sync(st);
@@ -301,7 +334,10 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1};
   const size_t jsm = 2ull * (kJumpTile + halo) * 4;
   CK(cudaFuncSetAttribute(block_jump_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
+  KT_START(2, st);
   block_jump_kernel<W><<<(unsigned)((n + kJumpTile - 1) / kJumpTile), kJumpThreads, jsm, st>>>(ja);
+  ++g_launches;
+  KT_STOP(2, st);
   CK(cudaGetLastError());
   unsigned int hctl[4];
   CK(cudaMemcpyAsync(hctl, ctl, 16, cudaMemcpyDeviceToHost, st));
@@ -318,15 +354,18 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(blk_size, uint32_t, nblk, false);
   GET(blk_pos, uint64_t, nblk + 1, false);
   block_desc_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(bch.nodes, nblk, jmp, bsz, blk_first, blk_n, blk_size);
+  ++g_launches;
   {
     const uint64_t nt = std::max<uint64_t>(1, (nblk + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
     GET(lb, uint64_t, nt, true);
     GET(ctr, unsigned int, 1, true);
     scan_excl_kernel<uint32_t><<<(unsigned)nt, kScanThreads, 0, st>>>(blk_size, nblk, blk_pos, lb, ctr);
+    ++g_launches;
   }
   // ---- SST cut ----
   GET(sjmp, uint32_t, nblk, false);
   sst_jump_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, p.sst_target, sjmp, ctl + 2);
+  ++g_launches;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(hctl, ctl, 16, cudaMemcpyDeviceToHost, st));
   rc = sync(st);
@@ -342,11 +381,13 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(sst_off, uint64_t, nsst + 1, false);
   SstLayoutArgs la{sch.nodes, nsst, nblk, blk_first, blk_pos, n, p.K, p.bpk, sst_size, sst_data, sst_nent, sst_last};
   sst_layout_kernel<<<(nsst + 255) / 256, 256, 0, st>>>(la);
+  ++g_launches;
   {
     const uint64_t nt = std::max<uint64_t>(1, (nsst + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
     GET(lb, uint64_t, nt, true);
     GET(ctr, unsigned int, 1, true);
     scan_excl_kernel<uint64_t><<<(unsigned)nt, kScanThreads, 0, st>>>(sst_size, nsst, sst_off, lb, ctr);
+    ++g_launches;
   }
   priv->off.resize(nsst + 1);
   priv->len.resize(nsst);
@@ -370,7 +411,8 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
     }
   }
   void* outp = nullptr;
-  CK(cudaMalloc(&outp, total + 256));
+  CK(cudaMallocAsync(&outp, total + 256, st));
+  priv->st = st;
   res->out = reinterpret_cast<uint8_t*>(outp);
   res->out_bytes = total;
   GET(bigs, uint32_t, big_words + 16, true);
@@ -379,17 +421,23 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(d_keys, uint8_t, 2ull * nsst * p.K, false);
   // ---- encode data blocks ----
   EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off, res->out};
-  const size_t esm = sizeof(CrcSmem) + (size_t)kEncWarps * kEncBuf;
+  const size_t esm = sizeof(CrcSmem) + (size_t)kEncWarps * kEncWarpBytes;
   CK(cudaFuncSetAttribute(encode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
   const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncWarps - 1) / kEncWarps, (uint64_t)g_num_sms);
+  KT_START(3, st);
   encode_kernel<W><<<std::max(1u, egrid), kEncWarps * 32, esm, st>>>(ea);
+  ++g_launches;
+  KT_STOP(3, st);
   CK(cudaGetLastError());
   // ---- filter / index / footer ----
   const uint32_t kprobes = std::max(1, std::min(30, (int)std::lround(p.bpk * std::log(2.0))));
   MetaArgs<W> ma{S, p.K, p.bpk, kprobes, nsst, sch.nodes, sst_last, sst_off, sst_data, sst_nent, sst_size,
                  blk_first, blk_n, blk_size, blk_pos, res->out, bigs, d_soff, d_keys};
   CK(cudaFuncSetAttribute(sst_meta_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMetaSmem));
+  KT_START(4, st);
   sst_meta_kernel<W><<<nsst, kMetaThreads, kMetaSmem, st>>>(ma);
+  ++g_launches;
+  KT_STOP(4, st);
   CK(cudaGetLastError());
   if (ev) CK(cudaEventRecord(ev[1], st));
   priv->keys.resize(2ull * nsst * p.K);
@@ -425,11 +473,15 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     GET(lb, uint64_t, nblk, true);
     GET(ctr, unsigned int, 1, true);
     DecodeArgs<W> da{jd->arena, bt, nblk, K, X, cap, lb, ctr, d_base, errs, errs + 1};
+    KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
+    ++g_launches;
+    KT_STOP(0, st);
     CK(cudaGetLastError());
     GET(d_fbase, uint64_t, jd->n_files + 1, false);
     file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_base, d_file_blk_base, jd->n_files,
                                                                            d_fbase);
+    ++g_launches;
     unsigned long long herr[2];
     CK(cudaMemcpyAsync(herr, errs, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
@@ -557,7 +609,9 @@ int build_w(cudaStream_t st, Scratch& scratch, const uint8_t* keys, uint32_t L, 
   CK(cudaMemsetAsync(bad, 0xFF, 8, st));
   const unsigned g = (unsigned)((n + 255) / 256);
   records_from_arrays_kernel<W><<<g, 256, 0, st>>>(keys, L, tr, voff, vlen, n, R, bad);
+  ++g_launches;
   check_sorted_kernel<W><<<g, 256, 0, st>>>(R, n, bad);
+  ++g_launches;
   unsigned long long hb = 0;
   CK(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
   int rc = sync(st);
@@ -683,6 +737,7 @@ int luda_crc32_batch(const void* data, const uint64_t* off, const uint32_t* len,
   CK(cudaFuncSetAttribute(crc_ranges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   const unsigned grid = std::min<unsigned>((n + kCrcWarps - 1) / kCrcWarps, 4 * g_num_sms);
   crc_ranges_kernel<<<grid, kCrcWarps * 32, sm, (cudaStream_t)stream>>>((const uint8_t*)data, off, len, n, out);
+  ++g_launches;
   CK(cudaGetLastError());
   return LUDA_OK;
 }
@@ -713,6 +768,7 @@ int luda_crc32(const void* data, uint64_t n, uint32_t* out_crc, void* stream) {
     const uint64_t np = (n + kGroup - 1) / kGroup;
     const unsigned grid = (unsigned)std::min<uint64_t>((np + kCrcWarps - 1) / kCrcWarps, 4ull * g_num_sms);
     crc_big_kernel<<<grid, kCrcWarps * 32, sm, st>>>((const uint8_t*)data, n, d);
+    ++g_launches;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out_crc, d, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -723,8 +779,16 @@ int luda_crc32(const void* data, uint64_t n, uint32_t* out_crc, void* stream) {
 
 int luda_job_release(luda_job_result* r) {
   if (!r) return LUDA_OK;
-  if (r->out) cudaFree(r->out);
-  delete reinterpret_cast<JobPriv*>(r->priv);
+  JobPriv* priv = reinterpret_cast<JobPriv*>(r->priv);
+  if (r->out) {
+    if (priv && priv->st) {
+      cudaStreamSynchronize(priv->st);
+      cudaFreeAsync(r->out, priv->st);
+    } else {
+      cudaFree(r->out);
+    }
+  }
+  delete priv;
   memset(r, 0, sizeof(*r));
   return LUDA_OK;
 }
@@ -766,6 +830,10 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
   memset(res, 0, sizeof(*res));
   cudaStream_t st = (cudaStream_t)stream;
+  KTimer kt;
+  g_kt = &kt;
+  g_launches = 0;
+  struct KtGuard { ~KtGuard() { g_kt = nullptr; } } ktg;
   Scratch scratch(st);
   cudaEvent_t ev[8];
   for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -788,6 +856,7 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   GET(ccrc, uint32_t, 2ull * nf, false);
   ParseArgs pa{jd->arena, d_faddr, d_fsize, nf, info, caddr, clen, cstored};
   parse_files_a<<<(nf * 32 + 255) / 256, 256, 0, st>>>(pa);
+  ++g_launches;
   CK(cudaGetLastError());
   int rc = luda_crc32_batch(jd->arena, caddr, clen, 2 * nf, ccrc, st);
   if (rc) return rc;
@@ -844,6 +913,7 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   GET(bound, unsigned long long, 1, true);
   parse_files_c<<<(nf * 32 + 255) / 256, 256, 0, st>>>(pa, d_fbb, bt, std::max<uint32_t>(jd->restart_interval, 16),
                                                        bound);
+  ++g_launches;
   CK(cudaGetLastError());
   unsigned long long hbound = 0;
   CK(cudaMemcpyAsync(&hbound, bound, 8, cudaMemcpyDeviceToHost, st));
@@ -869,6 +939,8 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
     for (int i = 0; i < 5; ++i) res->t_ms[i] = ev_ms(ev[i], ev[i + 1]);
   }
   res->t_ms[7] = ev_ms(ev[0], ev[7]);
+  kt.read(res->k_ms);
+  res->launches = g_launches;
   return LUDA_OK;
 }
 

@@ -84,34 +84,51 @@ __device__ __forceinline__ uint32_t crc_shift(uint32_t c, uint64_t n) {
 
 // Raw CRC register over 33 words of shared memory starting at byte address p
 // (may be unaligned; reads the aligned words covering it). Bytes whose
-// data-index (idx0 + k) is < 0 are replaced by zero and bytes with index in
+// data-index (idx0 + k) is < 0 are treated as zero and bytes with index in
 // [0,4) are complemented: F(~0, D) = F(0, D with its first 4 bytes inverted)
 // and leading zero bytes leave a zero register unchanged, so the preset folds
-// into the data (requires n >= 4). The smem window [p, p+136) must be readable.
+// into the data (requires n >= 4). Only the first segment (idx0 < 4) has such
+// bytes: it skips its all-zero leading words and masks the next two, so the
+// main loop carries no per-word checks. Reads the smem window [p, p+136).
 __device__ __forceinline__ uint32_t seg_crc_smem(const uint8_t* p, int64_t idx0,
                                                  const uint32_t* __restrict__ tl) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
   const uint32_t sh = (uint32_t)(a & 3u) * 8u;
-  uint32_t c = 0;
-  uint32_t lo = wp[0];
-#pragma unroll 11
-  for (int j = 0; j < kSegWords; ++j) {
-    uint32_t hi = wp[j + 1];
-    uint32_t w = __funnelshift_r(lo, hi, sh);
-    lo = hi;
-    int64_t bi = idx0 + 4 * j;  // data index of byte 0 of this word
-    if (bi < 4) {               // only the leading words of the first segment
-      uint32_t keep = 0, inv = 0;
+  // first word holding a data byte, and the masks of words j0, j0+1
+  int32_t j0 = 0;
+  uint32_t keep0 = 0xFFFFFFFFu, inv0 = 0, keep1 = 0xFFFFFFFFu, inv1 = 0;
+  if (idx0 < 4) {
+    const int32_t i0 = (int32_t)idx0;  // in (-132, 4)
+    j0 = i0 < 0 ? (-i0) >> 2 : 0;      // words entirely before data index 0 are zero
+    const int32_t b0 = i0 + 4 * j0;    // data index of byte 0 of word j0 (in (-4, 4))
+    keep0 = inv0 = keep1 = inv1 = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int64_t d = bi + k;
-        if (d >= 0) keep |= 0xFFu << (8 * k);
-        if (d >= 0 && d < 4) inv |= 0xFFu << (8 * k);
-      }
-      w = (w & keep) ^ inv;
+    for (int k = 0; k < 4; ++k) {
+      const int32_t d0 = b0 + k, d1 = b0 + 4 + k;
+      if (d0 >= 0) keep0 |= 0xFFu << (8 * k);
+      if (d0 >= 0 && d0 < 4) inv0 |= 0xFFu << (8 * k);
+      if (d1 >= 0) keep1 |= 0xFFu << (8 * k);
+      if (d1 >= 0 && d1 < 4) inv1 |= 0xFFu << (8 * k);
     }
-    c = crc_word(c, w, tl);
+  }
+  uint32_t c = 0;
+  uint32_t lo = wp[j0];
+  {
+    const uint32_t hi = wp[j0 + 1];
+    c = crc_word(c, (__funnelshift_r(lo, hi, sh) & keep0) ^ inv0, tl);
+    lo = hi;
+  }
+  if (j0 + 1 < kSegWords) {
+    const uint32_t hi = wp[j0 + 2];
+    c = crc_word(c, (__funnelshift_r(lo, hi, sh) & keep1) ^ inv1, tl);
+    lo = hi;
+  }
+#pragma unroll 4
+  for (int32_t j = j0 + 2; j < kSegWords; ++j) {
+    const uint32_t hi = wp[j + 1];
+    c = crc_word(c, __funnelshift_r(lo, hi, sh), tl);
+    lo = hi;
   }
   return c;
 }
@@ -147,6 +164,70 @@ __device__ __forceinline__ uint32_t crc32_bytes(const uint8_t* p, uint32_t n, co
   uint32_t c = 0xFFFFFFFFu;
   for (uint32_t i = 0; i < n; ++i) c = crc_byte(c, p[i], tl);
   return ~c;
+}
+
+// ---- TMA bulk copies (cp.async.bulk) + mbarrier -----------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global → shared (16-byte aligned addresses, size % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Order this thread's earlier generic-proxy smem accesses before later
+// async-proxy (TMA) writes to the same smem.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Warp copy of n bytes between two shared-memory buffers of any alignment:
+// lanes own destination-aligned words (funnel-shifted from the source);
+// the two partial edge words are read-modify-written (callers guarantee no
+// other thread writes those words concurrently). Reads [src-3, src+n+4).
+__device__ __forceinline__ void warp_smem_copy(uint8_t* dst, const uint8_t* src, uint32_t n, uint32_t lane) {
+  if (n == 0) return;
+  const uintptr_t da = reinterpret_cast<uintptr_t>(dst);
+  const uintptr_t w0 = da & ~uintptr_t(3);
+  const uint32_t nw = (uint32_t)((((da + n + 3) & ~uintptr_t(3)) - w0) >> 2);
+  const intptr_t delta = reinterpret_cast<intptr_t>(src) - (intptr_t)da;
+  for (uint32_t w = lane; w < nw; w += 32) {
+    const uintptr_t A = w0 + 4ull * w;
+    const uintptr_t sA = (uintptr_t)((intptr_t)A + delta);
+    const uint32_t* sp = reinterpret_cast<const uint32_t*>(sA & ~uintptr_t(3));
+    const uint32_t v = __funnelshift_r(sp[0], sp[1], (uint32_t)(sA & 3u) * 8u);
+    const uint32_t lo = A < da ? (uint32_t)(da - A) : 0u;
+    const uint32_t hi = (A + 4 > da + n) ? (uint32_t)(da + n - A) : 4u;
+    uint32_t* p = reinterpret_cast<uint32_t*>(A);
+    if (lo == 0 && hi == 4) {
+      *p = v;
+    } else {
+      const uint32_t m = (hi == 4 ? 0xFFFFFFFFu : ((1u << (8 * hi)) - 1u)) & ~((1u << (8 * lo)) - 1u);
+      *p = (*p & ~m) | (v & m);
+    }
+  }
 }
 
 // ---- small helpers ------------------------------------------------------------
@@ -192,13 +273,16 @@ constexpr uint64_t kLbAgg = 1ull << 62;
 constexpr uint64_t kLbInc = 2ull << 62;
 constexpr uint64_t kLbMask = (1ull << 62) - 1;
 
+// The status word is self-contained (flag + count), so no memory fence is
+// needed: nothing else is communicated through the look-back.
 __device__ __forceinline__ void lb_publish(uint64_t* st, uint64_t tile, uint64_t flag, uint64_t v) {
-  __threadfence();
-  atomicExch(reinterpret_cast<unsigned long long*>(st + tile), (unsigned long long)(flag | v));
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(st + tile), "l"(flag | v) : "memory");
 }
 
 __device__ __forceinline__ uint64_t lb_load(const uint64_t* st, int64_t i) {
-  return *reinterpret_cast<const volatile uint64_t*>(st + i);
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(st + i) : "memory");
+  return v;
 }
 
 // Whole warp: returns the exclusive prefix of tile `tile` (tile 0 → 0).
@@ -208,22 +292,22 @@ __device__ __forceinline__ uint64_t lb_exclusive(const uint64_t* st, uint64_t ti
   uint64_t excl = 0;
   int64_t pos = (int64_t)tile - 1;
   while (pos >= 0) {
-    int64_t i = pos - (int64_t)lane;
+    const int64_t i = pos - (int64_t)lane;
     uint64_t s = 0;
-    uint32_t ready;
-    do {
+    uint32_t spins = 0;
+    while (true) {
       s = (i >= 0) ? lb_load(st, i) : kLbInc;
-      ready = __all_sync(0xFFFFFFFFu, (s >> 62) != 0);
-    } while (!ready);
-    uint32_t inc_mask = __ballot_sync(0xFFFFFFFFu, (s >> 62) == 2);
+      if (__all_sync(0xFFFFFFFFu, (s >> 62) != 0)) break;
+      if (++spins > 2) __nanosleep(64);
+    }
+    const uint32_t inc_mask = __ballot_sync(0xFFFFFFFFu, (s >> 62) == 2);
     // lanes up to and including the first inclusive one contribute
-    uint32_t first_inc = inc_mask ? (uint32_t)(__ffs(inc_mask) - 1) : 32u;
-    uint64_t contrib = (lane <= first_inc && i >= 0) ? (s & kLbMask) : 0;
+    const uint32_t first_inc = inc_mask ? (uint32_t)(__ffs(inc_mask) - 1) : 32u;
+    const uint64_t contrib = (lane <= first_inc && i >= 0) ? (s & kLbMask) : 0;
     excl += warp_sum(contrib);
     if (inc_mask) break;
     pos -= 32;
   }
-  __threadfence();
   return excl;
 }
 

@@ -5,25 +5,28 @@
 // work item (kernels.py:72-104), except that it emits fixed-width sort
 // records (luda_rec.cuh) with a value HANDLE instead of copying values.
 //
-// One warp per block, blocks taken in order from a global counter:
-//  1. stage the 16-byte-aligned window of the block into the warp's smem
-//     buffer (coalesced 16 B loads), blocks > kDecStageBytes are read in place;
-//  2. phase 1 — count entries. Fast path: lane k walks restart interval k
-//     (restart offsets from the block tail) and the walk is accepted only if
-//     every interval starts with shared == 0 and ends exactly on the next
-//     restart offset; then the sequential reference parse passes through the
-//     same entry boundaries and yields identical keys. Otherwise lane 0 runs
-//     the exact sequential reference parse (errors included);
-//  3. decoupled look-back over block order gives the block's first record
-//     index (single pass, no count kernel);
-//  4. warp CRC-32 of the payload (end-aligned segments, luda_common.cuh);
-//  5. phase 2 — lanes take consecutive entries; each loads its key suffix and
-//     the prefix bytes it shares are filled from earlier lanes by a
-//     Hillis-Steele scan over "valid-from" byte positions (shuffles only);
-//     records are written coalesced (lane i → record base+i).
+// One warp per block, blocks taken in order from a global counter. Per warp:
+//  * two smem staging buffers; while block b is processed, the 16-byte-aligned
+//    window of the next block is already in flight (cp.async.bulk + mbarrier);
+//    blocks longer than kDecStage are read in place from global memory;
+//  * phase 1 — entry walk. Fast path: lane k walks restart interval k
+//    (offsets from the block tail) with a 1–2-byte varint header decoder and
+//    records every entry (key-suffix position, shared, value length) in smem.
+//    It is accepted only if every interval starts with shared == 0 and ends
+//    exactly on the next restart offset — then the sequential reference parse
+//    passes through the same entry boundaries and yields identical keys.
+//    Otherwise lane 0 runs the exact sequential reference parse (errors
+//    included);
+//  * decoupled look-back over block order gives the block's first record
+//    index (single pass, no count kernel);
+//  * warp CRC-32 of the payload (end-aligned segments, luda_common.cuh);
+//  * phase 2 — lanes take consecutive entries; each loads its key suffix and
+//    the prefix bytes it shares are filled from earlier lanes by a
+//    Hillis-Steele scan over "valid-from" byte positions (shuffles only);
+//    records are written coalesced (lane i → record base+i).
 // Errors: reference errors → min((block << 8) | code) in err_ref; inputs that
 // are valid for the reference but outside the fixed-key-length envelope →
-// err_unsup (host raises those only if no reference error exists).
+// err_unsup (the host raises those only if no reference error exists).
 #pragma once
 #include "luda_parse.cuh"
 #include "luda_rec.cuh"
@@ -44,11 +47,12 @@ enum BlockCode : uint32_t {
 };
 
 constexpr int kDecWarps = 16;
-constexpr int kDecStageBytes = 8192;
-constexpr int kDecPre = 160;
-constexpr int kDecBuf = kDecPre + kDecStageBytes + 64;
-constexpr int kDecSlots = 256;
-constexpr int kDecWarpBytes = kDecBuf + kDecSlots * 8;
+constexpr int kDecStage = 4352;                  // staged window bytes (block + alignment)
+constexpr int kDecPre = 160;                     // CRC lead-in before the data
+constexpr int kDecBuf = kDecPre + kDecStage + 64;
+constexpr int kDecSlots = 128;
+constexpr int kDecStride = 16;                   // slots per restart interval (single-walk path)
+constexpr int kDecWarpBytes = 2 * kDecBuf + kDecSlots * 8 + 16;
 
 struct DecSlot {
   uint32_t pos;  // block-relative offset of the key suffix
@@ -70,6 +74,25 @@ struct DecodeArgs {
   unsigned long long* err_unsup;
 };
 
+// Entry header at pos: 1-byte shared and unshared, 1–2-byte value length.
+__device__ __forceinline__ bool hdr_fast(const uint8_t* d, uint64_t pos, uint64_t end, uint64_t& s, uint64_t& u,
+                                         uint64_t& vl, uint64_t& np) {
+  const uint32_t b0 = d[pos], b1 = d[pos + 1], b2 = d[pos + 2], b3 = d[pos + 3];
+  if ((b0 | b1) & 0x80u) return false;
+  if (!(b2 & 0x80u)) {
+    vl = b2;
+    np = pos + 3;
+  } else if (!(b3 & 0x80u)) {
+    vl = (b2 & 0x7Fu) | (b3 << 7);
+    np = pos + 4;
+  } else {
+    return false;
+  }
+  s = b0;
+  u = b1;
+  return np <= end;
+}
+
 // Walk one restart interval [start, end) under fast-path rules; calls
 // emit(j, pos_suffix, shared, vlen) per entry; returns entry count or -1.
 template <typename Emit>
@@ -78,8 +101,12 @@ __device__ __forceinline__ int64_t interval_walk(const uint8_t* d, uint64_t star
   uint64_t pos = start;
   int64_t j = 0;
   while (pos < end) {
-    uint64_t s, u, vl;
-    if (varint_read(d, end, pos, s) || varint_read(d, end, pos, u) || varint_read(d, end, pos, vl)) return -1;
+    uint64_t s, u, vl, np;
+    if (hdr_fast(d, pos, end, s, u, vl, np)) {
+      pos = np;
+    } else if (varint_read(d, end, pos, s) || varint_read(d, end, pos, u) || varint_read(d, end, pos, vl)) {
+      return -1;
+    }
     if (j == 0 ? s != 0 : s > K) return -1;
     if (u != (uint64_t)K - s || vl > kMaxValueLen) return -1;
     if (u > end || vl > end || pos + u + vl > end) return -1;
@@ -120,26 +147,52 @@ __device__ uint32_t block_walk_exact(const uint8_t* d, uint64_t payload, uint64_
   return pos != entries_end ? B_TRAILING : B_OK;
 }
 
+struct DecWarp {
+  uint8_t* buf[2];
+  uint64_t* bar[2];
+  uint32_t phase[2];
+  DecSlot* slots;
+};
+
+__device__ __forceinline__ uint32_t dec_window(const uint8_t* g, uint32_t len) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(g);
+  return (uint32_t)(((a + len + 15) & ~uintptr_t(15)) - (a & ~uintptr_t(15)));
+}
+
+// Issue the TMA staging of block b into buffer `which` (lane 0). Returns
+// whether the block is staged (else it is read in place).
 template <int W>
-__device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_t b, uint8_t* wbuf,
-                                                 DecSlot* slots, const CrcSmem& cs) {
+__device__ __forceinline__ bool dec_prefetch(const DecodeArgs<W>& a, uint32_t b, DecWarp& w, int which) {
+  if (b >= a.nblk) return false;
+  const uint32_t len = a.bt.len[b];
+  const uint8_t* g = a.arena + a.bt.addr[b];
+  const uint32_t win = dec_window(g, len);
+  if (len < 12 || win > (uint32_t)kDecStage) return false;
+  if (lane_id() == 0) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(w.bar[which], win);
+    bulk_g2s(w.buf[which] + kDecPre, reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(g) & ~uintptr_t(15)),
+             win, w.bar[which]);
+  }
+  return true;
+}
+
+template <int W>
+__device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_t b, bool staged, DecWarp& w,
+                                                 int which, const CrcSmem& cs) {
   constexpr int NW = 2 * W + 2;
   const uint32_t lane = lane_id();
   const uint32_t len = a.bt.len[b];
   const uint64_t addr = a.bt.addr[b];
   const uint32_t K = a.K;
-  const bool staged = len <= (uint32_t)kDecStageBytes;
   const uint8_t* g = a.arena + addr;
   const uint8_t* d = g;
-  if (len >= 12 && staged) {
-    const uintptr_t w0 = reinterpret_cast<uintptr_t>(g) & ~uintptr_t(15);
-    const uintptr_t w1 = (reinterpret_cast<uintptr_t>(g) + len + 15) & ~uintptr_t(15);
-    const uint32_t nch = (uint32_t)((w1 - w0) >> 4);
-    uint4* dst = reinterpret_cast<uint4*>(wbuf + kDecPre);
-    for (uint32_t c = lane; c < nch; c += 32) dst[c] = *reinterpret_cast<const uint4*>(w0 + 16ull * c);
-    __syncwarp();
-    d = wbuf + kDecPre + (reinterpret_cast<uintptr_t>(g) & 15);
+  if (staged) {
+    mbar_wait(w.bar[which], w.phase[which]);
+    w.phase[which] ^= 1u;
+    d = w.buf[which] + kDecPre + (reinterpret_cast<uintptr_t>(g) & 15);
   }
+  DecSlot* slots = w.slots;
   uint32_t code = len < 12 ? (uint32_t)B_SHORT : 0u;
   uint32_t nres = 0;
   int64_t entries_end = 0;
@@ -149,30 +202,40 @@ __device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_
     entries_end = (int64_t)len - 8 - 4 * (int64_t)nres;
     restart_bad = nres < 1 || entries_end < 0;
   }
-  // ---- phase 1: count -------------------------------------------------------
-  bool fast = false;
+  // ---- phase 1: walk --------------------------------------------------------
+  // mode 1: single walk, interval k's entries in slots [16k, 16k + cnt_k)
+  // mode 2: fast intervals, entries re-walked per window (dense slots)
+  // mode 3: exact sequential walk (lane 0)
+  int mode = 3;
   uint64_t n = 0;
   uint32_t pcode = 0, unsup = 0;
-  int64_t my_cnt = 0, my_pre = 0;  // fast path: this lane's interval (lane < nres)
+  int64_t my_cnt = 0, my_pre = 0;
+  uint64_t my_st = 0, my_en = 0;
   if (!code && !restart_bad) {
     if (nres <= 32) {
       bool ok = true;
+      const bool single = nres <= (uint32_t)(kDecSlots / kDecStride);
       if (lane < nres) {
-        const uint64_t st = ld_u32_le(d + entries_end + 4 * lane);
-        const uint64_t en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint64_t)entries_end;
-        ok = (lane != 0 || st == 0) && st < en && en <= (uint64_t)entries_end;
+        my_st = ld_u32_le(d + entries_end + 4 * lane);
+        my_en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint64_t)entries_end;
+        ok = (lane != 0 || my_st == 0) && my_st < my_en && my_en <= (uint64_t)entries_end;
         if (ok) {
-          my_cnt = interval_walk(d, st, en, K, [](int64_t, uint32_t, uint32_t, uint32_t) {});
+          DecSlot* mine = slots + kDecStride * lane;
+          my_cnt = interval_walk(d, my_st, my_en, K, [&](int64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+            if (single && j < kDecStride) mine[j] = DecSlot{pos, (vl << 8) | s};
+          });
           ok = my_cnt >= 0;
         }
       }
-      fast = __all_sync(0xFFFFFFFFu, ok);
+      if (__all_sync(0xFFFFFFFFu, ok)) {
+        const int64_t c = lane < nres ? my_cnt : 0;
+        const int64_t incl = warp_incl_scan<int64_t>(c);
+        my_pre = incl - c;
+        n = (uint64_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
+        mode = (single && __all_sync(0xFFFFFFFFu, c <= kDecStride)) ? 1 : 2;
+      }
     }
-    if (fast) {
-      const int64_t incl = warp_incl_scan<int64_t>(lane < nres ? my_cnt : 0);
-      my_pre = incl - (lane < nres ? my_cnt : 0);
-      n = (uint64_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
-    } else {
+    if (mode == 3) {
       uint64_t nn = 0;
       uint32_t pc = 0, us = 0;
       if (lane == 0)
@@ -199,53 +262,61 @@ __device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_
     } else {
       const uint64_t np = ((uint64_t)len - 4 + kGroup - 1) / kGroup;
       uint32_t raw = 0;
-      for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(g, len - 4, q, wbuf, cs);
+      for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(g, len - 4, q, w.buf[which], cs);
       crc = ~raw;
     }
     if (crc != ld_u32_le(d + len - 4)) code = B_CRC;
     else if (restart_bad) code = B_RESTART;
     else code = pcode;
   }
-  if (code) {
-    if (lane == 0) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
+  if (code || unsup || excl + n > a.cap) {  // capacity overflow: the host re-runs with exact capacity
+    if (lane == 0 && code) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
+    if (lane == 0 && !code && unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | unsup);
+    fence_proxy_async_smem();
+    __syncwarp();
     return;
   }
-  if (unsup) {
-    if (lane == 0) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | unsup);
-    return;
-  }
-  if (excl + n > a.cap) return;  // host re-runs with exact capacity
   // ---- phase 2: records ------------------------------------------------------
   const uint32_t L = K - 8;
   uint32_t carry[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) carry[i] = 0;
-  for (uint64_t w0 = 0; w0 < n; w0 += kDecSlots) {
+  const uint64_t wstep = mode == 1 ? n : (uint64_t)kDecSlots;
+  for (uint64_t w0 = 0; w0 < n; w0 += wstep) {
     const uint64_t w1 = w0 + kDecSlots;
-    auto put = [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
-      if (j >= w0 && j < w1) slots[j - w0] = DecSlot{pos, (vl << 8) | s};
-    };
-    if (fast) {
-      if (lane < nres) {
-        const uint64_t st = ld_u32_le(d + entries_end + 4 * lane);
-        const uint64_t en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint64_t)entries_end;
-        const int64_t pre = my_pre;
-        if ((uint64_t)(pre + my_cnt) > w0 && (uint64_t)pre < w1)
-          interval_walk(d, st, en, K, [&](int64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+    if (mode != 1) {
+      auto put = [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+        if (j >= w0 && j < w1) slots[j - w0] = DecSlot{pos, (vl << 8) | s};
+      };
+      __syncwarp();
+      if (mode == 2) {
+        if (lane < nres && (uint64_t)(my_pre + my_cnt) > w0 && (uint64_t)my_pre < w1) {
+          const int64_t pre = my_pre;
+          interval_walk(d, my_st, my_en, K, [&](int64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
             put((uint64_t)(pre + j), pos, s, vl);
           });
+        }
+      } else if (lane == 0) {
+        uint64_t nn;
+        uint32_t us;
+        block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us, put);
       }
-    } else if (lane == 0) {
-      uint64_t nn;
-      uint32_t us;
-      block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us, put);
     }
     __syncwarp();
-    const uint32_t wn = (uint32_t)((n - w0) < (uint64_t)kDecSlots ? (n - w0) : (uint64_t)kDecSlots);
+    const uint32_t wn = (uint32_t)((n - w0) < wstep ? (n - w0) : wstep);
     for (uint32_t c0 = 0; c0 < wn; c0 += 32) {
       const uint32_t e = c0 + lane;
       const bool act = e < wn;
-      DecSlot sl = act ? slots[e] : DecSlot{0, 0};
+      uint32_t sidx = e;
+      if (mode == 1) {  // entry e lives in interval k with pre_k <= e < pre_{k+1}
+        uint32_t k = 0, pk = 0;
+        for (uint32_t kk = 1; kk < nres; ++kk) {
+          const uint32_t p = (uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_pre, kk);
+          if (p <= e) { k = kk; pk = p; }
+        }
+        sidx = kDecStride * k + (e - pk);
+      }
+      const DecSlot sl = act ? slots[sidx] : DecSlot{0, 0};
       const uint32_t s = sl.sv & 0xFFu;
       const uint32_t vl = sl.sv >> 8;
       uint32_t kw[NW];
@@ -299,25 +370,45 @@ __device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_
         a.out[excl + w0 + e] = r;
       }
     }
-    __syncwarp();
   }
+  fence_proxy_async_smem();  // generic smem writes of this block before the next TMA into these buffers
+  __syncwarp();
 }
 
 template <int W>
 __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
-  uint8_t* wbuf = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kDecWarpBytes;
-  DecSlot* slots = reinterpret_cast<DecSlot*>(wbuf + kDecBuf);
-  crc_smem_init(cs);
-  __syncthreads();
+  uint8_t* wb = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kDecWarpBytes;
+  DecWarp w;
+  w.buf[0] = wb;
+  w.buf[1] = wb + kDecBuf;
+  w.slots = reinterpret_cast<DecSlot*>(wb + 2 * kDecBuf);
+  w.bar[0] = reinterpret_cast<uint64_t*>(wb + 2 * kDecBuf + kDecSlots * 8);
+  w.bar[1] = w.bar[0] + 1;
+  w.phase[0] = w.phase[1] = 0;
   const uint32_t lane = lane_id();
-  while (true) {
-    uint32_t b = 0;
-    if (lane == 0) b = atomicAdd(a.tile_ctr, 1u);
-    b = __shfl_sync(0xFFFFFFFFu, b, 0);
-    if (b >= a.nblk) break;
-    decode_one_block<W>(a, b, wbuf, slots, cs);
+  crc_smem_init(cs);
+  if (lane == 0) {
+    mbar_init(w.bar[0], 1);
+    mbar_init(w.bar[1], 1);
+  }
+  __syncthreads();
+  // Static round-robin assignment over a fully resident grid (one CTA per
+  // SM): warp g owns blocks g, g + NW, g + 2NW, ... The next block is known
+  // up front, so its TMA prefetch never delays this warp's look-back publish
+  // (successor blocks depend on it); look-back waits are just inter-warp skew.
+  const uint32_t nw = gridDim.x * kDecWarps;
+  uint32_t cur = blockIdx.x * kDecWarps + (threadIdx.x >> 5);
+  int which = 0;
+  bool cur_staged = dec_prefetch(a, cur, w, which);
+  while (cur < a.nblk) {
+    const uint32_t nxt = cur + nw;
+    const bool nxt_staged = dec_prefetch(a, nxt, w, which ^ 1);
+    decode_one_block<W>(a, cur, cur_staged, w, which, cs);
+    cur = nxt;
+    cur_staged = nxt_staged;
+    which ^= 1;
   }
 }
 

@@ -26,9 +26,11 @@
 namespace luda {
 
 constexpr int kEncWarps = 16;
-constexpr int kEncStage = 8192;
+constexpr int kEncStage = 4608;                        // blocks up to this size are assembled in smem
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
+constexpr int kEncStg = 6144;                          // per-warp TMA staging for value windows
+constexpr int kEncWarpBytes = kEncBuf + kEncStg + 16;  // + mbarrier
 
 // Copy n bytes src → dst (any alignment; dst generic: smem or global) with
 // `nl` cooperating threads (rank `r`). Destination-aligned 32-bit words are
@@ -163,7 +165,8 @@ struct EncodeArgs {
 };
 
 template <int W>
-__device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_t k, uint8_t* wbuf, const CrcSmem& cs) {
+__device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_t k, uint8_t* wbuf, uint8_t* stg,
+                                                 uint64_t* bar, uint32_t& phase, const CrcSmem& cs) {
   const uint32_t lane = lane_id();
   const uint64_t first = a.blk_first[k];
   const uint32_t cnt = a.blk_n[k];
@@ -209,12 +212,43 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
       put_key_tail<W>(p + h, r, L, s);
       if (i % ri == 0) put_u32(dst + entries_end + 4 * (i / ri), off);
     }
-    // values: whole warp per entry
-    const uint32_t nact = cnt - c0 < 32 ? cnt - c0 : 32;
-    for (uint32_t j = 0; j < nact; ++j) {
+    __syncwarp();  // headers/keys written before values (edge words are read-modified-written)
+    // ---- values: TMA bulk copies of each entry's 16-byte-aligned source window
+    // into the warp's staging area (all in flight at once), then realigned
+    // smem→block. Windows larger than the staging area are copied directly.
+    const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + voff;
+    const uint32_t win = (act && vl) ? (uint32_t)(((vs + vl + 15) & ~uintptr_t(15)) - (vs & ~uintptr_t(15))) : 0u;
+    const uint32_t dpos = off + hv + u;
+    uint32_t pending = __ballot_sync(0xFFFFFFFFu, win != 0 && win <= (uint32_t)kEncStg);
+    while (pending) {
+      const uint32_t my = ((pending >> lane) & 1u) ? win : 0u;
+      const uint32_t inc = warp_incl_scan<uint32_t>(my);
+      const bool take = my != 0 && inc <= (uint32_t)kEncStg;
+      const uint32_t tmask = __ballot_sync(0xFFFFFFFFu, take);
+      const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31 - __clz(tmask));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(bar, total);
+      __syncwarp();
+      if (take) bulk_g2s(stg + inc - my, reinterpret_cast<const void*>(vs & ~uintptr_t(15)), my, bar);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+      const uint32_t soff = inc - my + (uint32_t)(vs & 15u);
+      for (uint32_t m = tmask; m; m &= m - 1) {
+        const uint32_t j = __ffs(m) - 1;
+        const uint32_t so = __shfl_sync(0xFFFFFFFFu, soff, j);
+        const uint32_t dp = __shfl_sync(0xFFFFFFFFu, dpos, j);
+        const uint32_t sl = __shfl_sync(0xFFFFFFFFu, vl, j);
+        warp_smem_copy(dst + dp, stg + so, sl, lane);
+      }
+      __syncwarp();
+      pending &= ~tmask;
+    }
+    for (uint32_t m = __ballot_sync(0xFFFFFFFFu, win > (uint32_t)kEncStg); m; m &= m - 1) {
+      const uint32_t j = __ffs(m) - 1;
       const uint64_t so = __shfl_sync(0xFFFFFFFFu, voff, j);
       const uint32_t sl = __shfl_sync(0xFFFFFFFFu, vl, j);
-      const uint32_t dp = __shfl_sync(0xFFFFFFFFu, off + hv + u, j);
+      const uint32_t dp = __shfl_sync(0xFFFFFFFFu, dpos, j);
       coop_copy(dst + dp, a.arena + so, sl, lane, 32);
     }
   }
@@ -237,14 +271,19 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
     const uintptr_t g = reinterpret_cast<uintptr_t>(a.out + out_off);
     const uintptr_t g0 = g & ~uintptr_t(15), g1 = (g + size + 15) & ~uintptr_t(15);
     const uint32_t nch = (uint32_t)((g1 - g0) >> 4);
-    for (uint32_t c = lane; c < nch; c += 32) {
-      const uintptr_t A = g0 + 16ull * c;
-      const uint8_t* sp = sbase + 16 * c;
-      if (A >= g && A + 16 <= g + size) {
-        *reinterpret_cast<uint4*>(A) = *reinterpret_cast<const uint4*>(sp);
-      } else {
+    // interior 16-byte chunks (fully inside the block)
+    const uint32_t c_first = (g0 == g) ? 0u : 1u;
+    const uint32_t c_last = ((g + size) & 15u) ? nch - 1 : nch;  // exclusive
+    for (uint32_t c = c_first + lane; c < c_last; c += 32)
+      *reinterpret_cast<uint4*>(g0 + 16ull * c) = *reinterpret_cast<const uint4*>(sbase + 16 * c);
+    // partial head / tail chunks: bytewise (neighbouring blocks own the rest)
+    if (lane < 2) {
+      const bool head = lane == 0;
+      const uint32_t c = head ? 0u : nch - 1;
+      if ((head && c_first == 1) || (!head && c_last == nch - 1 && !(c == 0 && c_first == 1))) {
+        const uintptr_t A = g0 + 16ull * c;
         for (int b = 0; b < 16; ++b)
-          if (A + b >= g && A + b < g + size) reinterpret_cast<uint8_t*>(A)[b] = sp[b];
+          if (A + b >= g && A + b < g + size) reinterpret_cast<uint8_t*>(A)[b] = sbase[16 * c + b];
       }
     }
   }
@@ -255,12 +294,16 @@ template <int W>
 __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
-  uint8_t* wbuf = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kEncBuf;
+  uint8_t* wbuf = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kEncWarpBytes;
+  uint8_t* stg = wbuf + kEncBuf;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kEncStg);
   crc_smem_init(cs);
+  if (lane_id() == 0) mbar_init(bar, 1);
   __syncthreads();
+  uint32_t phase = 0;
   const uint32_t gw = blockIdx.x * kEncWarps + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kEncWarps;
-  for (uint32_t k = gw; k < a.nblk; k += nw) encode_one_block<W>(a, k, wbuf, cs);
+  for (uint32_t k = gw; k < a.nblk; k += nw) encode_one_block<W>(a, k, wbuf, stg, bar, phase, cs);
 }
 
 // ---- per-SST filter + index + footer -----------------------------------------------------
