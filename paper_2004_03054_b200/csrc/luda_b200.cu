@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -55,27 +56,84 @@ int fail(int status, const std::string& msg, int64_t off = -1) {
       return fail(LUDA_DEVICE, std::string(#expr " failed: ") + cudaGetErrorString(e_)); \
   } while (0)
 
-// Stream-ordered scratch allocations released together.
+// Persistent device workspace: a bump allocator over cudaMalloc'd chunks
+// that is reset at the start of every job, so steady-state jobs do no device
+// allocation at all (multi-GB scratch would otherwise be re-mapped per job).
+struct Workspace {
+  struct Chunk {
+    char* p;
+    uint64_t size, used;
+  };
+  std::vector<Chunk> chunks;
+  void reset() {
+    for (auto& c : chunks) c.used = 0;
+  }
+  void* get(uint64_t bytes) {
+    bytes = (bytes + 255) & ~uint64_t(255);
+    for (auto& c : chunks)
+      if (c.size - c.used >= bytes) {
+        void* p = c.p + c.used;
+        c.used += bytes;
+        return p;
+      }
+    const uint64_t sz = std::max<uint64_t>(bytes, 256ull << 20);
+    void* p = nullptr;
+    if (cudaMalloc(&p, sz) != cudaSuccess) return nullptr;
+    chunks.push_back({reinterpret_cast<char*>(p), sz, bytes});
+    return p;
+  }
+  void release_all() {
+    for (auto& c : chunks) cudaFree(c.p);
+    chunks.clear();
+  }
+};
+Workspace g_ws;
+
+// Output buffers handed to the caller (luda_job_result.out); recycled by
+// luda_job_release.
+struct OutCache {
+  struct Buf {
+    void* p;
+    uint64_t size;
+    bool used;
+  };
+  std::vector<Buf> bufs;
+  void* get(uint64_t bytes) {
+    Buf* best = nullptr;
+    for (auto& b : bufs)
+      if (!b.used && b.size >= bytes && (!best || b.size < best->size)) best = &b;
+    if (best) {
+      best->used = true;
+      return best->p;
+    }
+    void* p = nullptr;
+    const uint64_t sz = bytes + (bytes >> 3) + 4096;
+    if (cudaMalloc(&p, sz) != cudaSuccess) return nullptr;
+    bufs.push_back({p, sz, true});
+    return p;
+  }
+  bool put(void* p) {
+    for (auto& b : bufs)
+      if (b.p == p) {
+        b.used = false;
+        return true;
+      }
+    return false;
+  }
+};
+OutCache g_out;
+std::mutex g_job_mu;  // one job at a time per process (shared workspace)
+
 struct Scratch {
   cudaStream_t st;
-  std::vector<void*> ptrs;
-  explicit Scratch(cudaStream_t s) : st(s) {}
-  ~Scratch() {
-    for (void* p : ptrs) cudaFreeAsync(p, st);
-  }
+  explicit Scratch(cudaStream_t s) : st(s) { g_ws.reset(); }
   template <typename T>
   T* get(uint64_t count, bool zero = false) {
-    void* p = nullptr;
     const uint64_t bytes = std::max<uint64_t>(count * sizeof(T), 16) + 256;
-    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) return nullptr;
-    ptrs.push_back(p);
+    void* p = g_ws.get(bytes);
+    if (!p) return nullptr;
     if (zero) cudaMemsetAsync(p, 0, bytes, st);
     return reinterpret_cast<T*>(p);
-  }
-  void* release_last() {
-    void* p = ptrs.back();
-    ptrs.pop_back();
-    return p;
   }
 };
 
@@ -410,8 +468,8 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
       big_words += (nbits / 8 + 1 + 3) / 4 + 8;
     }
   }
-  void* outp = nullptr;
-  CK(cudaMallocAsync(&outp, total + 256, st));
+  void* outp = g_out.get(total + 256);
+  if (!outp) return fail(LUDA_DEVICE, "output allocation failed");
   priv->st = st;
   res->out = reinterpret_cast<uint8_t*>(outp);
   res->out_bytes = total;
@@ -650,6 +708,10 @@ int luda_init(int device_ordinal) {
 
 int luda_shutdown(void) {
   if (g_device >= 0) cudaDeviceSynchronize();
+  {
+    std::lock_guard<std::mutex> lock(g_job_mu);
+    g_ws.release_all();
+  }
   g_device = -1;
   return LUDA_OK;
 }
@@ -781,12 +843,8 @@ int luda_job_release(luda_job_result* r) {
   if (!r) return LUDA_OK;
   JobPriv* priv = reinterpret_cast<JobPriv*>(r->priv);
   if (r->out) {
-    if (priv && priv->st) {
-      cudaStreamSynchronize(priv->st);
-      cudaFreeAsync(r->out, priv->st);
-    } else {
-      cudaFree(r->out);
-    }
+    if (priv && priv->st) cudaStreamSynchronize(priv->st);
+    if (!g_out.put(r->out)) cudaFree(r->out);
   }
   delete priv;
   memset(r, 0, sizeof(*r));
@@ -798,6 +856,7 @@ int luda_build_from_sorted(const uint8_t* keys, uint32_t L, const uint64_t* trai
                            uint32_t restart_interval, uint32_t bits_per_key, uint64_t sst_size_target,
                            luda_job_result* res, void* stream) {
   if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
+  std::lock_guard<std::mutex> lock(g_job_mu);
   memset(res, 0, sizeof(*res));
   if (L > 32) return fail(LUDA_UNSUPPORTED, "user keys longer than 32 bytes");
   if (restart_interval < 1) return fail(LUDA_DEVICE, "restart_interval must be >= 1");
@@ -828,6 +887,7 @@ int luda_dispatch(int kind, const int64_t* items, uint32_t n_items, void* const*
 
 int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
+  std::lock_guard<std::mutex> lock(g_job_mu);
   memset(res, 0, sizeof(*res));
   cudaStream_t st = (cudaStream_t)stream;
   KTimer kt;

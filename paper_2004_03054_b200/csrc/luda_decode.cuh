@@ -52,7 +52,7 @@ constexpr int kDecPre = 160;                     // CRC lead-in before the data
 constexpr int kDecBuf = kDecPre + kDecStage + 64;
 constexpr int kDecSlots = 128;
 constexpr int kDecStride = 16;                   // slots per restart interval (single-walk path)
-constexpr int kDecWarpBytes = 2 * kDecBuf + kDecSlots * 8 + 16;
+constexpr int kDecWarpBytes = 2 * kDecBuf + 2 * kDecSlots * 8 + 16;  // 2 = kDecTile
 
 struct DecSlot {
   uint32_t pos;  // block-relative offset of the key suffix
@@ -74,47 +74,37 @@ struct DecodeArgs {
   unsigned long long* err_unsup;
 };
 
-// Entry header at pos: 1-byte shared and unshared, 1–2-byte value length.
-__device__ __forceinline__ bool hdr_fast(const uint8_t* d, uint64_t pos, uint64_t end, uint64_t& s, uint64_t& u,
-                                         uint64_t& vl, uint64_t& np) {
-  const uint32_t b0 = d[pos], b1 = d[pos + 1], b2 = d[pos + 2], b3 = d[pos + 3];
-  if ((b0 | b1) & 0x80u) return false;
-  if (!(b2 & 0x80u)) {
-    vl = b2;
-    np = pos + 3;
-  } else if (!(b3 & 0x80u)) {
-    vl = (b2 & 0x7Fu) | (b3 << 7);
-    np = pos + 4;
-  } else {
-    return false;
-  }
-  s = b0;
-  u = b1;
-  return np <= end;
-}
-
-// Walk one restart interval [start, end) under fast-path rules; calls
-// emit(j, pos_suffix, shared, vlen) per entry; returns entry count or -1.
+// Walk one restart interval [start, end) under fast-path rules and call
+// emit(j, pos_suffix, shared, vlen) per entry; returns the entry count or -1
+// when the interval is not in canonical form (the exact path then decides).
+// Fast form: 1-byte shared/unshared varints, 1–2-byte value length,
+// shared + unshared == K (so shared <= len(prev key) == K), shared == 0 on the
+// interval's first entry, entries tiling [start, end) exactly.
 template <typename Emit>
-__device__ __forceinline__ int64_t interval_walk(const uint8_t* d, uint64_t start, uint64_t end, uint32_t K,
+__device__ __forceinline__ int32_t interval_walk(const uint8_t* d, uint32_t start, uint32_t end, uint32_t K,
                                                  Emit emit) {
-  uint64_t pos = start;
-  int64_t j = 0;
+  uint32_t pos = start;
+  int32_t j = 0;
   while (pos < end) {
-    uint64_t s, u, vl, np;
-    if (hdr_fast(d, pos, end, s, u, vl, np)) {
-      pos = np;
-    } else if (varint_read(d, end, pos, s) || varint_read(d, end, pos, u) || varint_read(d, end, pos, vl)) {
+    const uint32_t b0 = d[pos], b1 = d[pos + 1], b2 = d[pos + 2], b3 = d[pos + 3];
+    uint32_t vl, hl;
+    if (((b0 | b1 | b2) & 0x80u) == 0) {
+      vl = b2;
+      hl = 3;
+    } else if (((b0 | b1 | b3) & 0x80u) == 0) {
+      vl = (b2 & 0x7Fu) | (b3 << 7);
+      hl = 4;
+    } else {
       return -1;
     }
-    if (j == 0 ? s != 0 : s > K) return -1;
-    if (u != (uint64_t)K - s || vl > kMaxValueLen) return -1;
-    if (u > end || vl > end || pos + u + vl > end) return -1;
-    emit(j, (uint32_t)pos, (uint32_t)s, (uint32_t)vl);
-    pos += u + vl;
+    if ((j == 0 && b0 != 0) || b0 + b1 != K) return -1;
+    const uint32_t np = pos + hl + b1 + vl;
+    if (np > end) return -1;
+    emit(j, pos + hl, b0, vl);
+    pos = np;
     ++j;
   }
-  return pos == end ? j : -1;
+  return j;
 }
 
 // Exact sequential decode_data_block walk (blocks.py:151-164). Returns the
@@ -147,17 +137,37 @@ __device__ uint32_t block_walk_exact(const uint8_t* d, uint64_t payload, uint64_
   return pos != entries_end ? B_TRAILING : B_OK;
 }
 
+constexpr int kDecTile = 2;  // consecutive blocks per warp tile (one look-back per tile)
+
 struct DecWarp {
-  uint8_t* buf[2];
-  uint64_t* bar[2];
-  uint32_t phase[2];
-  DecSlot* slots;
+  uint8_t* buf[kDecTile];
+  uint64_t* bar[kDecTile];
+  uint32_t phase[kDecTile];
+  DecSlot* slots[kDecTile];
 };
 
 __device__ __forceinline__ uint32_t dec_window(const uint8_t* g, uint32_t len) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(g);
   return (uint32_t)(((a + len + 15) & ~uintptr_t(15)) - (a & ~uintptr_t(15)));
 }
+
+// Per-block state carried from phase 1 to phase 2.
+struct DecState {
+  const uint8_t* d;       // block bytes (smem staging or global)
+  uint64_t addr;          // arena offset of the block
+  uint32_t len;
+  uint32_t nres;
+  int64_t entries_end;
+  uint32_t code;          // reference error so far (before CRC)
+  uint32_t restart_bad;
+  uint32_t pcode, unsup;
+  int mode;               // 1 single walk, 2 fast windows, 3 exact walk
+  uint64_t n;
+  int32_t my_cnt, my_pre;
+  uint32_t my_st, my_en;
+  bool staged;
+  bool valid;
+};
 
 // Issue the TMA staging of block b into buffer `which` (lane 0). Returns
 // whether the block is staged (else it is read in place).
@@ -177,107 +187,110 @@ __device__ __forceinline__ bool dec_prefetch(const DecodeArgs<W>& a, uint32_t b,
   return true;
 }
 
+// Phase 1: structural checks + entry walk (counts; single-walk fills slots).
 template <int W>
-__device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_t b, bool staged, DecWarp& w,
-                                                 int which, const CrcSmem& cs) {
-  constexpr int NW = 2 * W + 2;
+__device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t b, bool staged, DecWarp& w,
+                                               int which) {
   const uint32_t lane = lane_id();
-  const uint32_t len = a.bt.len[b];
-  const uint64_t addr = a.bt.addr[b];
+  DecState st{};
+  st.valid = b < a.nblk;
+  if (!st.valid) return st;
+  st.len = a.bt.len[b];
+  st.addr = a.bt.addr[b];
+  st.staged = staged;
   const uint32_t K = a.K;
-  const uint8_t* g = a.arena + addr;
+  const uint8_t* g = a.arena + st.addr;
   const uint8_t* d = g;
   if (staged) {
     mbar_wait(w.bar[which], w.phase[which]);
     w.phase[which] ^= 1u;
     d = w.buf[which] + kDecPre + (reinterpret_cast<uintptr_t>(g) & 15);
   }
-  DecSlot* slots = w.slots;
-  uint32_t code = len < 12 ? (uint32_t)B_SHORT : 0u;
-  uint32_t nres = 0;
-  int64_t entries_end = 0;
-  bool restart_bad = false;
-  if (!code) {
-    nres = ld_u32_le(d + len - 8);
-    entries_end = (int64_t)len - 8 - 4 * (int64_t)nres;
-    restart_bad = nres < 1 || entries_end < 0;
+  st.d = d;
+  DecSlot* slots = w.slots[which];
+  const uint32_t len = st.len;
+  st.code = len < 12 ? (uint32_t)B_SHORT : 0u;
+  if (!st.code) {
+    st.nres = ld_u32_le(d + len - 8);
+    st.entries_end = (int64_t)len - 8 - 4 * (int64_t)st.nres;
+    st.restart_bad = st.nres < 1 || st.entries_end < 0;
   }
-  // ---- phase 1: walk --------------------------------------------------------
-  // mode 1: single walk, interval k's entries in slots [16k, 16k + cnt_k)
-  // mode 2: fast intervals, entries re-walked per window (dense slots)
-  // mode 3: exact sequential walk (lane 0)
-  int mode = 3;
-  uint64_t n = 0;
-  uint32_t pcode = 0, unsup = 0;
-  int64_t my_cnt = 0, my_pre = 0;
-  uint64_t my_st = 0, my_en = 0;
-  if (!code && !restart_bad) {
+  st.mode = 3;
+  if (!st.code && !st.restart_bad) {
+    const uint32_t nres = st.nres;
+    const int64_t entries_end = st.entries_end;
     if (nres <= 32) {
       bool ok = true;
       const bool single = nres <= (uint32_t)(kDecSlots / kDecStride);
       if (lane < nres) {
-        my_st = ld_u32_le(d + entries_end + 4 * lane);
-        my_en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint64_t)entries_end;
-        ok = (lane != 0 || my_st == 0) && my_st < my_en && my_en <= (uint64_t)entries_end;
+        st.my_st = ld_u32_le(d + entries_end + 4 * lane);
+        st.my_en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint32_t)entries_end;
+        ok = (lane != 0 || st.my_st == 0) && st.my_st < st.my_en && (int64_t)st.my_en <= entries_end;
         if (ok) {
           DecSlot* mine = slots + kDecStride * lane;
-          my_cnt = interval_walk(d, my_st, my_en, K, [&](int64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+          st.my_cnt = interval_walk(d, st.my_st, st.my_en, K, [&](int32_t j, uint32_t pos, uint32_t s, uint32_t vl) {
             if (single && j < kDecStride) mine[j] = DecSlot{pos, (vl << 8) | s};
           });
-          ok = my_cnt >= 0;
+          ok = st.my_cnt >= 0;
         }
       }
       if (__all_sync(0xFFFFFFFFu, ok)) {
-        const int64_t c = lane < nres ? my_cnt : 0;
-        const int64_t incl = warp_incl_scan<int64_t>(c);
-        my_pre = incl - c;
-        n = (uint64_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
-        mode = (single && __all_sync(0xFFFFFFFFu, c <= kDecStride)) ? 1 : 2;
+        const int32_t c = lane < nres ? st.my_cnt : 0;
+        const int32_t incl = warp_incl_scan<int32_t>(c);
+        st.my_pre = incl - c;
+        st.n = (uint64_t)(uint32_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
+        st.mode = (single && __all_sync(0xFFFFFFFFu, c <= kDecStride)) ? 1 : 2;
       }
     }
-    if (mode == 3) {
+    if (st.mode == 3) {
       uint64_t nn = 0;
       uint32_t pc = 0, us = 0;
       if (lane == 0)
         pc = block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us,
                               [](uint64_t, uint32_t, uint32_t, uint32_t) {});
-      n = __shfl_sync(0xFFFFFFFFu, nn, 0);
-      pcode = __shfl_sync(0xFFFFFFFFu, pc, 0);
-      unsup = __shfl_sync(0xFFFFFFFFu, us, 0);
+      st.n = __shfl_sync(0xFFFFFFFFu, nn, 0);
+      st.pcode = __shfl_sync(0xFFFFFFFFu, pc, 0);
+      st.unsup = __shfl_sync(0xFFFFFFFFu, us, 0);
     }
   }
-  // ---- look-back: first record index of this block --------------------------
-  if (lane == 0) lb_publish(a.lb, b, kLbAgg, n);
-  const uint64_t excl = lb_exclusive(a.lb, b);
-  if (lane == 0) {
-    lb_publish(a.lb, b, kLbInc, excl + n);
-    a.blk_base[b] = excl;
-    if (b + 1 == a.nblk) a.blk_base[a.nblk] = excl + n;
-  }
-  // ---- CRC ------------------------------------------------------------------
+  return st;
+}
+
+// Phase 2: CRC verify, then records at out[base ...].
+template <int W>
+__device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, DecState& st, uint64_t base,
+                                           DecWarp& w, int which, const CrcSmem& cs) {
+  constexpr int NW = 2 * W + 2;
+  const uint32_t lane = lane_id();
+  const uint32_t K = a.K;
+  const uint8_t* d = st.d;
+  const uint32_t len = st.len;
+  DecSlot* slots = w.slots[which];
+  uint32_t code = st.code;
   if (!code) {
     uint32_t crc;
-    if (staged) {
+    if (st.staged) {
       crc = warp_crc32_smem(d, len - 4, cs);
     } else {
+      const uint8_t* g = a.arena + st.addr;
       const uint64_t np = ((uint64_t)len - 4 + kGroup - 1) / kGroup;
       uint32_t raw = 0;
       for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(g, len - 4, q, w.buf[which], cs);
       crc = ~raw;
     }
     if (crc != ld_u32_le(d + len - 4)) code = B_CRC;
-    else if (restart_bad) code = B_RESTART;
-    else code = pcode;
+    else if (st.restart_bad) code = B_RESTART;
+    else code = st.pcode;
   }
-  if (code || unsup || excl + n > a.cap) {  // capacity overflow: the host re-runs with exact capacity
+  const uint64_t n = st.n;
+  if (code || st.unsup || base + n > a.cap) {  // capacity overflow: the host re-runs with exact capacity
     if (lane == 0 && code) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
-    if (lane == 0 && !code && unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | unsup);
-    fence_proxy_async_smem();
-    __syncwarp();
+    if (lane == 0 && !code && st.unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | st.unsup);
     return;
   }
-  // ---- phase 2: records ------------------------------------------------------
   const uint32_t L = K - 8;
+  const int mode = st.mode;
+  const uint32_t nres = st.nres;
   uint32_t carry[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) carry[i] = 0;
@@ -290,16 +303,16 @@ __device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_
       };
       __syncwarp();
       if (mode == 2) {
-        if (lane < nres && (uint64_t)(my_pre + my_cnt) > w0 && (uint64_t)my_pre < w1) {
-          const int64_t pre = my_pre;
-          interval_walk(d, my_st, my_en, K, [&](int64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+        if (lane < nres && (uint64_t)(st.my_pre + st.my_cnt) > w0 && (uint64_t)st.my_pre < w1) {
+          const int32_t pre = st.my_pre;
+          interval_walk(d, st.my_st, st.my_en, K, [&](int32_t j, uint32_t pos, uint32_t s, uint32_t vl) {
             put((uint64_t)(pre + j), pos, s, vl);
           });
         }
       } else if (lane == 0) {
         uint64_t nn;
         uint32_t us;
-        block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us, put);
+        block_walk_exact(d, len - 4, (uint64_t)st.entries_end, K, nn, us, put);
       }
     }
     __syncwarp();
@@ -311,7 +324,7 @@ __device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_
       if (mode == 1) {  // entry e lives in interval k with pre_k <= e < pre_{k+1}
         uint32_t k = 0, pk = 0;
         for (uint32_t kk = 1; kk < nres; ++kk) {
-          const uint32_t p = (uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)my_pre, kk);
+          const uint32_t p = (uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)st.my_pre, kk);
           if (p <= e) { k = kk; pk = p; }
         }
         sidx = kDecStride * k + (e - pk);
@@ -365,14 +378,12 @@ __device__ __forceinline__ void decode_one_block(const DecodeArgs<W>& a, uint32_
       if (act) {
         Rec<W> r;
         words_to_rec<W, NW>(kw, L, r);
-        const uint64_t voff = addr + sl.pos + (K - s);
+        const uint64_t voff = st.addr + sl.pos + (K - s);
         r.h = handle_pack(voff, vl);
-        a.out[excl + w0 + e] = r;
+        a.out[base + w0 + e] = r;
       }
     }
   }
-  fence_proxy_async_smem();  // generic smem writes of this block before the next TMA into these buffers
-  __syncwarp();
 }
 
 template <int W>
@@ -381,34 +392,53 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
   uint8_t* wb = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kDecWarpBytes;
   DecWarp w;
-  w.buf[0] = wb;
-  w.buf[1] = wb + kDecBuf;
-  w.slots = reinterpret_cast<DecSlot*>(wb + 2 * kDecBuf);
-  w.bar[0] = reinterpret_cast<uint64_t*>(wb + 2 * kDecBuf + kDecSlots * 8);
-  w.bar[1] = w.bar[0] + 1;
-  w.phase[0] = w.phase[1] = 0;
+#pragma unroll
+  for (int i = 0; i < kDecTile; ++i) {
+    w.buf[i] = wb + i * kDecBuf;
+    w.slots[i] = reinterpret_cast<DecSlot*>(wb + kDecTile * kDecBuf) + i * kDecSlots;
+    w.bar[i] = reinterpret_cast<uint64_t*>(wb + kDecTile * kDecBuf + kDecTile * kDecSlots * 8) + i;
+    w.phase[i] = 0;
+  }
   const uint32_t lane = lane_id();
   crc_smem_init(cs);
-  if (lane == 0) {
-    mbar_init(w.bar[0], 1);
-    mbar_init(w.bar[1], 1);
-  }
+  if (lane == 0)
+    for (int i = 0; i < kDecTile; ++i) mbar_init(w.bar[i], 1);
   __syncthreads();
-  // Static round-robin assignment over a fully resident grid (one CTA per
-  // SM): warp g owns blocks g, g + NW, g + 2NW, ... The next block is known
-  // up front, so its TMA prefetch never delays this warp's look-back publish
-  // (successor blocks depend on it); look-back waits are just inter-warp skew.
-  const uint32_t nw = gridDim.x * kDecWarps;
-  uint32_t cur = blockIdx.x * kDecWarps + (threadIdx.x >> 5);
-  int which = 0;
-  bool cur_staged = dec_prefetch(a, cur, w, which);
-  while (cur < a.nblk) {
-    const uint32_t nxt = cur + nw;
-    const bool nxt_staged = dec_prefetch(a, nxt, w, which ^ 1);
-    decode_one_block<W>(a, cur, cur_staged, w, which, cs);
-    cur = nxt;
-    cur_staged = nxt_staged;
-    which ^= 1;
+  const uint32_t ntiles = (a.nblk + kDecTile - 1) / kDecTile;
+  while (true) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(a.tile_ctr, 1u);
+    t = __shfl_sync(0xFFFFFFFFu, t, 0);
+    if (t >= ntiles) break;
+    const uint32_t b0 = t * kDecTile;
+    bool staged[kDecTile];
+#pragma unroll
+    for (int i = 0; i < kDecTile; ++i) staged[i] = dec_prefetch(a, b0 + i, w, i);
+    DecState st[kDecTile];
+    uint64_t tot = 0;
+#pragma unroll
+    for (int i = 0; i < kDecTile; ++i) {
+      st[i] = dec_phase1(a, b0 + i, staged[i], w, i);
+      tot += st[i].n;
+    }
+    if (lane == 0) lb_publish(a.lb, t, kLbAgg, tot);
+    const uint64_t excl = lb_exclusive(a.lb, t);
+    if (lane == 0) lb_publish(a.lb, t, kLbInc, excl + tot);
+    uint64_t base = excl;
+#pragma unroll
+    for (int i = 0; i < kDecTile; ++i) {
+      const uint32_t b = b0 + i;
+      if (st[i].valid) {
+        if (lane == 0) {
+          a.blk_base[b] = base;
+          if (b + 1 == a.nblk) a.blk_base[a.nblk] = base + st[i].n;
+        }
+        dec_phase2(a, b, st[i], base, w, i, cs);
+        base += st[i].n;
+      }
+    }
+    fence_proxy_async_smem();  // generic smem accesses before the next TMA into these buffers
+    __syncwarp();
   }
 }
 
