@@ -516,7 +516,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   const uint32_t L = K - 8;
   res->blocks_in = nblk;
   // ---- decode ----
-  uint64_t cap = std::max<uint64_t>(bound, 1);
+  (void)bound;
   GET(d_base, uint64_t, nblk + 1, false);
   GET(errs, unsigned long long, 2, false);
   const size_t dsm = sizeof(CrcSmem) + (size_t)kDecWarps * kDecWarpBytes;
@@ -524,25 +524,39 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   Rec<W>* X = nullptr;
   uint64_t n_in = 0;
   std::vector<uint64_t> fbase(jd->n_files + 1);
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    X = scratch.get<Rec<W>>(cap, false);
-    if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
-    CK(cudaMemsetAsync(errs, 0xFF, 16, st));
-    GET(lb, uint64_t, nblk, true);
+  // count pre-pass + exclusive scan → first record index of every block
+  GET(d_cnt, uint32_t, nblk, false);
+  block_count_kernel<<<std::min<uint32_t>((nblk + 255) / 256, 8 * g_num_sms), 256, 0, st>>>(jd->arena, bt, nblk, K,
+                                                                                         d_cnt);
+  ++g_launches;
+  {
+    const uint64_t nt = std::max<uint64_t>(1, (nblk + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
+    GET(lb, uint64_t, nt, true);
     GET(ctr, unsigned int, 1, true);
-    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, cap, lb, ctr, d_base, errs, errs + 1};
+    scan_excl_kernel<uint32_t><<<(unsigned)nt, kScanThreads, 0, st>>>(d_cnt, nblk, d_base, lb, ctr);
+    ++g_launches;
+  }
+  GET(d_fbase, uint64_t, jd->n_files + 1, false);
+  file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_base, d_file_blk_base, jd->n_files, d_fbase);
+  ++g_launches;
+  CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
+  {
+    int rc = sync(st);
+    if (rc) return rc;
+  }
+  n_in = fbase[jd->n_files];
+  X = scratch.get<Rec<W>>(std::max<uint64_t>(n_in, 1), false);
+  if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
+  {
+    CK(cudaMemsetAsync(errs, 0xFF, 16, st));
+    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, n_in, d_base, errs, errs + 1};
     KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
     ++g_launches;
     KT_STOP(0, st);
     CK(cudaGetLastError());
-    GET(d_fbase, uint64_t, jd->n_files + 1, false);
-    file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_base, d_file_blk_base, jd->n_files,
-                                                                           d_fbase);
-    ++g_launches;
     unsigned long long herr[2];
     CK(cudaMemcpyAsync(herr, errs, 16, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
     int rc = sync(st);
     if (rc) return rc;
     if (herr[0] != ~0ull || herr[1] != ~0ull) {
@@ -555,9 +569,6 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
       if (code == B_CRC) return fail(LUDA_CORRUPT, block_msg(code), foff);
       return fail(LUDA_FORMAT, block_msg(code));
     }
-    n_in = fbase[jd->n_files];
-    if (n_in <= cap) break;
-    cap = n_in;  // exact re-run (non-canonical restart layout exceeded the bound)
   }
   res->n_in = n_in;
   if (ev) CK(cudaEventRecord(ev[2], st));
@@ -975,10 +986,7 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
                                                        bound);
   ++g_launches;
   CK(cudaGetLastError());
-  unsigned long long hbound = 0;
-  CK(cudaMemcpyAsync(&hbound, bound, 8, cudaMemcpyDeviceToHost, st));
-  rc = sync(st);
-  if (rc) return rc;
+  const unsigned long long hbound = 0;  // (entry counts now come from the count pre-pass)
   const uint32_t W = std::max<uint32_t>(1, (L + 7) / 8);
   CK(cudaEventRecord(ev[1], st));
   cudaEvent_t* pev = ev;

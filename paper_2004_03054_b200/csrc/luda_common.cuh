@@ -2,12 +2,18 @@
 //
 // CRC-32/IEEE (reflected 0xEDB88320, init/xorout 0xFFFFFFFF; the zlib flavour
 // of checksum.py:12-13) is computed warp-parallel: a byte range is cut into
-// END-ALIGNED 132-byte segments (33 words), lane d owning the segment that ends
-// 132*d bytes before the range end. Each lane computes the raw CRC register of
-// its segment with a bank-replicated byte table in shared memory, and the
-// segments are combined with the GF(2) "advance over n zero bytes" operator
-// Z_n (the crc32_combine algebra): raw(A∥B) = Z_|B|(raw(A)) ^ raw(B).
-// 132 (not 128) makes the 32 lanes' LDS.32 streams hit 32 distinct banks.
+// END-ALIGNED 68-byte segments (17 words). In one pass a warp covers 64
+// segments (4352 B): lane d owns the segments at distance d and d+32 from the
+// pass end and runs their two byte-table chains interleaved (2-way ILP; the
+// table is replicated per bank so lanes never conflict). Segment registers are
+// combined with the GF(2) "advance over n zero bytes" operator Z_n (the
+// crc32_combine algebra: raw(A∥B) = Z_|B|(raw(A)) ^ raw(B)):
+//   lane value = Z_{68d}( raw(seg d) ^ Z_2176(raw(seg d+32)) ), XOR over lanes.
+// 17 words (odd) per segment makes the 32 lanes' LDS.32 streams hit 32
+// distinct banks. The ~0 preset is folded into the data: callers run
+// crc_prep() on the smem copy (zero the 72 bytes before it, complement the
+// first 4 bytes: F(~0, D) = F(0, D') and leading zeros leave a zero register
+// unchanged) and crc_unprep() afterwards; the inner loop has no masking.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -15,30 +21,38 @@
 namespace luda {
 
 constexpr uint32_t kCrcPoly = 0xEDB88320u;
-constexpr int kSeg = 132;           // bytes per CRC segment
-constexpr int kSegWords = kSeg / 4; // 33
-constexpr int kGroup = kSeg * 32;   // bytes one warp covers per pass (4224)
+constexpr int kSeg = 68;             // bytes per CRC segment
+constexpr int kSegWords = kSeg / 4;  // 17
+constexpr int kHalf = 32 * kSeg;     // 2176: distance between a lane's two segments
+constexpr int kGroup = 64 * kSeg;    // 4352: bytes one warp covers per pass
+constexpr int kCrcLead = 72;         // zeroed bytes required before the data
 
 // ---- tables (device globals; initialised by luda_init) ---------------------
 // g_crc_tab[b]          : byte table T[b]
-// g_seg_nib[n][v][d]    : Z_{132*d}(v << 4n)   (8 x 16 x 32 words)
-// g_zpow[i][j]          : Z_{2^i}(1 << j)      (48 x 32 words) for arbitrary shifts
+// g_seg_nib[n][v][d]    : Z_{68*d}(v << 4n)    (8 x 16 x 32 words)
+// g_half_tab[k][b]      : Z_2176(b << 8k)     (4 x 256 words)
+// c_zpow[i][j]          : Z_{2^i}(1 << j)      (48 x 32 words) for arbitrary shifts
+// c_zgroup[j]           : Z_4352(1 << j)       (one warp pass)
 // (single translation unit: luda_b200.cu includes every stage header)
 __device__ uint32_t g_crc_tab[256];
 __device__ uint32_t g_seg_nib[8 * 16 * 32];
+__device__ uint32_t g_half_tab[4 * 256];
 __constant__ uint32_t c_zpow[48][32];
-__constant__ uint32_t c_zgroup[32]; // Z_{4224}(1<<j)
+__constant__ uint32_t c_zgroup[32];
 
-// Shared-memory CRC state: 32 bank-replicated copies of T (32 KB) + the
-// per-lane nibble tables (16 KB). Lane l reads tab[(idx<<5)|l] → bank l.
+// Shared-memory CRC state: 32 bank-replicated copies of T (32 KB), the
+// per-lane nibble tables (16 KB) and the Z_2176 byte tables (4 KB).
+// Lane l reads tab[(idx<<5)|l] → bank l.
 struct CrcSmem {
   uint32_t tab[256 * 32];
   uint32_t nib[8 * 16 * 32];
+  uint32_t half[4 * 256];
 };
 
 __device__ __forceinline__ void crc_smem_init(CrcSmem& s) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) s.tab[i] = g_crc_tab[i >> 5];
   for (int i = threadIdx.x; i < 8 * 16 * 32; i += blockDim.x) s.nib[i] = g_seg_nib[i];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) s.half[i] = g_half_tab[i];
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -58,12 +72,17 @@ __device__ __forceinline__ uint32_t crc_byte(uint32_t c, uint32_t b, const uint3
   return tl[((c ^ b) & 0xFFu) << 5] ^ (c >> 8);
 }
 
-// Z_{132*lane}(c) via the lane's nibble tables. `nl` = s.nib + lane.
+// Z_{68*lane}(c) via the lane's nibble tables. `nl` = s.nib + lane.
 __device__ __forceinline__ uint32_t seg_shift(uint32_t c, const uint32_t* __restrict__ nl) {
   uint32_t r = 0;
 #pragma unroll
   for (int n = 0; n < 8; ++n) r ^= nl[((n << 4) | ((c >> (4 * n)) & 0xFu)) << 5];
   return r;
+}
+
+// Z_2176(c) (warp-uniform operator, byte tables).
+__device__ __forceinline__ uint32_t half_shift(uint32_t c, const uint32_t* __restrict__ ht) {
+  return ht[c & 0xFFu] ^ ht[256 + ((c >> 8) & 0xFFu)] ^ ht[512 + ((c >> 16) & 0xFFu)] ^ ht[768 + (c >> 24)];
 }
 
 // Apply a 32x32 GF(2) operator given by its columns (constant memory; the
@@ -82,81 +101,84 @@ __device__ __forceinline__ uint32_t crc_shift(uint32_t c, uint64_t n) {
   return c;
 }
 
-// Raw CRC register over 33 words of shared memory starting at byte address p
-// (may be unaligned; reads the aligned words covering it). Bytes whose
-// data-index (idx0 + k) is < 0 are treated as zero and bytes with index in
-// [0,4) are complemented: F(~0, D) = F(0, D with its first 4 bytes inverted)
-// and leading zero bytes leave a zero register unchanged, so the preset folds
-// into the data (requires n >= 4). Only the first segment (idx0 < 4) has such
-// bytes: it skips its all-zero leading words and masks the next two, so the
-// main loop carries no per-word checks. Reads the smem window [p, p+136).
-__device__ __forceinline__ uint32_t seg_crc_smem(const uint8_t* p, int64_t idx0,
-                                                 const uint32_t* __restrict__ tl) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-  const uint32_t sh = (uint32_t)(a & 3u) * 8u;
-  // first word holding a data byte, and the masks of words j0, j0+1
-  int32_t j0 = 0;
-  uint32_t keep0 = 0xFFFFFFFFu, inv0 = 0, keep1 = 0xFFFFFFFFu, inv1 = 0;
-  if (idx0 < 4) {
-    const int32_t i0 = (int32_t)idx0;  // in (-132, 4)
-    j0 = i0 < 0 ? (-i0) >> 2 : 0;      // words entirely before data index 0 are zero
-    const int32_t b0 = i0 + 4 * j0;    // data index of byte 0 of word j0 (in (-4, 4))
-    keep0 = inv0 = keep1 = inv1 = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int32_t d0 = b0 + k, d1 = b0 + 4 + k;
-      if (d0 >= 0) keep0 |= 0xFFu << (8 * k);
-      if (d0 >= 0 && d0 < 4) inv0 |= 0xFFu << (8 * k);
-      if (d1 >= 0) keep1 |= 0xFFu << (8 * k);
-      if (d1 >= 0 && d1 < 4) inv1 |= 0xFFu << (8 * k);
-    }
-  }
-  uint32_t c = 0;
-  uint32_t lo = wp[j0];
-  {
-    const uint32_t hi = wp[j0 + 1];
-    c = crc_word(c, (__funnelshift_r(lo, hi, sh) & keep0) ^ inv0, tl);
-    lo = hi;
-  }
-  if (j0 + 1 < kSegWords) {
-    const uint32_t hi = wp[j0 + 2];
-    c = crc_word(c, (__funnelshift_r(lo, hi, sh) & keep1) ^ inv1, tl);
-    lo = hi;
-  }
-#pragma unroll 4
-  for (int32_t j = j0 + 2; j < kSegWords; ++j) {
-    const uint32_t hi = wp[j + 1];
-    c = crc_word(c, __funnelshift_r(lo, hi, sh), tl);
-    lo = hi;
-  }
-  return c;
+// Prepare / restore an smem copy of the data for crc: zero [data-72, data)
+// and complement data[0..4). Whole warp; n >= 4.
+__device__ __forceinline__ void crc_prep(uint8_t* data) {
+  const uint32_t lane = lane_id();
+  for (uint32_t i = lane; i < (uint32_t)kCrcLead; i += 32) data[(int)i - kCrcLead] = 0;
+  if (lane < 4) data[lane] ^= 0xFFu;
+  __syncwarp();
+}
+__device__ __forceinline__ void crc_unprep(uint8_t* data) {
+  __syncwarp();
+  if (lane_id() < 4) data[lane_id()] ^= 0xFFu;
+  __syncwarp();
 }
 
-// Warp-cooperative CRC-32 of `n` bytes at shared address `data` (n >= 4).
-// All 32 lanes must call; every lane returns the final CRC. Requires the smem
-// window [data - kSeg - 4, data + n + 8) to be readable (callers pad).
-__device__ __forceinline__ uint32_t warp_crc32_smem(const uint8_t* data, uint32_t n, const CrcSmem& s) {
+// Raw CRC register of the 17 words starting at smem byte address p (any
+// alignment; reads the aligned words covering [p, p+72)).
+struct SegPtr {
+  const uint32_t* wp;
+  uint32_t sh;
+};
+__device__ __forceinline__ SegPtr seg_ptr(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  return SegPtr{reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3)), (uint32_t)(a & 3u) * 8u};
+}
+
+// Warp: un-combined pass value of pass q over prepared smem data of length n:
+// this lane's Z_{68 lane}( raw(seg d) ^ Z_2176(raw(seg d+32)) ) before the
+// cross-lane XOR, with d = lane + 64q (pass q covers distances [64q, 64q+64)).
+__device__ __forceinline__ uint32_t pass_lane_value(const uint8_t* data, uint64_t n, uint32_t q, const CrcSmem& cs,
+                                                    const uint8_t* safe) {
   const uint32_t lane = lane_id();
-  const uint32_t* tl = s.tab + lane;
-  const uint32_t* nl = s.nib + lane;
-  const int64_t nseg = (int64_t)((n + kSeg - 1) / kSeg);
-  const int64_t npass = (nseg + 31) / 32;
-  uint32_t acc = 0;
-  for (int64_t q = npass - 1; q >= 0; --q) {
-    const int64_t d = (int64_t)lane + 32 * q;  // segment distance from the end
-    uint32_t r = 0;
-    if (d < nseg) {
-      int64_t start = (int64_t)n - (int64_t)kSeg * (d + 1);  // may be negative (first segment)
-      r = seg_crc_smem(data + start, start, tl);
-    }
-    if (q != npass - 1) acc = gf2_apply(c_zgroup, acc);
-    acc ^= r;
+  const uint32_t* tl = cs.tab + lane;
+  const int64_t nseg = ((int64_t)n + kSeg - 1) / kSeg;
+  const int64_t dlo = (int64_t)lane + 64 * (int64_t)q;
+  const int64_t dhi = dlo + 32;
+  const bool vlo = dlo < nseg, vhi = dhi < nseg;
+  const int64_t slo = (int64_t)n - (int64_t)kSeg * (dlo + 1);
+  const int64_t shi = (int64_t)n - (int64_t)kSeg * (dhi + 1);
+  const SegPtr a = seg_ptr(vlo ? data + slo : safe);  // `safe`: any readable smem (skipped chain)
+  const SegPtr b = seg_ptr(vhi ? data + shi : safe);
+  uint32_t ca = 0, cb = 0;
+  uint32_t la = a.wp[0], lb = b.wp[0];
+#pragma unroll 17
+  for (int j = 0; j < kSegWords; ++j) {
+    const uint32_t ha = a.wp[j + 1], hb = b.wp[j + 1];
+    ca = crc_word(ca, __funnelshift_r(la, ha, a.sh), tl);
+    cb = crc_word(cb, __funnelshift_r(lb, hb, b.sh), tl);
+    la = ha;
+    lb = hb;
   }
-  acc = seg_shift(acc, nl);
+  uint32_t r = (vlo ? ca : 0u) ^ (vhi ? half_shift(cb, cs.half) : 0u);
+  return seg_shift(r, cs.nib + lane);
+}
+
+__device__ __forceinline__ uint32_t warp_xor(uint32_t v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc ^= __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+// Warp-cooperative CRC-32 of n >= 4 bytes of PREPARED smem data (crc_prep).
+// All 32 lanes call; every lane returns the final CRC.
+__device__ __forceinline__ uint32_t warp_crc32_prepped(const uint8_t* data, uint32_t n, const CrcSmem& cs) {
+  const uint32_t npass = (n + kGroup - 1) / kGroup;
+  uint32_t acc = 0;
+  for (int q = (int)npass - 1; q >= 0; --q) {
+    const uint32_t v = warp_xor(pass_lane_value(data, n, (uint32_t)q, cs, data));
+    acc = (q == (int)npass - 1) ? v : (gf2_apply(c_zgroup, acc) ^ v);
+  }
   return ~acc;
+}
+
+// Convenience: prep, crc, restore (data must have 72 writable bytes before it).
+__device__ __forceinline__ uint32_t warp_crc32_smem(uint8_t* data, uint32_t n, const CrcSmem& cs) {
+  crc_prep(data);
+  const uint32_t c = warp_crc32_prepped(data, n, cs);
+  crc_unprep(data);
+  return c;
 }
 
 // Scalar CRC (any n) for tiny ranges; `tl` = table row of the calling lane.

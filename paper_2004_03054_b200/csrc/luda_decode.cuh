@@ -52,7 +52,7 @@ constexpr int kDecPre = 160;                     // CRC lead-in before the data
 constexpr int kDecBuf = kDecPre + kDecStage + 64;
 constexpr int kDecSlots = 128;
 constexpr int kDecStride = 16;                   // slots per restart interval (single-walk path)
-constexpr int kDecWarpBytes = 2 * kDecBuf + 2 * kDecSlots * 8 + 16;  // 2 = kDecTile
+constexpr int kDecWarpBytes = 2 * kDecBuf + kDecSlots * 8 + 16;  // 2 staging buffers, 1 slot array
 
 struct DecSlot {
   uint32_t pos;  // block-relative offset of the key suffix
@@ -67,9 +67,7 @@ struct DecodeArgs {
   uint32_t K;               // internal key length of the job
   Rec<W>* out;
   uint64_t cap;
-  uint64_t* lb;             // look-back status per block (zeroed)
-  unsigned int* tile_ctr;   // zeroed
-  uint64_t* blk_base;       // [nblk+1] first record index of each block
+  const uint64_t* blk_base; // [nblk+1] first record index of each block (count pre-pass + scan)
   unsigned long long* err_ref;
   unsigned long long* err_unsup;
 };
@@ -270,7 +268,7 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   if (!code) {
     uint32_t crc;
     if (st.staged) {
-      crc = warp_crc32_smem(d, len - 4, cs);
+      crc = warp_crc32_smem(const_cast<uint8_t*>(d), len - 4, cs);
     } else {
       const uint8_t* g = a.arena + st.addr;
       const uint64_t np = ((uint64_t)len - 4 + kGroup - 1) / kGroup;
@@ -386,6 +384,43 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   }
 }
 
+// Entry count of one block with exactly the decision procedure of phase 1:
+// fast restart-interval walk if the block is canonical, else the exact
+// sequential walk (count up to the first error). Thread-level, header bytes
+// read straight from global memory.
+__device__ __forceinline__ uint32_t block_count(const uint8_t* d, uint32_t len, uint32_t K) {
+  if (len < 12) return 0;
+  const uint32_t nres = ld_u32_le(d + len - 8);
+  const int64_t entries_end = (int64_t)len - 8 - 4 * (int64_t)nres;
+  if (nres < 1 || entries_end < 0) return 0;
+  if (nres <= 32) {
+    uint32_t total = 0;
+    bool ok = true;
+    uint32_t st = ld_u32_le(d + entries_end);
+    ok = st == 0;
+    for (uint32_t k = 0; ok && k < nres; ++k) {
+      const uint32_t en = (k + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (k + 1)) : (uint32_t)entries_end;
+      ok = st < en && (int64_t)en <= entries_end;
+      if (!ok) break;
+      const int32_t c = interval_walk(d, st, en, K, [](int32_t, uint32_t, uint32_t, uint32_t) {});
+      ok = c >= 0;
+      total += (uint32_t)c;
+      st = en;
+    }
+    if (ok) return total;
+  }
+  uint64_t nn = 0;
+  uint32_t us;
+  block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us, [](uint64_t, uint32_t, uint32_t, uint32_t) {});
+  return (uint32_t)nn;
+}
+
+__global__ void __launch_bounds__(256) block_count_kernel(const uint8_t* arena, BlockTable bt, uint32_t nblk,
+                                                          uint32_t K, uint32_t* count) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
+    count[b] = block_count(arena + bt.addr[b], bt.len[b], K);
+}
+
 template <int W>
 __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -395,8 +430,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
 #pragma unroll
   for (int i = 0; i < kDecTile; ++i) {
     w.buf[i] = wb + i * kDecBuf;
-    w.slots[i] = reinterpret_cast<DecSlot*>(wb + kDecTile * kDecBuf) + i * kDecSlots;
-    w.bar[i] = reinterpret_cast<uint64_t*>(wb + kDecTile * kDecBuf + kDecTile * kDecSlots * 8) + i;
+    w.slots[i] = reinterpret_cast<DecSlot*>(wb + kDecTile * kDecBuf);  // one block in flight at a time
+    w.bar[i] = reinterpret_cast<uint64_t*>(wb + kDecTile * kDecBuf + kDecSlots * 8) + i;
     w.phase[i] = 0;
   }
   const uint32_t lane = lane_id();
@@ -404,41 +439,24 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
   if (lane == 0)
     for (int i = 0; i < kDecTile; ++i) mbar_init(w.bar[i], 1);
   __syncthreads();
-  const uint32_t ntiles = (a.nblk + kDecTile - 1) / kDecTile;
-  while (true) {
-    uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(a.tile_ctr, 1u);
-    t = __shfl_sync(0xFFFFFFFFu, t, 0);
-    if (t >= ntiles) break;
-    const uint32_t b0 = t * kDecTile;
-    bool staged[kDecTile];
-#pragma unroll
-    for (int i = 0; i < kDecTile; ++i) staged[i] = dec_prefetch(a, b0 + i, w, i);
-    DecState st[kDecTile];
-    uint64_t tot = 0;
-#pragma unroll
-    for (int i = 0; i < kDecTile; ++i) {
-      st[i] = dec_phase1(a, b0 + i, staged[i], w, i);
-      tot += st[i].n;
-    }
-    if (lane == 0) lb_publish(a.lb, t, kLbAgg, tot);
-    const uint64_t excl = lb_exclusive(a.lb, t);
-    if (lane == 0) lb_publish(a.lb, t, kLbInc, excl + tot);
-    uint64_t base = excl;
-#pragma unroll
-    for (int i = 0; i < kDecTile; ++i) {
-      const uint32_t b = b0 + i;
-      if (st[i].valid) {
-        if (lane == 0) {
-          a.blk_base[b] = base;
-          if (b + 1 == a.nblk) a.blk_base[a.nblk] = base + st[i].n;
-        }
-        dec_phase2(a, b, st[i], base, w, i, cs);
-        base += st[i].n;
-      }
-    }
-    fence_proxy_async_smem();  // generic smem accesses before the next TMA into these buffers
+  // Record bases come from the count pre-pass (blk_base), so blocks are
+  // independent: static round-robin assignment, the next block's TMA staging
+  // in flight while the current one is processed.
+  const uint32_t nw = gridDim.x * kDecWarps;
+  uint32_t cur = blockIdx.x * kDecWarps + (threadIdx.x >> 5);
+  int which = 0;
+  bool cur_staged = dec_prefetch(a, cur, w, which);
+  while (cur < a.nblk) {
+    const uint32_t nxt = cur + nw;
+    const bool nxt_staged = dec_prefetch(a, nxt, w, which ^ 1);
+    DecState st = dec_phase1(a, cur, cur_staged, w, which);
+    const uint64_t base = a.blk_base[cur];
+    dec_phase2(a, cur, st, base, w, which, cs);
+    fence_proxy_async_smem();  // generic smem accesses before the next TMA into this buffer
     __syncwarp();
+    cur = nxt;
+    cur_staged = nxt_staged;
+    which ^= 1;
   }
 }
 

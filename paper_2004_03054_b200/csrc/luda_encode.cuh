@@ -86,27 +86,11 @@ __device__ __forceinline__ void put_key_tail(uint8_t* p, const Rec<W>& r, uint32
   }
 }
 
-// CRC of one pass over smem data (un-shifted, warp-reduced raw register).
-__device__ __forceinline__ uint32_t warp_pass_raw_smem(const uint8_t* data, uint32_t n, int64_t q, const CrcSmem& cs) {
-  const uint32_t lane = lane_id();
-  const int64_t nseg = ((int64_t)n + kSeg - 1) / kSeg;
-  const int64_t d = (int64_t)lane + 32 * q;
-  uint32_t r = 0;
-  if (d < nseg) {
-    const int64_t start = (int64_t)n - (int64_t)kSeg * (d + 1);
-    r = seg_crc_smem(data + start, start, cs.tab + lane);
-  }
-  r = seg_shift(r, cs.nib + lane);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) r ^= __shfl_xor_sync(0xFFFFFFFFu, r, o);
-  return r;
-}
-
 // CTA-wide CRC-32 of smem data (passes spread over warps). All threads call;
-// returns the CRC in every thread. `red` = smem scratch of >= 32 words.
-__device__ __forceinline__ uint32_t cta_crc32_smem(const uint8_t* data, uint32_t n, const CrcSmem& cs, uint32_t* red) {
+// returns the CRC in every thread. The data needs kCrcLead writable bytes
+// before it (prepared and restored here). `red` = smem scratch of >= 32 words.
+__device__ __forceinline__ uint32_t cta_crc32_smem(uint8_t* data, uint32_t n, const CrcSmem& cs, uint32_t* red) {
   const uint32_t nwarps = blockDim.x >> 5, wid = threadIdx.x >> 5;
-  uint32_t acc = 0;
   if (n < 4) {
     if (threadIdx.x == 0) red[0] = crc32_bytes(data, n, cs.tab);
     __syncthreads();
@@ -114,12 +98,17 @@ __device__ __forceinline__ uint32_t cta_crc32_smem(const uint8_t* data, uint32_t
     __syncthreads();
     return v;
   }
-  const int64_t npass = ((int64_t)n + kGroup - 1) / kGroup;
-  for (int64_t q = wid; q < npass; q += nwarps) acc ^= crc_shift(warp_pass_raw_smem(data, n, q, cs), (uint64_t)kGroup * q);
+  if (wid == 0) crc_prep(data);
+  __syncthreads();
+  uint32_t acc = 0;
+  const uint32_t npass = (n + kGroup - 1) / kGroup;
+  for (uint32_t q = wid; q < npass; q += nwarps)
+    acc ^= crc_shift(warp_xor(pass_lane_value(data, n, q, cs, data)), (uint64_t)kGroup * q);
   if (lane_id() == 0) red[wid] = acc;
   __syncthreads();
   uint32_t v = 0;
   for (uint32_t w = 0; w < nwarps; ++w) v ^= red[w];
+  if (wid == 0) crc_unprep(data);
   __syncthreads();
   return ~v;
 }

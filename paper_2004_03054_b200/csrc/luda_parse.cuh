@@ -173,19 +173,20 @@ __global__ void parse_files_a(ParseArgs a) {
   }
 }
 
-// Warp CRC contribution of pass q (segments [32q, 32q+32) from the end) of
-// the n-byte range at global address g, staged through the warp's smem buffer
-// `stage` (>= kGroup + 160 bytes, 16-aligned). Returns Z_{4224 q}(raw part);
-// the XOR over all passes of a range is its raw register (preset folded in).
+// Warp CRC contribution of pass q (segments at distances [64q, 64q+64) from
+// the end) of the n-byte range at global address g, staged through the
+// warp's smem buffer `stage` (>= kGroup + 160 bytes, 16-aligned). Returns
+// Z_{4352 q}(pass raw); the XOR over all passes of a range is its raw
+// register with the ~0 preset folded in (the staged copy is prepared:
+// bytes before the range are zeroed, its first 4 bytes complemented).
 __device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint64_t n, uint64_t q,
                                                          uint8_t* stage, const CrcSmem& cs) {
   const uint32_t lane = lane_id();
   const int64_t hi = (int64_t)n - (int64_t)kGroup * (int64_t)q;          // pass end (data index)
   const int64_t lo0 = hi - kGroup;
-  const int64_t lo = lo0 > -(int64_t)kSeg - 8 ? lo0 : -(int64_t)kSeg - 8;  // first segment starts > -132
+  const int64_t lo = lo0 > -(int64_t)kCrcLead ? lo0 : -(int64_t)kCrcLead;  // first segment starts > -68
   // Stage data indices [lo - 8, hi + 8) into smem, keeping 16-byte phase.
-  // Only 16-byte granules that hold bytes of [0, n) are loaded (always
-  // mapped); the rest of the window is zero (those bytes are masked anyway).
+  // Only 16-byte granules that hold bytes of [0, n) are loaded (always mapped).
   const uintptr_t gA = reinterpret_cast<uintptr_t>(g);
   const uintptr_t w0 = (uintptr_t)((int64_t)gA + lo - 8) & ~uintptr_t(15);
   const uintptr_t w1 = (uintptr_t)((int64_t)gA + hi + 8 + 15) & ~uintptr_t(15);
@@ -199,19 +200,15 @@ __device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint6
     reinterpret_cast<uint4*>(stage)[c] = v;
   }
   __syncwarp();
-  const uint8_t* base = stage + ((uintptr_t)((int64_t)gA + lo) - w0);  // smem addr of data index lo
-  const int64_t nseg = ((int64_t)n + kSeg - 1) / kSeg;
-  const int64_t d = (int64_t)lane + 32 * (int64_t)q;
-  uint32_t r = 0;
-  if (d < nseg) {
-    const int64_t start = (int64_t)n - (int64_t)kSeg * (d + 1);
-    r = seg_crc_smem(base + (start - lo), start, cs.tab + lane);
+  uint8_t* base = stage + ((uintptr_t)((int64_t)gA + lo) - w0);  // smem addr of data index lo
+  if (lo < 0) {  // prepare: zero data indices [lo-8, 0), complement [0, 4)
+    for (int64_t i = lo - 8 + lane; i < 0; i += 32) base[i - lo] = 0;
+    if (lane < 4 && (uint64_t)lane < n) base[lane - lo] ^= 0xFFu;
+    __syncwarp();
   }
-  r = seg_shift(r, cs.nib + lane);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) r ^= __shfl_xor_sync(0xFFFFFFFFu, r, o);
+  const uint32_t v = warp_xor(pass_lane_value(base - lo, n, (uint32_t)q, cs, base));
   __syncwarp();
-  return crc_shift(r, (uint64_t)kGroup * q);
+  return crc_shift(v, (uint64_t)kGroup * q);
 }
 
 // Stage B: CRC of many ranges; warp per range, looping passes. out[i] = crc.

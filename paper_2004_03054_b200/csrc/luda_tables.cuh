@@ -2,9 +2,10 @@
 //
 // Host code computes, once per process (luda_init):
 //   g_crc_tab   byte table of the reflected polynomial 0xEDB88320
-//   g_seg_nib   nibble tables of Z_{132*d}, d = 0..31 (segment combine)
+//   g_seg_nib   nibble tables of Z_{68*d}, d = 0..31 (segment combine)
+//   g_half_tab  byte tables of Z_2176 (a lane's second segment)
 //   c_zpow      columns of Z_{2^i}, i = 0..47 (arbitrary shifts)
-//   c_zgroup    columns of Z_{4224} (one warp pass)
+//   c_zgroup    columns of Z_4352 (one warp pass)
 // where Z_n advances a raw CRC register over n zero bytes (the operator
 // behind zlib's crc32_combine).
 #pragma once
@@ -45,7 +46,7 @@ using namespace tables_detail;
 int upload_crc_tables() {
   uint32_t t[256];
   host_table(t);
-  // Z_132 columns, then Z_{132 d} by repeated application.
+  // Z_68 columns, then Z_{68 d} by repeated application.
   uint32_t z132[32];
   for (int j = 0; j < 32; ++j) z132[j] = zero_bytes(t, 1u << j, kSeg);
   static uint32_t nib[8 * 16 * 32];
@@ -65,6 +66,12 @@ int upload_crc_tables() {
     for (int j = 0; j < 32; ++j) zpow[i][j] = apply_cols(zpow[i - 1], zpow[i - 1][j]);
   uint32_t zg[32];
   for (int j = 0; j < 32; ++j) zg[j] = zero_bytes(t, 1u << j, kGroup);
+  uint32_t zh[32];
+  for (int j = 0; j < 32; ++j) zh[j] = zero_bytes(t, 1u << j, kHalf);
+  static uint32_t half[4 * 256];
+  for (int k = 0; k < 4; ++k)
+    for (int b = 0; b < 256; ++b) half[k * 256 + b] = apply_cols(zh, (uint32_t)b << (8 * k));
+  if (cudaMemcpyToSymbol(g_half_tab, half, sizeof(half)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(g_crc_tab, t, sizeof(t)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(g_seg_nib, nib, sizeof(nib)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(c_zpow, zpow, sizeof(zpow)) != cudaSuccess) return 1;
