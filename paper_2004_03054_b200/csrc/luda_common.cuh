@@ -122,8 +122,9 @@ struct SegPtr {
   uint32_t sh;
 };
 __device__ __forceinline__ SegPtr seg_ptr(const uint8_t* p) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  return SegPtr{reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3)), (uint32_t)(a & 3u) * 8u};
+  // pointer arithmetic (not an integer round trip) keeps the smem address space
+  const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3u);
+  return SegPtr{reinterpret_cast<const uint32_t*>(p - mis), mis * 8u};
 }
 
 // Warp: un-combined pass value of pass q over prepared smem data of length n:
@@ -231,23 +232,23 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // other thread writes those words concurrently). Reads [src-3, src+n+4).
 __device__ __forceinline__ void warp_smem_copy(uint8_t* dst, const uint8_t* src, uint32_t n, uint32_t lane) {
   if (n == 0) return;
-  const uintptr_t da = reinterpret_cast<uintptr_t>(dst);
-  const uintptr_t w0 = da & ~uintptr_t(3);
-  const uint32_t nw = (uint32_t)((((da + n + 3) & ~uintptr_t(3)) - w0) >> 2);
-  const intptr_t delta = reinterpret_cast<intptr_t>(src) - (intptr_t)da;
+  // pointer arithmetic only (no integer round trips) so smem stays LDS/STS
+  const uint32_t dmis = (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 3u);
+  uint32_t* dw = reinterpret_cast<uint32_t*>(dst - dmis);
+  const uint32_t nw = (dmis + n + 3) >> 2;
+  const uint8_t* s0 = src - dmis;  // source byte for dst word 0, byte 0
+  const uint32_t smis = (uint32_t)(reinterpret_cast<uintptr_t>(s0) & 3u);
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>(s0 - smis);
+  const uint32_t sh = smis * 8u;
   for (uint32_t w = lane; w < nw; w += 32) {
-    const uintptr_t A = w0 + 4ull * w;
-    const uintptr_t sA = (uintptr_t)((intptr_t)A + delta);
-    const uint32_t* sp = reinterpret_cast<const uint32_t*>(sA & ~uintptr_t(3));
-    const uint32_t v = __funnelshift_r(sp[0], sp[1], (uint32_t)(sA & 3u) * 8u);
-    const uint32_t lo = A < da ? (uint32_t)(da - A) : 0u;
-    const uint32_t hi = (A + 4 > da + n) ? (uint32_t)(da + n - A) : 4u;
-    uint32_t* p = reinterpret_cast<uint32_t*>(A);
+    const uint32_t v = __funnelshift_r(sw[w], sw[w + 1], sh);
+    const uint32_t lo = w == 0 ? dmis : 0u;
+    const uint32_t hi = (4 * w + 4 > dmis + n) ? (dmis + n - 4 * w) : 4u;
     if (lo == 0 && hi == 4) {
-      *p = v;
+      dw[w] = v;
     } else {
       const uint32_t m = (hi == 4 ? 0xFFFFFFFFu : ((1u << (8 * hi)) - 1u)) & ~((1u << (8 * lo)) - 1u);
-      *p = (*p & ~m) | (v & m);
+      dw[w] = (dw[w] & ~m) | (v & m);
     }
   }
 }
@@ -287,6 +288,67 @@ __device__ __forceinline__ T warp_max(T v) {
     v = u > v ? u : v;
   }
   return v;
+}
+
+// Warp copy of up to 32 (src, dst, n) ranges (one per lane; n = 0 for idle
+// lanes; base_dst and base_src 16-byte aligned, src in smem, dst smem or
+// global), any alignments, flattened over 16-byte destination chunks:
+// lane t of each round realigns one chunk with two LDS.128 + funnel shifts
+// and writes it with one STS.128; the first/last chunk of a range are written
+// per word (partial words read-modify-written — distinct ranges are >= 12
+// bytes apart so they never share a word). `pre` = smem scratch of 33 words.
+// Source windows must be readable 16 bytes beyond each range.
+__device__ __forceinline__ void warp_copy_ranges16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
+                                                   uint32_t src_off, uint32_t n, uint32_t* pre) {
+  const uint32_t lane = lane_id();
+  const uint32_t dmis = dst_off & 15u;
+  const uint32_t nch = n ? (dmis + n + 15) >> 4 : 0u;
+  const uint32_t incl = warp_incl_scan<uint32_t>(nch);
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  pre[lane] = incl - nch;                         // first chunk of range `lane`
+  pre[32 + lane] = dst_off;
+  pre[64 + lane] = src_off;
+  pre[96 + lane] = n;
+  __syncwarp();
+  for (uint32_t t = lane; t < total; t += 32) {
+    // range j: last lane with pre[j] <= t (ranges with nch = 0 share starts; take the last)
+    uint32_t j = 0;  // largest j with pre[j] <= t (empty ranges sharing a start come first)
+#pragma unroll
+    for (uint32_t step = 16; step >= 1; step >>= 1)
+      if (j + step < 32 && pre[j + step] <= t) j += step;
+    const uint32_t dj = pre[32 + j], sj = pre[64 + j], nj = pre[96 + j];
+    const uint32_t i = t - pre[j];
+    const uint32_t dchunk = (dj & ~15u) + 16u * i;          // dst chunk offset
+    const int32_t sstart = (int32_t)(sj + dchunk) - (int32_t)dj;  // src offset of dst chunk byte 0
+    const uint32_t o = (uint32_t)sstart & 15u;
+    const uint4* sp = reinterpret_cast<const uint4*>(base_src + (sstart - (int32_t)o));
+    const uint4 A = sp[0], B = sp[1];
+    uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+    const uint32_t q = o >> 2, sh = (o & 3u) * 8u;
+    uint32_t x[6], y[5];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) x[k] = (q & 2u) ? w[k + 2] : w[k];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) y[k] = (q & 1u) ? x[k + 1] : x[k];
+    uint32_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __funnelshift_r(y[k], y[k + 1], sh);
+    uint32_t* dw = reinterpret_cast<uint32_t*>(base_dst + dchunk);
+    const uint32_t lo = dchunk < dj ? dj - dchunk : 0u;                 // first valid byte in chunk
+    const uint32_t hi = (dchunk + 16 > dj + nj) ? dj + nj - dchunk : 16u;  // one past last valid byte
+    if (lo == 0 && hi == 16) {
+      *reinterpret_cast<uint4*>(dw) = make_uint4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t a = (int32_t)lo - 4 * k, b = (int32_t)hi - 4 * k;  // valid bytes [a, b) of word k
+        if (b <= 0 || a >= 4) continue;
+        const uint32_t m = (b >= 4 ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u)) & (a <= 0 ? 0xFFFFFFFFu : ~((1u << (8 * a)) - 1u));
+        dw[k] = m == 0xFFFFFFFFu ? v[k] : ((dw[k] & ~m) | (v[k] & m));
+      }
+    }
+  }
+  __syncwarp();
 }
 
 // ---- decoupled look-back (single-pass prefix over tiles) ----------------------

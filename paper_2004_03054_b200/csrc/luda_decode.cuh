@@ -53,6 +53,7 @@ constexpr int kDecBuf = kDecPre + kDecStage + 64;
 constexpr int kDecSlots = 128;
 constexpr int kDecStride = 16;                   // slots per restart interval (single-walk path)
 constexpr int kDecWarpBytes = 2 * kDecBuf + kDecSlots * 8 + 16;  // 2 staging buffers, 1 slot array
+static_assert(sizeof(CrcSmem) + kDecWarps * kDecWarpBytes <= 232448, "decode smem over the 227 KB limit");
 
 struct DecSlot {
   uint32_t pos;  // block-relative offset of the key suffix
@@ -135,14 +136,19 @@ __device__ uint32_t block_walk_exact(const uint8_t* d, uint64_t payload, uint64_
   return pos != entries_end ? B_TRAILING : B_OK;
 }
 
-constexpr int kDecTile = 2;  // consecutive blocks per warp tile (one look-back per tile)
+constexpr int kDecTile = 2;  // staging buffers per warp (double buffer)
 
-struct DecWarp {
-  uint8_t* buf[kDecTile];
-  uint64_t* bar[kDecTile];
-  uint32_t phase[kDecTile];
-  DecSlot* slots[kDecTile];
-};
+// Per-warp smem layout (offsets from the warp's base `wb`, all smem-derived
+// pointers so the compiler emits LDS/STS):
+//   [0, kDecBuf)            staging buffer 0
+//   [kDecBuf, 2 kDecBuf)    staging buffer 1
+//   [2 kDecBuf, +1 KB)      entry slots
+//   then 2 mbarriers
+__device__ __forceinline__ uint8_t* dec_buf(uint8_t* wb, int which) { return wb + which * kDecBuf; }
+__device__ __forceinline__ DecSlot* dec_slots(uint8_t* wb) { return reinterpret_cast<DecSlot*>(wb + kDecTile * kDecBuf); }
+__device__ __forceinline__ uint64_t* dec_bar(uint8_t* wb, int which) {
+  return reinterpret_cast<uint64_t*>(wb + kDecTile * kDecBuf + kDecSlots * 8) + which;
+}
 
 __device__ __forceinline__ uint32_t dec_window(const uint8_t* g, uint32_t len) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(g);
@@ -151,7 +157,6 @@ __device__ __forceinline__ uint32_t dec_window(const uint8_t* g, uint32_t len) {
 
 // Per-block state carried from phase 1 to phase 2.
 struct DecState {
-  const uint8_t* d;       // block bytes (smem staging or global)
   uint64_t addr;          // arena offset of the block
   uint32_t len;
   uint32_t nres;
@@ -163,14 +168,12 @@ struct DecState {
   uint64_t n;
   int32_t my_cnt, my_pre;
   uint32_t my_st, my_en;
-  bool staged;
-  bool valid;
 };
 
 // Issue the TMA staging of block b into buffer `which` (lane 0). Returns
 // whether the block is staged (else it is read in place).
 template <int W>
-__device__ __forceinline__ bool dec_prefetch(const DecodeArgs<W>& a, uint32_t b, DecWarp& w, int which) {
+__device__ __forceinline__ bool dec_prefetch(const DecodeArgs<W>& a, uint32_t b, uint8_t* wb, int which) {
   if (b >= a.nblk) return false;
   const uint32_t len = a.bt.len[b];
   const uint8_t* g = a.arena + a.bt.addr[b];
@@ -178,34 +181,23 @@ __device__ __forceinline__ bool dec_prefetch(const DecodeArgs<W>& a, uint32_t b,
   if (len < 12 || win > (uint32_t)kDecStage) return false;
   if (lane_id() == 0) {
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(w.bar[which], win);
-    bulk_g2s(w.buf[which] + kDecPre, reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(g) & ~uintptr_t(15)),
-             win, w.bar[which]);
+    mbar_arrive_expect_tx(dec_bar(wb, which), win);
+    bulk_g2s(dec_buf(wb, which) + kDecPre,
+             reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(g) & ~uintptr_t(15)), win,
+             dec_bar(wb, which));
   }
   return true;
 }
 
 // Phase 1: structural checks + entry walk (counts; single-walk fills slots).
 template <int W>
-__device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t b, bool staged, DecWarp& w,
-                                               int which) {
+__device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t b, const uint8_t* d,
+                                               DecSlot* slots) {
   const uint32_t lane = lane_id();
   DecState st{};
-  st.valid = b < a.nblk;
-  if (!st.valid) return st;
   st.len = a.bt.len[b];
   st.addr = a.bt.addr[b];
-  st.staged = staged;
   const uint32_t K = a.K;
-  const uint8_t* g = a.arena + st.addr;
-  const uint8_t* d = g;
-  if (staged) {
-    mbar_wait(w.bar[which], w.phase[which]);
-    w.phase[which] ^= 1u;
-    d = w.buf[which] + kDecPre + (reinterpret_cast<uintptr_t>(g) & 15);
-  }
-  st.d = d;
-  DecSlot* slots = w.slots[which];
   const uint32_t len = st.len;
   st.code = len < 12 ? (uint32_t)B_SHORT : 0u;
   if (!st.code) {
@@ -254,26 +246,25 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
   return st;
 }
 
-// Phase 2: CRC verify, then records at out[base ...].
-template <int W>
+// Phase 2: CRC verify, then records at out[base ...]. kStaged: `d` is the
+// smem copy (CRC in place); else the block is read from global memory and its
+// CRC staged pass by pass through `stage`.
+template <int W, bool kStaged>
 __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, DecState& st, uint64_t base,
-                                           DecWarp& w, int which, const CrcSmem& cs) {
+                                           const uint8_t* d, DecSlot* slots, uint8_t* stage, const CrcSmem& cs) {
   constexpr int NW = 2 * W + 2;
   const uint32_t lane = lane_id();
   const uint32_t K = a.K;
-  const uint8_t* d = st.d;
   const uint32_t len = st.len;
-  DecSlot* slots = w.slots[which];
   uint32_t code = st.code;
   if (!code) {
     uint32_t crc;
-    if (st.staged) {
+    if (kStaged) {
       crc = warp_crc32_smem(const_cast<uint8_t*>(d), len - 4, cs);
     } else {
-      const uint8_t* g = a.arena + st.addr;
       const uint64_t np = ((uint64_t)len - 4 + kGroup - 1) / kGroup;
       uint32_t raw = 0;
-      for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(g, len - 4, q, w.buf[which], cs);
+      for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(d, len - 4, q, stage, cs);
       crc = ~raw;
     }
     if (crc != ld_u32_le(d + len - 4)) code = B_CRC;
@@ -281,7 +272,7 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
     else code = st.pcode;
   }
   const uint64_t n = st.n;
-  if (code || st.unsup || base + n > a.cap) {  // capacity overflow: the host re-runs with exact capacity
+  if (code || st.unsup || base + n > a.cap) {
     if (lane == 0 && code) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
     if (lane == 0 && !code && st.unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | st.unsup);
     return;
@@ -333,9 +324,9 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
       uint32_t kw[NW];
       {
         const uint8_t* V = d + sl.pos - s;  // key byte i at V + i
-        const uintptr_t va = reinterpret_cast<uintptr_t>(V);
-        const uint32_t* wp = reinterpret_cast<const uint32_t*>(va & ~uintptr_t(3));
-        const uint32_t sh = (uint32_t)(va & 3u) * 8u;
+        const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(V) & 3u);
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(V - mis);
+        const uint32_t sh = mis * 8u;
         uint32_t lo = act ? wp[0] : 0u;
 #pragma unroll
         for (int i = 0; i < NW; ++i) {
@@ -384,6 +375,24 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   }
 }
 
+template <int W, bool kStaged>
+__device__ __forceinline__ void dec_block(const DecodeArgs<W>& a, uint32_t b, uint8_t* wb, int which,
+                                          uint32_t& phase, const CrcSmem& cs) {
+  uint8_t* buf = dec_buf(wb, which);
+  const uint8_t* g = a.arena + a.bt.addr[b];
+  const uint8_t* d;
+  if (kStaged) {
+    mbar_wait(dec_bar(wb, which), (phase >> which) & 1u);
+    phase ^= 1u << which;
+    d = buf + kDecPre + (reinterpret_cast<uintptr_t>(g) & 15);
+  } else {
+    d = g;
+  }
+  DecSlot* slots = dec_slots(wb);
+  DecState st = dec_phase1(a, b, d, slots);
+  dec_phase2<W, kStaged>(a, b, st, a.blk_base[b], d, slots, buf, cs);
+}
+
 // Entry count of one block with exactly the decision procedure of phase 1:
 // fast restart-interval walk if the block is canonical, else the exact
 // sequential walk (count up to the first error). Thread-level, header bytes
@@ -426,32 +435,26 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
   uint8_t* wb = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kDecWarpBytes;
-  DecWarp w;
-#pragma unroll
-  for (int i = 0; i < kDecTile; ++i) {
-    w.buf[i] = wb + i * kDecBuf;
-    w.slots[i] = reinterpret_cast<DecSlot*>(wb + kDecTile * kDecBuf);  // one block in flight at a time
-    w.bar[i] = reinterpret_cast<uint64_t*>(wb + kDecTile * kDecBuf + kDecSlots * 8) + i;
-    w.phase[i] = 0;
-  }
   const uint32_t lane = lane_id();
   crc_smem_init(cs);
-  if (lane == 0)
-    for (int i = 0; i < kDecTile; ++i) mbar_init(w.bar[i], 1);
+  if (lane == 0) {
+    mbar_init(dec_bar(wb, 0), 1);
+    mbar_init(dec_bar(wb, 1), 1);
+  }
   __syncthreads();
   // Record bases come from the count pre-pass (blk_base), so blocks are
   // independent: static round-robin assignment, the next block's TMA staging
   // in flight while the current one is processed.
   const uint32_t nw = gridDim.x * kDecWarps;
   uint32_t cur = blockIdx.x * kDecWarps + (threadIdx.x >> 5);
+  uint32_t phase = 0;
   int which = 0;
-  bool cur_staged = dec_prefetch(a, cur, w, which);
+  bool cur_staged = dec_prefetch(a, cur, wb, which);
   while (cur < a.nblk) {
     const uint32_t nxt = cur + nw;
-    const bool nxt_staged = dec_prefetch(a, nxt, w, which ^ 1);
-    DecState st = dec_phase1(a, cur, cur_staged, w, which);
-    const uint64_t base = a.blk_base[cur];
-    dec_phase2(a, cur, st, base, w, which, cs);
+    const bool nxt_staged = dec_prefetch(a, nxt, wb, which ^ 1);
+    if (cur_staged) dec_block<W, true>(a, cur, wb, which, phase, cs);
+    else dec_block<W, false>(a, cur, wb, which, phase, cs);
     fence_proxy_async_smem();  // generic smem accesses before the next TMA into this buffer
     __syncwarp();
     cur = nxt;

@@ -29,8 +29,9 @@ constexpr int kEncWarps = 16;
 constexpr int kEncStage = 4608;                        // blocks up to this size are assembled in smem
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
-constexpr int kEncStg = 6144;                          // per-warp TMA staging for value windows
-constexpr int kEncWarpBytes = kEncBuf + kEncStg + 16;  // + mbarrier
+constexpr int kEncStg = 5632;                          // per-warp TMA staging for value windows
+constexpr int kEncWarpBytes = kEncBuf + kEncStg + 16 + 512;  // + mbarrier + copy scratch
+static_assert(sizeof(CrcSmem) + kEncWarps * kEncWarpBytes <= 232448, "encode smem over the 227 KB limit");
 
 // Copy n bytes src → dst (any alignment; dst generic: smem or global) with
 // `nl` cooperating threads (rank `r`). Destination-aligned 32-bit words are
@@ -153,27 +154,18 @@ struct EncodeArgs {
   uint8_t* out;
 };
 
-template <int W>
-__device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_t k, uint8_t* wbuf, uint8_t* stg,
-                                                 uint64_t* bar, uint32_t& phase, const CrcSmem& cs) {
+template <int W, bool kStaged>
+__device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_t k, uint64_t first, uint32_t cnt,
+                                                 uint32_t size, uint64_t out_off, uint8_t* wbuf, uint8_t* stg,
+                                                 uint64_t* bar, uint32_t& phase, uint32_t* pre,
+                                                 const CrcSmem& cs) {
   const uint32_t lane = lane_id();
-  const uint64_t first = a.blk_first[k];
-  const uint32_t cnt = a.blk_n[k];
-  const uint32_t size = a.blk_size[k];
   const uint32_t K = a.K, L = K - 8, ri = a.ri;
-  // owning SST: last s with sst_first_blk[s] <= k
-  uint32_t lo = 0, hi = a.nsst;
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a.sst_first_blk[mid] <= k) lo = mid;
-    else hi = mid;
-  }
-  const uint64_t out_off = a.sst_off[lo] + (a.blk_pos[k] - a.blk_pos[a.sst_first_blk[lo]]);
   const uint32_t nres = (cnt + ri - 1) / ri;
   const uint32_t entries_end = size - 8 - 4 * nres;
-  const bool staged = size <= (uint32_t)kEncStage;
+  constexpr bool staged = kStaged;
   uint8_t* sbase = wbuf + kEncPre;
-  uint8_t* dst = staged ? sbase + (out_off & 15) : a.out + out_off;
+  uint8_t* dst = kStaged ? sbase + (out_off & 15) : a.out + out_off;
   uint32_t carry = 0;
   for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
     const uint32_t i = c0 + lane;
@@ -223,13 +215,8 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
       mbar_wait(bar, phase);
       phase ^= 1u;
       const uint32_t soff = inc - my + (uint32_t)(vs & 15u);
-      for (uint32_t m = tmask; m; m &= m - 1) {
-        const uint32_t j = __ffs(m) - 1;
-        const uint32_t so = __shfl_sync(0xFFFFFFFFu, soff, j);
-        const uint32_t dp = __shfl_sync(0xFFFFFFFFu, dpos, j);
-        const uint32_t sl = __shfl_sync(0xFFFFFFFFu, vl, j);
-        warp_smem_copy(dst + dp, stg + so, sl, lane);
-      }
+      warp_copy_ranges16(kStaged ? sbase : a.out + (out_off & ~15ull), stg, (uint32_t)(out_off & 15u) + dpos, soff,
+                         take ? vl : 0u, pre);
       __syncwarp();
       pending &= ~tmask;
     }
@@ -286,13 +273,30 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
   uint8_t* wbuf = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kEncWarpBytes;
   uint8_t* stg = wbuf + kEncBuf;
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kEncStg);
+  uint32_t* pre = reinterpret_cast<uint32_t*>(stg + kEncStg + 16);
   crc_smem_init(cs);
   if (lane_id() == 0) mbar_init(bar, 1);
   __syncthreads();
   uint32_t phase = 0;
   const uint32_t gw = blockIdx.x * kEncWarps + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kEncWarps;
-  for (uint32_t k = gw; k < a.nblk; k += nw) encode_one_block<W>(a, k, wbuf, stg, bar, phase, cs);
+  for (uint32_t k = gw; k < a.nblk; k += nw) {
+    const uint64_t first = a.blk_first[k];
+    const uint32_t cnt = a.blk_n[k];
+    const uint32_t size = a.blk_size[k];
+    // owning SST: last s with sst_first_blk[s] <= k
+    uint32_t lo = 0, hi = a.nsst;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (a.sst_first_blk[mid] <= k) lo = mid;
+      else hi = mid;
+    }
+    const uint64_t out_off = a.sst_off[lo] + (a.blk_pos[k] - a.blk_pos[a.sst_first_blk[lo]]);
+    if (size <= (uint32_t)kEncStage)
+      encode_one_block<W, true>(a, k, first, cnt, size, out_off, wbuf, stg, bar, phase, pre, cs);
+    else
+      encode_one_block<W, false>(a, k, first, cnt, size, out_off, wbuf, stg, bar, phase, pre, cs);
+  }
 }
 
 // ---- per-SST filter + index + footer -----------------------------------------------------
