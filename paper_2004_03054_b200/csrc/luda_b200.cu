@@ -478,7 +478,11 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   CK(cudaMemcpyAsync(d_soff, soff.data(), 8ull * nsst, cudaMemcpyHostToDevice, st));
   GET(d_keys, uint8_t, 2ull * nsst * p.K, false);
   // ---- encode data blocks ----
-  EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off, res->out};
+  GET(blk_out, uint64_t, nblk, false);
+  block_out_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, sch.nodes, nsst, sst_off, blk_out);
+  ++g_launches;
+  EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off,
+                   blk_out, res->out};
   const size_t esm = sizeof(CrcSmem) + (size_t)kEncWarps * kEncWarpBytes;
   CK(cudaFuncSetAttribute(encode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
   const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncWarps - 1) / kEncWarps, (uint64_t)g_num_sms);

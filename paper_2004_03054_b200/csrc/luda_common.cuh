@@ -292,60 +292,93 @@ __device__ __forceinline__ T warp_max(T v) {
 
 // Warp copy of up to 32 (src, dst, n) ranges (one per lane; n = 0 for idle
 // lanes; base_dst and base_src 16-byte aligned, src in smem, dst smem or
-// global), any alignments, flattened over 16-byte destination chunks:
-// lane t of each round realigns one chunk with two LDS.128 + funnel shifts
-// and writes it with one STS.128; the first/last chunk of a range are written
-// per word (partial words read-modify-written — distinct ranges are >= 12
-// bytes apart so they never share a word). `pre` = smem scratch of 33 words.
-// Source windows must be readable 16 bytes beyond each range.
+// global), any alignments. Pass 1 (branch-free): the INTERIOR 16-byte
+// destination chunks of all ranges, flattened over lanes through a
+// chunk→range map; each is realigned from two LDS.128 with funnel shifts and
+// written with one STS.128. Pass 2: the <= 2 partial edge chunks per range,
+// one per lane, written per word (partial words read-modify-written —
+// distinct ranges are >= 12 bytes apart so they never share a word).
+// `scratch` = smem of 512 + kCopyMap bytes; the interior chunk count of one
+// call must be <= kCopyMap (callers bound it by their staging size). Source
+// windows must be readable 16 bytes beyond each range.
+constexpr int kCopyMap = 512;
+__device__ __forceinline__ void copy_chunk16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dchunk,
+                                             int32_t sstart, uint32_t& v0, uint32_t& v1, uint32_t& v2,
+                                             uint32_t& v3) {
+  const uint32_t o = (uint32_t)sstart & 15u;
+  const uint4* sp = reinterpret_cast<const uint4*>(base_src + (sstart - (int32_t)o));
+  const uint4 A = sp[0], B = sp[1];
+  const uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+  const uint32_t q = o >> 2, sh = (o & 3u) * 8u;
+  uint32_t x[6], y[5];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) x[k] = (q & 2u) ? w[k + 2] : w[k];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) y[k] = (q & 1u) ? x[k + 1] : x[k];
+  v0 = __funnelshift_r(y[0], y[1], sh);
+  v1 = __funnelshift_r(y[1], y[2], sh);
+  v2 = __funnelshift_r(y[2], y[3], sh);
+  v3 = __funnelshift_r(y[3], y[4], sh);
+}
+
 __device__ __forceinline__ void warp_copy_ranges16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
-                                                   uint32_t src_off, uint32_t n, uint32_t* pre) {
+                                                   uint32_t src_off, uint32_t n, uint32_t* scratch) {
   const uint32_t lane = lane_id();
-  const uint32_t dmis = dst_off & 15u;
-  const uint32_t nch = n ? (dmis + n + 15) >> 4 : 0u;
-  const uint32_t incl = warp_incl_scan<uint32_t>(nch);
+  uint32_t* rd = scratch;          // [32] dst offsets
+  uint32_t* rs = scratch + 32;     // [32] src offsets
+  uint32_t* rn = scratch + 64;     // [32] lengths
+  uint32_t* rf = scratch + 96;     // [32] first flattened interior chunk of each range
+  uint8_t* map = reinterpret_cast<uint8_t*>(scratch + 128);  // [kCopyMap] interior chunk → range
+  const uint32_t c0 = (dst_off + 15) & ~15u;             // first interior chunk (offset)
+  const uint32_t c1 = (dst_off + n) & ~15u;              // end of interior chunks
+  const uint32_t nint = (n && c1 > c0) ? (c1 - c0) >> 4 : 0u;
+  const uint32_t incl = warp_incl_scan<uint32_t>(nint);
   const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  pre[lane] = incl - nch;                         // first chunk of range `lane`
-  pre[32 + lane] = dst_off;
-  pre[64 + lane] = src_off;
-  pre[96 + lane] = n;
+  rd[lane] = dst_off;
+  rs[lane] = src_off;
+  rn[lane] = n;
+  rf[lane] = incl - nint;
+  for (uint32_t i = incl - nint; i < incl; ++i) map[i] = (uint8_t)lane;  // total <= kCopyMap (staging bound)
   __syncwarp();
+  // pass 1: interior chunks, branch-free
   for (uint32_t t = lane; t < total; t += 32) {
-    // range j: last lane with pre[j] <= t (ranges with nch = 0 share starts; take the last)
-    uint32_t j = 0;  // largest j with pre[j] <= t (empty ranges sharing a start come first)
-#pragma unroll
-    for (uint32_t step = 16; step >= 1; step >>= 1)
-      if (j + step < 32 && pre[j + step] <= t) j += step;
-    const uint32_t dj = pre[32 + j], sj = pre[64 + j], nj = pre[96 + j];
-    const uint32_t i = t - pre[j];
-    const uint32_t dchunk = (dj & ~15u) + 16u * i;          // dst chunk offset
-    const int32_t sstart = (int32_t)(sj + dchunk) - (int32_t)dj;  // src offset of dst chunk byte 0
-    const uint32_t o = (uint32_t)sstart & 15u;
-    const uint4* sp = reinterpret_cast<const uint4*>(base_src + (sstart - (int32_t)o));
-    const uint4 A = sp[0], B = sp[1];
-    uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
-    const uint32_t q = o >> 2, sh = (o & 3u) * 8u;
-    uint32_t x[6], y[5];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) x[k] = (q & 2u) ? w[k + 2] : w[k];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) y[k] = (q & 1u) ? x[k + 1] : x[k];
-    uint32_t v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = __funnelshift_r(y[k], y[k + 1], sh);
-    uint32_t* dw = reinterpret_cast<uint32_t*>(base_dst + dchunk);
-    const uint32_t lo = dchunk < dj ? dj - dchunk : 0u;                 // first valid byte in chunk
-    const uint32_t hi = (dchunk + 16 > dj + nj) ? dj + nj - dchunk : 16u;  // one past last valid byte
-    if (lo == 0 && hi == 16) {
-      *reinterpret_cast<uint4*>(dw) = make_uint4(v[0], v[1], v[2], v[3]);
+    const uint32_t j = map[t];
+    const uint32_t dj = rd[j], sj = rs[j];
+    const uint32_t dchunk = ((dj + 15) & ~15u) + 16u * (t - rf[j]);
+    const int32_t sstart = (int32_t)(sj + dchunk) - (int32_t)dj;
+    uint32_t v0, v1, v2, v3;
+    copy_chunk16(base_dst, base_src, dchunk, sstart, v0, v1, v2, v3);
+    *reinterpret_cast<uint4*>(base_dst + dchunk) = make_uint4(v0, v1, v2, v3);
+  }
+  // pass 2: edge chunks: lane e → range e>>1, side e&1 (head / tail)
+  for (uint32_t e = lane; e < 64; e += 32) {
+    const uint32_t j = e >> 1;
+    const uint32_t dj = rd[j], sj = rs[j], nj = rn[j];
+    if (nj == 0) continue;
+    const uint32_t head = (dj & ~15u);
+    const uint32_t tail = (dj + nj - 1) & ~15u;
+    uint32_t dchunk;
+    if ((e & 1) == 0) {
+      if ((dj & 15u) == 0 && (dj + nj >= head + 16)) continue;  // head chunk fully interior
+      dchunk = head;
     } else {
+      if (tail == head) continue;                                 // single chunk: done by the head lane
+      if (((dj + nj) & 15u) == 0) continue;                       // tail chunk fully interior
+      dchunk = tail;
+    }
+    const int32_t sstart = (int32_t)(sj + dchunk) - (int32_t)dj;
+    uint32_t v[4];
+    copy_chunk16(base_dst, base_src, dchunk, sstart, v[0], v[1], v[2], v[3]);
+    const uint32_t lo = dchunk < dj ? dj - dchunk : 0u;
+    const uint32_t hi = (dchunk + 16 > dj + nj) ? dj + nj - dchunk : 16u;
+    uint32_t* dw = reinterpret_cast<uint32_t*>(base_dst + dchunk);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int32_t a = (int32_t)lo - 4 * k, b = (int32_t)hi - 4 * k;  // valid bytes [a, b) of word k
-        if (b <= 0 || a >= 4) continue;
-        const uint32_t m = (b >= 4 ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u)) & (a <= 0 ? 0xFFFFFFFFu : ~((1u << (8 * a)) - 1u));
-        dw[k] = m == 0xFFFFFFFFu ? v[k] : ((dw[k] & ~m) | (v[k] & m));
-      }
+    for (int k = 0; k < 4; ++k) {
+      const int32_t a = (int32_t)lo - 4 * k, b = (int32_t)hi - 4 * k;  // valid bytes [a, b) of word k
+      if (b <= 0 || a >= 4) continue;
+      const uint32_t m =
+          (b >= 4 ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u)) & (a <= 0 ? 0xFFFFFFFFu : ~((1u << (8 * a)) - 1u));
+      dw[k] = m == 0xFFFFFFFFu ? v[k] : ((dw[k] & ~m) | (v[k] & m));
     }
   }
   __syncwarp();

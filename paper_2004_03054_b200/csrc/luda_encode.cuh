@@ -29,8 +29,9 @@ constexpr int kEncWarps = 16;
 constexpr int kEncStage = 4608;                        // blocks up to this size are assembled in smem
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
-constexpr int kEncStg = 5632;                          // per-warp TMA staging for value windows
-constexpr int kEncWarpBytes = kEncBuf + kEncStg + 16 + 512;  // + mbarrier + copy scratch
+constexpr int kEncStg = 5120;                          // per-warp TMA staging for value windows
+constexpr int kEncWarpBytes = kEncBuf + kEncStg + 16 + 512 + kCopyMap;  // + mbarrier + copy scratch
+static_assert(kEncStg / 16 <= kCopyMap, "copy map smaller than the staging chunk count");
 static_assert(sizeof(CrcSmem) + kEncWarps * kEncWarpBytes <= 232448, "encode smem over the 227 KB limit");
 
 // Copy n bytes src → dst (any alignment; dst generic: smem or global) with
@@ -151,8 +152,23 @@ struct EncodeArgs {
   const uint32_t* sst_first_blk;
   uint32_t nsst;
   const uint64_t* sst_off;
+  const uint64_t* blk_out;   // output offset of every block
   uint8_t* out;
 };
+
+// Output offset of every block: its SST's offset + its data offset in the SST.
+__global__ void block_out_kernel(const uint64_t* blk_pos, uint32_t nblk, const uint32_t* sst_first_blk,
+                                 uint32_t nsst, const uint64_t* sst_off, uint64_t* blk_out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nblk) return;
+  uint32_t lo = 0, hi = nsst;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sst_first_blk[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  blk_out[k] = sst_off[lo] + (blk_pos[k] - blk_pos[sst_first_blk[lo]]);
+}
 
 template <int W, bool kStaged>
 __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_t k, uint64_t first, uint32_t cnt,
@@ -167,15 +183,29 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
   uint8_t* sbase = wbuf + kEncPre;
   uint8_t* dst = kStaged ? sbase + (out_off & 15) : a.out + out_off;
   uint32_t carry = 0;
+  Rec<W> prev_rec;  // entry c0-1 (only used when the block has > 32 entries)
+#pragma unroll
+  for (int q = 0; q < W; ++q) prev_rec.k[q] = 0;
+  prev_rec.t = 0;
+  prev_rec.h = 0;
   for (uint32_t c0 = 0; c0 < cnt; c0 += 32) {
     const uint32_t i = c0 + lane;
     const bool act = i < cnt;
     Rec<W> r;
     if (act) r = a.rec[first + i];
+    // previous record: from lane-1 (lane 0: the last record of the previous chunk)
+    Rec<W> pr;
+#pragma unroll
+    for (int q = 0; q < W; ++q) pr.k[q] = __shfl_up_sync(0xFFFFFFFFu, r.k[q], 1);
+    pr.t = __shfl_up_sync(0xFFFFFFFFu, r.t, 1);
+    if (lane == 0) pr = prev_rec;
+#pragma unroll
+    for (int q = 0; q < W; ++q) prev_rec.k[q] = __shfl_sync(0xFFFFFFFFu, r.k[q], 31);
+    prev_rec.t = __shfl_sync(0xFFFFFFFFu, r.t, 31);
     uint32_t s = 0, u = 0, vl = 0, hv = 0, esz = 0;
     uint64_t voff = 0;
     if (act) {
-      if (i % ri != 0) s = ikey_lcp(a.rec[first + i - 1], r, L);
+      if (i % ri != 0) s = ikey_lcp(pr, r, L);
       u = K - s;
       vl = handle_len(r.h);
       voff = handle_off(r.h);
@@ -252,15 +282,13 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
     const uint32_t c_last = ((g + size) & 15u) ? nch - 1 : nch;  // exclusive
     for (uint32_t c = c_first + lane; c < c_last; c += 32)
       *reinterpret_cast<uint4*>(g0 + 16ull * c) = *reinterpret_cast<const uint4*>(sbase + 16 * c);
-    // partial head / tail chunks: bytewise (neighbouring blocks own the rest)
-    if (lane < 2) {
-      const bool head = lane == 0;
-      const uint32_t c = head ? 0u : nch - 1;
-      if ((head && c_first == 1) || (!head && c_last == nch - 1 && !(c == 0 && c_first == 1))) {
-        const uintptr_t A = g0 + 16ull * c;
-        for (int b = 0; b < 16; ++b)
-          if (A + b >= g && A + b < g + size) reinterpret_cast<uint8_t*>(A)[b] = sbase[16 * c + b];
-      }
+    // partial head / tail chunks: bytewise, lanes 0-15 head, 16-31 tail (neighbouring blocks own the rest)
+    {
+      const uint32_t c = lane < 16 ? 0u : nch - 1;
+      const bool partial = lane < 16 ? (c_first == 1) : (c_last == nch - 1 && !(c == 0 && c_first == 1));
+      const uint32_t bb = lane & 15u;
+      const uintptr_t A = g0 + 16ull * c + bb;
+      if (partial && A >= g && A < g + size) *reinterpret_cast<uint8_t*>(A) = sbase[16 * c + bb];
     }
   }
   __syncwarp();
@@ -284,14 +312,7 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
     const uint64_t first = a.blk_first[k];
     const uint32_t cnt = a.blk_n[k];
     const uint32_t size = a.blk_size[k];
-    // owning SST: last s with sst_first_blk[s] <= k
-    uint32_t lo = 0, hi = a.nsst;
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (a.sst_first_blk[mid] <= k) lo = mid;
-      else hi = mid;
-    }
-    const uint64_t out_off = a.sst_off[lo] + (a.blk_pos[k] - a.blk_pos[a.sst_first_blk[lo]]);
+    const uint64_t out_off = a.blk_out[k];
     if (size <= (uint32_t)kEncStage)
       encode_one_block<W, true>(a, k, first, cnt, size, out_off, wbuf, stg, bar, phase, pre, cs);
     else
