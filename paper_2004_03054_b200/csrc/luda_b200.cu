@@ -390,7 +390,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(bsz, uint32_t, n, false);
   GET(ctl, unsigned int, 4, true);  // jmax, overflow, jmax_sst
   BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1};
-  const size_t jsm = 2ull * (kJumpTile + halo) * 4;
+  const size_t jsm = (2ull * (kJumpTile + halo) + 1) * 4;
   CK(cudaFuncSetAttribute(block_jump_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
   KT_START(2, st);
   block_jump_kernel<W><<<(unsigned)((n + kJumpTile - 1) / kJumpTile), kJumpThreads, jsm, st>>>(ja);

@@ -118,6 +118,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[kMergeThreads / 32];
   __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_total;
+  __shared__ __align__(8) uint64_t s_bar;
+  constexpr bool kTma = (sizeof(Rec<W>) % 16) == 0;
   const uint32_t tid = threadIdx.x;
   uint64_t tile;
   if (m.ra.resolve) {
@@ -134,16 +137,26 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   const uint64_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t na_t = (uint32_t)(a1 - a0), nb_t = (uint32_t)(b1 - b0);
   const uint32_t nt = na_t + nb_t;
-  // load slices (8-byte words, coalesced)
-  {
+  // ---- load the A and B slices: TMA bulk copies (or vector loads) ----
+  if (kTma) {
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      const uint32_t bytes = nt * (uint32_t)sizeof(Rec<W>);
+      mbar_arrive_expect_tx(&s_bar, bytes);
+      if (na_t) bulk_g2s(S, m.A + a0, na_t * (uint32_t)sizeof(Rec<W>), &s_bar);
+      if (nb_t) bulk_g2s(S + na_t, m.B + b0, nb_t * (uint32_t)sizeof(Rec<W>), &s_bar);
+    }
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+  } else {
     constexpr int RW = sizeof(Rec<W>) / 8;
     const uint64_t* ga = reinterpret_cast<const uint64_t*>(m.A + a0);
     const uint64_t* gb = reinterpret_cast<const uint64_t*>(m.B + b0);
-    uint64_t* s = reinterpret_cast<uint64_t*>(S);
-    for (uint32_t i = tid; i < na_t * RW; i += kMergeThreads) s[i] = ga[i];
-    for (uint32_t i = tid; i < nb_t * RW; i += kMergeThreads) s[na_t * RW + i] = gb[i];
+    uint64_t* sw = reinterpret_cast<uint64_t*>(S);
+    for (uint32_t i = tid; i < na_t * RW; i += kMergeThreads) sw[i] = ga[i];
+    for (uint32_t i = tid; i < nb_t * RW; i += kMergeThreads) sw[na_t * RW + i] = gb[i];
+    __syncthreads();
   }
-  __syncthreads();
   // strict-order check of both slices (including the seam to the previous tile)
   for (uint32_t i = tid; i < nt; i += kMergeThreads) {
     const bool inA = i < na_t;
@@ -157,8 +170,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     if (rec_cmp(prev, cur) >= 0)
       atomicMin(m.err_order, (unsigned long long)((inA ? m.a_run_base : m.b_run_base) + gpos));
   }
-  // per-thread merge of kMergeItems outputs
+  // ---- per-thread merge of kMergeItems outputs (heads kept in registers) ----
   const uint32_t p0 = tid * kMergeItems;
+  uint32_t keep_bits = 0, cnt = 0;
   if (p0 < nt) {
     uint32_t lo = p0 > nb_t ? p0 - nb_t : 0;
     uint32_t hi = p0 < na_t ? p0 : na_t;
@@ -168,6 +182,33 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
       else hi = mid;
     }
     uint32_t i = lo, j = p0 - lo;
+    Rec<W> ha, hb;
+    if (i < na_t) ha = S[i];
+    if (j < nb_t) hb = S[na_t + j];
+    // resolve: predecessor of output p0 in merge order
+    Rec<W> prev;
+    bool has_prev = false;
+    if (m.ra.resolve) {
+      if (p0 > 0) {
+        // the element output just before p0 is the larger of S[i-1] (A) and S[na_t+j-1] (B)
+        if (i > 0 && j > 0) {
+          const Rec<W>& pa = S[i - 1];
+          const Rec<W>& pb = S[na_t + j - 1];
+          prev = rec_le(pa, pb) ? pb : pa;
+        } else {
+          prev = i > 0 ? S[i - 1] : S[na_t + j - 1];
+        }
+        has_prev = true;
+      } else if (d0 > 0) {
+        if (a0 > 0 && b0 > 0) {
+          const Rec<W> pa = m.A[a0 - 1], pb = m.B[b0 - 1];
+          prev = rec_le(pa, pb) ? pb : pa;
+        } else {
+          prev = a0 > 0 ? m.A[a0 - 1] : m.B[b0 - 1];
+        }
+        has_prev = true;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < kMergeItems; ++k) {
       const uint32_t p = p0 + k;
@@ -175,55 +216,52 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
         bool takeA;
         if (i >= na_t) takeA = false;
         else if (j >= nb_t) takeA = true;
-        else takeA = rec_le(S[i], S[na_t + j]);
-        perm[p] = (uint16_t)(takeA ? i++ : na_t + j++);
+        else takeA = rec_le(ha, hb);
+        const Rec<W> cur = takeA ? ha : hb;
+        perm[p] = (uint16_t)(takeA ? i : na_t + j);
+        if (takeA) {
+          ++i;
+          if (i < na_t) ha = S[i];
+        } else {
+          ++j;
+          if (j < nb_t) hb = S[na_t + j];
+        }
+        if (m.ra.resolve) {
+          const bool first = !has_prev || !same_user(prev, cur);
+          bool keep = first && above_lo(cur, m.ra.range_lo) && below_hi(cur, m.ra.range_hi);
+          if (keep && is_tombstone(cur) && !covered_below(cur, m.ra)) keep = false;
+          if (keep) {
+            keep_bits |= 1u << k;
+            ++cnt;
+          }
+          prev = cur;
+          has_prev = true;
+        }
       }
     }
   }
   __syncthreads();
   if (!m.ra.resolve) {
-    constexpr int RW = sizeof(Rec<W>) / 8;
-    uint64_t* go = reinterpret_cast<uint64_t*>(m.out + d0);
-    const uint64_t* s = reinterpret_cast<const uint64_t*>(S);
-    for (uint32_t i = tid; i < nt * RW; i += kMergeThreads) go[i] = s[(uint32_t)perm[i / RW] * RW + i % RW];
+    constexpr int R16 = sizeof(Rec<W>) / 16;
+    if (R16 * 16 == sizeof(Rec<W>)) {
+      uint4* go = reinterpret_cast<uint4*>(m.out + d0);
+      const uint4* sv = reinterpret_cast<const uint4*>(S);
+      for (uint32_t i = tid; i < nt * R16; i += kMergeThreads) go[i] = sv[(uint32_t)perm[i / R16] * R16 + i % R16];
+    } else {
+      constexpr int RW = sizeof(Rec<W>) / 8;
+      uint64_t* go = reinterpret_cast<uint64_t*>(m.out + d0);
+      const uint64_t* sv = reinterpret_cast<const uint64_t*>(S);
+      for (uint32_t i = tid; i < nt * RW; i += kMergeThreads) go[i] = sv[(uint32_t)perm[i / RW] * RW + i % RW];
+    }
     return;
   }
-  // ---- resolve: keep flags ---------------------------------------------------
-  // predecessor of output d0 in merge order (last of A[a0-1], B[b0-1])
-  uint32_t keep_bits = 0, cnt = 0;
-  {
-    Rec<W> pred;
-    bool has_pred = false;
-    if (d0 > 0) {
-      if (a0 > 0 && b0 > 0) {
-        const Rec<W> pa = m.A[a0 - 1], pb = m.B[b0 - 1];
-        pred = rec_le(pa, pb) ? pb : pa;
-      } else {
-        pred = a0 > 0 ? m.A[a0 - 1] : m.B[b0 - 1];
-      }
-      has_pred = true;
-    }
-#pragma unroll
-    for (int k = 0; k < kMergeItems; ++k) {
-      const uint32_t p = p0 + k;
-      if (p < nt) {
-        const Rec<W>& cur = S[perm[p]];
-        bool first;
-        if (p == 0) first = !has_pred || !same_user(pred, cur);
-        else first = !same_user(S[perm[p - 1]], cur);
-        bool keep = first && above_lo(cur, m.ra.range_lo) && below_hi(cur, m.ra.range_hi);
-        if (keep && is_tombstone(cur) && !covered_below(cur, m.ra)) keep = false;
-        if (keep) { keep_bits |= 1u << k; ++cnt; }
-      }
-    }
-  }
-  // CTA exclusive scan of cnt
+  // ---- CTA exclusive scan of keep counts + decoupled look-back over tiles ----
   const uint32_t lane = lane_id(), wid = tid >> 5;
   const uint32_t incl = warp_incl_scan<uint32_t>(cnt);
   if (lane == 31) s_warp[wid] = incl;
   __syncthreads();
   if (wid == 0) {
-    uint32_t v = lane < kMergeThreads / 32 ? s_warp[lane] : 0;
+    const uint32_t v = lane < kMergeThreads / 32 ? s_warp[lane] : 0;
     const uint32_t vi = warp_incl_scan<uint32_t>(v);
     if (lane < kMergeThreads / 32) s_warp[lane] = vi - v;
     const uint32_t total = __shfl_sync(0xFFFFFFFFu, vi, 31);
@@ -232,6 +270,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     if (lane == 0) {
       lb_publish(m.lb, tile, kLbInc, ex + total);
       s_base = ex;
+      s_total = total;
       if (tile + 1 == m.ntiles) *m.n_out = ex + total;
     }
   }
@@ -241,17 +280,19 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   for (int k = 0; k < kMergeItems; ++k)
     if (keep_bits & (1u << k)) comp[w++] = perm[p0 + k];
   __syncthreads();
-  const uint32_t kept = s_warp[kMergeThreads / 32 - 1] + 0;  // placeholder, recomputed below
-  (void)kept;
-  __shared__ uint32_t s_total;
-  if (tid == kMergeThreads - 1) s_total = w;
-  __syncthreads();
   {
-    constexpr int RW = sizeof(Rec<W>) / 8;
-    uint64_t* go = reinterpret_cast<uint64_t*>(m.out + s_base);
-    const uint64_t* s = reinterpret_cast<const uint64_t*>(S);
     const uint32_t tot = s_total;
-    for (uint32_t i = tid; i < tot * RW; i += kMergeThreads) go[i] = s[(uint32_t)comp[i / RW] * RW + i % RW];
+    constexpr int R16 = sizeof(Rec<W>) / 16;
+    if (R16 * 16 == sizeof(Rec<W>) && (s_base * sizeof(Rec<W>)) % 16 == 0) {
+      uint4* go = reinterpret_cast<uint4*>(m.out + s_base);
+      const uint4* sv = reinterpret_cast<const uint4*>(S);
+      for (uint32_t i = tid; i < tot * R16; i += kMergeThreads) go[i] = sv[(uint32_t)comp[i / R16] * R16 + i % R16];
+    } else {
+      constexpr int RW = sizeof(Rec<W>) / 8;
+      uint64_t* go = reinterpret_cast<uint64_t*>(m.out + s_base);
+      const uint64_t* sv = reinterpret_cast<const uint64_t*>(S);
+      for (uint32_t i = tid; i < tot * RW; i += kMergeThreads) go[i] = sv[(uint32_t)comp[i / RW] * RW + i % RW];
+    }
   }
 }
 

@@ -46,46 +46,98 @@ struct BlockJumpArgs {
   unsigned int* overflow;
 };
 
+// Block size if a block started at local index i held n entries:
+//   PB[i+n] - PB[i]                    compressed entry sizes (shared vs prev)
+// + sum_{k < m} D[i + k ri]            restart entries use the full size
+// + 4 m + 4                            restart array + count (pre-crc)
+// with m = ceil(n / ri). Within restart group k (n in (k ri, (k+1) ri]) m is
+// fixed, so the greedy cut is found group by group, then by binary search
+// inside the group that overflows.
 template <int W>
 __global__ void __launch_bounds__(kJumpThreads) block_jump_kernel(BlockJumpArgs<W> a) {
-  extern __shared__ __align__(16) uint32_t sz[];  // [2][kJumpTile + halo]: full, compressed
+  extern __shared__ __align__(16) uint32_t sz[];  // PB[span+1], D[span]
   const uint32_t span = kJumpTile + a.halo;
-  uint32_t* sa = sz;
-  uint32_t* sb = sz + span;
+  uint32_t* PB = sz;
+  uint32_t* D = sz + span + 1;
+  __shared__ uint32_t s_warp[kJumpThreads / 32];
   const uint64_t t0 = (uint64_t)blockIdx.x * kJumpTile;
-  const uint32_t K = a.K;
-  const uint32_t vK = varint_size(K);
-  for (uint32_t i = threadIdx.x; i < span; i += kJumpThreads) {
+  const uint32_t K = a.K, L = K - 8, vK = varint_size(K);
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  // sizes → D (full - compressed) and a CTA-wide exclusive scan PB of compressed sizes
+  __shared__ uint32_t s_total;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < span; base += kJumpThreads) {
+    const uint32_t i = base + threadIdx.x;
     const uint64_t j = t0 + i;
-    if (j >= a.n) break;
-    const Rec<W> cur = a.rec[j];
-    const uint32_t vl = handle_len(cur.h);
-    const uint32_t vv = varint_size(vl);
-    sa[i] = 1 + vK + vv + K + vl;
-    uint32_t s = 0;
-    if (j > 0) s = ikey_lcp(a.rec[j - 1], cur, K - 8);
-    sb[i] = varint_size(s) + varint_size(K - s) + vv + (K - s) + vl;
+    uint32_t sbv = 0;
+    if (i < span && j < a.n) {
+      const Rec<W> cur = a.rec[j];
+      const uint32_t vl = handle_len(cur.h);
+      const uint32_t vv = varint_size(vl);
+      uint32_t sh = 0;
+      if (j > 0) sh = ikey_lcp(a.rec[j - 1], cur, L);
+      sbv = varint_size(sh) + varint_size(K - sh) + vv + (K - sh) + vl;
+      D[i] = (1 + vK + vv + K + vl) - sbv;
+    } else if (i < span) {
+      D[i] = 0;
+    }
+    const uint32_t incl = warp_incl_scan<uint32_t>(sbv);
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t v = lane < kJumpThreads / 32 ? s_warp[lane] : 0u;
+      const uint32_t vi = warp_incl_scan<uint32_t>(v);
+      if (lane < kJumpThreads / 32) s_warp[lane] = vi - v;
+      if (lane == 31) s_total = vi;
+    }
+    __syncthreads();
+    if (i < span) PB[i] = carry + s_warp[wid] + incl - sbv;
+    carry += s_total;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) PB[span] = carry;
   __syncthreads();
+  const uint32_t ri = a.ri, bs = a.block_size;
   uint32_t mymax = 0;
   for (uint32_t i = threadIdx.x; i < (uint32_t)kJumpTile; i += kJumpThreads) {
     const uint64_t j = t0 + i;
     if (j >= a.n) break;
-    uint64_t size = 0;
-    uint32_t cnt = 0;
-    while (j + cnt < a.n) {
-      if (i + cnt >= span) { atomicExch(a.overflow, 1u); break; }
-      const uint32_t es = (cnt % a.ri == 0) ? sa[i + cnt] : sb[i + cnt];
-      if (cnt > 0 && size + es + 4ull * ((cnt + 1 + a.ri - 1) / a.ri) + 4 > a.block_size) break;
-      size += es;
-      ++cnt;
+    const uint64_t rem64 = a.n - j;
+    const uint32_t lim = (uint32_t)(rem64 < (uint64_t)(span - i) ? rem64 : (uint64_t)(span - i));  // entries available
+    uint32_t fixed = 0;  // sum of D over restart entries of groups < k, plus group k's once added
+    uint32_t best = 1, m = 0;
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t gs = k * ri;                 // group k covers n in (gs, gs + ri]
+      if (gs >= lim) break;
+      fixed += D[i + gs];
+      m = k + 1;
+      const uint32_t ge = gs + ri < lim ? gs + ri : lim;
+      const uint32_t full = PB[i + ge] - PB[i] + fixed + 4 * m + 4;
+      if (full <= bs) {
+        best = ge;
+        continue;
+      }
+      // largest n in (gs, ge) with size <= bs; n = 1 always fits (first entry)
+      uint32_t lo = gs, hi = ge - 1;  // invariant: n = lo fits (or lo == gs meaning none in group yet)
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (PB[i + mid] - PB[i] + fixed + 4 * m + 4 <= bs) lo = mid;
+        else hi = mid - 1;
+      }
+      if (lo > gs) best = lo;
+      else if (gs == 0) best = 1;
+      break;
     }
-    a.jmp[j] = cnt;
-    a.bsz[j] = (uint32_t)(size + 4ull * ((cnt + a.ri - 1) / a.ri) + 8);
-    mymax = cnt > mymax ? cnt : mymax;
+    if (best == lim && lim == span - i && rem64 > lim) atomicExch(a.overflow, 1u);
+    const uint32_t mb = (best + ri - 1) / ri;
+    uint32_t fx = 0;
+    for (uint32_t k = 0; k < mb; ++k) fx += D[i + k * ri];
+    a.jmp[j] = best;
+    a.bsz[j] = PB[i + best] - PB[i] + fx + 4 * mb + 8;
+    mymax = best > mymax ? best : mymax;
   }
   mymax = warp_max(mymax);
-  if (lane_id() == 0) atomicMax(a.jmax, mymax);
+  if (lane == 0) atomicMax(a.jmax, mymax);
 }
 
 // ---- SST jumps -------------------------------------------------------------------
