@@ -530,8 +530,10 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   std::vector<uint64_t> fbase(jd->n_files + 1);
   // count pre-pass + exclusive scan → first record index of every block
   GET(d_cnt, uint32_t, nblk, false);
-  block_count_kernel<<<std::min<uint32_t>((nblk + 255) / 256, 8 * g_num_sms), 256, 0, st>>>(jd->arena, bt, nblk, K,
-                                                                                         d_cnt);
+  GET(d_flags, uint32_t, nblk, false);
+  GET(d_gslots, DecSlot, (uint64_t)nblk * kSlotCap, false);
+  block_scan_kernel<<<std::min<uint32_t>((nblk + 255) / 256, 16 * g_num_sms), 256, 0, st>>>(jd->arena, bt, nblk, K,
+                                                                                          d_cnt, d_flags, d_gslots);
   ++g_launches;
   {
     const uint64_t nt = std::max<uint64_t>(1, (nblk + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
@@ -553,7 +555,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
   {
     CK(cudaMemsetAsync(errs, 0xFF, 16, st));
-    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, n_in, d_base, errs, errs + 1};
+    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, n_in, d_base, d_flags, d_gslots, errs, errs + 1};
     KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
     ++g_launches;

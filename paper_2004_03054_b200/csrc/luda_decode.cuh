@@ -60,6 +60,9 @@ struct DecSlot {
   uint32_t sv;   // value_len << 8 | shared
 };
 
+constexpr int kSlotCap = 48;         // scan-pass slots per block
+constexpr uint32_t kScanSlots = 1u;  // block flag: slots valid (no error, cnt <= kSlotCap)
+
 template <int W>
 struct DecodeArgs {
   const uint8_t* arena;
@@ -69,6 +72,8 @@ struct DecodeArgs {
   Rec<W>* out;
   uint64_t cap;
   const uint64_t* blk_base; // [nblk+1] first record index of each block (count pre-pass + scan)
+  const uint32_t* blk_flags;  // block_scan flags
+  const DecSlot* gslots;      // block_scan slots, kSlotCap per block
   unsigned long long* err_ref;
   unsigned long long* err_unsup;
 };
@@ -283,10 +288,10 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   uint32_t carry[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) carry[i] = 0;
-  const uint64_t wstep = mode == 1 ? n : (uint64_t)kDecSlots;
+  const uint64_t wstep = (mode == 1 || mode == 4) ? n : (uint64_t)kDecSlots;
   for (uint64_t w0 = 0; w0 < n; w0 += wstep) {
     const uint64_t w1 = w0 + kDecSlots;
-    if (mode != 1) {
+    if (mode != 1 && mode != 4) {
       auto put = [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
         if (j >= w0 && j < w1) slots[j - w0] = DecSlot{pos, (vl << 8) | s};
       };
@@ -389,45 +394,81 @@ __device__ __forceinline__ void dec_block(const DecodeArgs<W>& a, uint32_t b, ui
     d = g;
   }
   DecSlot* slots = dec_slots(wb);
-  DecState st = dec_phase1(a, b, d, slots);
-  dec_phase2<W, kStaged>(a, b, st, a.blk_base[b], d, slots, buf, cs);
+  const uint64_t base = a.blk_base[b];
+  DecState st;
+  if (a.blk_flags[b] & kScanSlots) {
+    // entries were located by the scan pass: no walk here
+    st = DecState{};
+    st.len = a.bt.len[b];
+    st.addr = a.bt.addr[b];
+    st.n = a.blk_base[b + 1] - base;
+    st.mode = 4;
+    const DecSlot* gs = a.gslots + (uint64_t)b * kSlotCap;
+    for (uint32_t e = lane_id(); e < st.n; e += 32) slots[e] = gs[e];
+    __syncwarp();
+  } else {
+    st = dec_phase1(a, b, d, slots);
+  }
+  dec_phase2<W, kStaged>(a, b, st, base, d, slots, buf, cs);
 }
 
-// Entry count of one block with exactly the decision procedure of phase 1:
-// fast restart-interval walk if the block is canonical, else the exact
-// sequential walk (count up to the first error). Thread-level, header bytes
-// read straight from global memory.
-__device__ __forceinline__ uint32_t block_count(const uint8_t* d, uint32_t len, uint32_t K) {
-  if (len < 12) return 0;
+// ---- block scan pre-pass ---------------------------------------------------------
+// One thread per block walks the entry headers straight from global memory
+// with exactly the decision procedure of phase 1 (canonical restart-interval
+// walk, else the exact sequential walk) and records the entry count, and —
+// when the block is error-free and has <= kSlotCap entries — every entry's
+// slot (key-suffix position, shared, value length). The decode kernel then
+// skips its own walk for those blocks; counts feed the scan that places
+// every block's records (no inter-block dependency inside decode).
+__device__ __forceinline__ void block_scan(const uint8_t* d, uint32_t len, uint32_t K, DecSlot* out, uint32_t& cnt,
+                                           uint32_t& flags) {
+  cnt = 0;
+  flags = 0;
+  if (len < 12) return;
   const uint32_t nres = ld_u32_le(d + len - 8);
   const int64_t entries_end = (int64_t)len - 8 - 4 * (int64_t)nres;
-  if (nres < 1 || entries_end < 0) return 0;
+  if (nres < 1 || entries_end < 0) return;
   if (nres <= 32) {
     uint32_t total = 0;
-    bool ok = true;
     uint32_t st = ld_u32_le(d + entries_end);
-    ok = st == 0;
+    bool ok = st == 0;
     for (uint32_t k = 0; ok && k < nres; ++k) {
       const uint32_t en = (k + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (k + 1)) : (uint32_t)entries_end;
       ok = st < en && (int64_t)en <= entries_end;
       if (!ok) break;
-      const int32_t c = interval_walk(d, st, en, K, [](int32_t, uint32_t, uint32_t, uint32_t) {});
+      const uint32_t base = total;
+      const int32_t c = interval_walk(d, st, en, K, [&](int32_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+        if (base + j < (uint32_t)kSlotCap) out[base + j] = DecSlot{pos, (vl << 8) | s};
+      });
       ok = c >= 0;
       total += (uint32_t)c;
       st = en;
     }
-    if (ok) return total;
+    if (ok) {
+      cnt = total;
+      flags = total <= (uint32_t)kSlotCap ? kScanSlots : 0u;
+      return;
+    }
   }
   uint64_t nn = 0;
-  uint32_t us;
-  block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us, [](uint64_t, uint32_t, uint32_t, uint32_t) {});
-  return (uint32_t)nn;
+  uint32_t us = 0;
+  const uint32_t pc = block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us,
+                                       [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
+                                         if (j < (uint64_t)kSlotCap) out[j] = DecSlot{pos, (vl << 8) | s};
+                                       });
+  cnt = (uint32_t)nn;
+  flags = (pc == 0 && us == 0 && nn <= (uint64_t)kSlotCap) ? kScanSlots : 0u;
 }
 
-__global__ void __launch_bounds__(256) block_count_kernel(const uint8_t* arena, BlockTable bt, uint32_t nblk,
-                                                          uint32_t K, uint32_t* count) {
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
-    count[b] = block_count(arena + bt.addr[b], bt.len[b], K);
+__global__ void __launch_bounds__(256) block_scan_kernel(const uint8_t* arena, BlockTable bt, uint32_t nblk,
+                                                         uint32_t K, uint32_t* count, uint32_t* flags,
+                                                         DecSlot* slots) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x) {
+    uint32_t c, f;
+    block_scan(arena + bt.addr[b], bt.len[b], K, slots + (uint64_t)b * kSlotCap, c, f);
+    count[b] = c;
+    flags[b] = f;
+  }
 }
 
 template <int W>
