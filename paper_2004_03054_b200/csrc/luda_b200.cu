@@ -238,9 +238,14 @@ struct RunSeg {
   uint64_t start, len;
 };
 
+// Merge sorted runs (logical record ranges) down to one, fusing version
+// resolution into the last pass. Pass 1 reads the decoder's segmented array
+// `X` through `seg`; later passes ping-pong between dense buffers (X is
+// reused densely: its physical capacity >= the record count).
 template <int W>
-int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, Rec<W>* Y, Rec<W>* S, std::vector<RunSeg> runs,
-               const ResolveArgs& ra_final, unsigned long long* d_err_order, unsigned long long* d_nout) {
+int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& seg, Rec<W>* Y, Rec<W>* S,
+               std::vector<RunSeg> runs, const ResolveArgs& ra_final, unsigned long long* d_err_order,
+               unsigned long long* d_nout) {
   // drop empty runs
   std::vector<RunSeg> segs;
   for (auto& r : runs)
@@ -252,7 +257,15 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, Rec<W>* Y, Rec<W>* 
   bool first_pass = true;
   const size_t smem = sizeof(Rec<W>) * kMergeTile + 4 * kMergeTile;
   CK(cudaFuncSetAttribute(merge_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  auto launch = [&](const Rec<W>* A, uint64_t na, const Rec<W>* B, uint64_t nb, Rec<W>* out, uint64_t abase,
+  Rec<W>* cur = X;
+  Rec<W>* nxt = Y;
+  auto view = [&](const RunSeg& r) {
+    RunView<W> v = seg;
+    if (!first_pass) v = RunView<W>{cur, nullptr, 0, 1, 0};
+    v.off = r.start;
+    return v;
+  };
+  auto launch = [&](const RunView<W>& A, uint64_t na, const RunView<W>& B, uint64_t nb, Rec<W>* out, uint64_t abase,
                     uint64_t bbase, bool resolve) -> int {
     const uint64_t ntiles = (na + nb + kMergeTile - 1) / kMergeTile;
     GET(split, uint64_t, ntiles + 1, false);
@@ -283,20 +296,18 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, Rec<W>* Y, Rec<W>* 
     CK(cudaGetLastError());
     return LUDA_OK;
   };
-  Rec<W>* cur = X;
-  Rec<W>* nxt = Y;
   while (segs.size() > 2) {
     std::vector<RunSeg> next;
     for (size_t i = 0; i < segs.size(); i += 2) {
       if (i + 1 < segs.size()) {
         const RunSeg a = segs[i], b = segs[i + 1];
-        int rc = launch(cur + a.start, a.len, cur + b.start, b.len, nxt + a.start, a.start, b.start, false);
+        int rc = launch(view(a), a.len, view(b), b.len, nxt + a.start, a.start, b.start, false);
         if (rc) return rc;
         next.push_back({a.start, a.len + b.len});
       } else {
         const RunSeg a = segs[i];
-        if (first_pass) {  // still order-check the odd run
-          int rc = launch(cur + a.start, a.len, cur + a.start, 0, nxt + a.start, a.start, a.start, false);
+        if (first_pass) {  // still order-check the odd run (and densify it)
+          int rc = launch(view(a), a.len, view(a), 0, nxt + a.start, a.start, a.start, false);
           if (rc) return rc;
         } else {
           CK(cudaMemcpyAsync(nxt + a.start, cur + a.start, a.len * sizeof(Rec<W>), cudaMemcpyDeviceToDevice, st));
@@ -308,9 +319,9 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, Rec<W>* Y, Rec<W>* 
     std::swap(cur, nxt);
     first_pass = false;
   }
-  if (segs.size() == 2) return launch(cur + segs[0].start, segs[0].len, cur + segs[1].start, segs[1].len, S,
-                                      segs[0].start, segs[1].start, true);
-  return launch(cur + segs[0].start, segs[0].len, cur + segs[0].start, 0, S, segs[0].start, segs[0].start, true);
+  if (segs.size() == 2) return launch(view(segs[0]), segs[0].len, view(segs[1]), segs[1].len, S, segs[0].start,
+                                      segs[1].start, true);
+  return launch(view(segs[0]), segs[0].len, view(segs[0]), 0, S, segs[0].start, segs[0].start, true);
 }
 
 struct ChainBufs {
@@ -521,48 +532,43 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   res->blocks_in = nblk;
   // ---- decode ----
   (void)bound;
-  GET(d_base, uint64_t, nblk + 1, false);
   GET(errs, unsigned long long, 2, false);
   const size_t dsm = sizeof(CrcSmem) + (size_t)kDecWarps * kDecWarpBytes;
   CK(cudaFuncSetAttribute(decode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   Rec<W>* X = nullptr;
   uint64_t n_in = 0;
   std::vector<uint64_t> fbase(jd->n_files + 1);
-  // count pre-pass + exclusive scan → first record index of every block
-  GET(d_cnt, uint32_t, nblk, false);
-  GET(d_flags, uint32_t, nblk, false);
-  GET(d_gslots, DecSlot, (uint64_t)nblk * kSlotCap, false);
-  block_scan_kernel<<<std::min<uint32_t>((nblk + 255) / 256, 16 * g_num_sms), 256, 0, st>>>(jd->arena, bt, nblk, K,
-                                                                                          d_cnt, d_flags, d_gslots);
-  ++g_launches;
-  {
-    const uint64_t nt = std::max<uint64_t>(1, (nblk + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
-    GET(lb, uint64_t, nt, true);
-    GET(ctr, unsigned int, 1, true);
-    scan_excl_kernel<uint32_t><<<(unsigned)nt, kScanThreads, 0, st>>>(d_cnt, nblk, d_base, lb, ctr);
-    ++g_launches;
-  }
-  GET(d_fbase, uint64_t, jd->n_files + 1, false);
-  file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_base, d_file_blk_base, jd->n_files, d_fbase);
-  ++g_launches;
-  CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
-  {
-    int rc = sync(st);
-    if (rc) return rc;
-  }
-  n_in = fbase[jd->n_files];
-  X = scratch.get<Rec<W>>(std::max<uint64_t>(n_in, 1), false);
-  if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
-  {
+  // Single-pass decode into warp segments (luda_decode.cuh). Segment
+  // capacity comes from the records-per-input-byte ratio of earlier jobs
+  // (first job: 1 record per 48 bytes); a job whose largest segment does not
+  // fit is decoded again with the exact capacity.
+  const uint32_t nw = (uint32_t)g_num_sms * kDecWarps;
+  uint64_t blk_bytes = 0;
+  for (uint32_t f = 0; f < jd->n_files; ++f) blk_bytes += jd->file_len[f];
+  static double s_ratio = 1.0 / 48.0;
+  uint64_t seg_cap = (uint64_t)((double)blk_bytes / nw * s_ratio * 1.25) + 4ull * (nblk / nw + 1) + 64;
+  GET(d_local, uint32_t, nblk, false);
+  GET(d_count, uint64_t, nw, false);
+  GET(d_lo, uint64_t, nw + 1, false);
+  GET(d_max, uint64_t, 1, false);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    X = scratch.get<Rec<W>>((uint64_t)nw * seg_cap, false);
+    if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
     CK(cudaMemsetAsync(errs, 0xFF, 16, st));
-    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, n_in, d_base, d_flags, d_gslots, errs, errs + 1};
+    CK(cudaMemsetAsync(d_max, 0, 8, st));
+    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, errs, errs + 1};
     KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
     ++g_launches;
     KT_STOP(0, st);
     CK(cudaGetLastError());
+    seg_scan_kernel<<<1, 1024, 0, st>>>(d_count, nw, d_lo, d_max);
+    ++g_launches;
     unsigned long long herr[2];
+    uint64_t hm[2];
     CK(cudaMemcpyAsync(herr, errs, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hm[0], d_lo + nw, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hm[1], d_max, 8, cudaMemcpyDeviceToHost, st));
     int rc = sync(st);
     if (rc) return rc;
     if (herr[0] != ~0ull || herr[1] != ~0ull) {
@@ -575,7 +581,22 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
       if (code == B_CRC) return fail(LUDA_CORRUPT, block_msg(code), foff);
       return fail(LUDA_FORMAT, block_msg(code));
     }
+    n_in = hm[0];
+    if (blk_bytes) s_ratio = std::max(s_ratio * 0.5, (double)n_in / (double)blk_bytes);
+    if (hm[1] <= seg_cap) break;
+    if (attempt == 1) return fail(LUDA_DEVICE, "decode record capacity overflow");
+    seg_cap = hm[1];
   }
+  GET(d_fbase, uint64_t, jd->n_files + 1, false);
+  file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_local, d_lo, nblk, nw, d_file_blk_base,
+                                                                          jd->n_files, d_fbase);
+  ++g_launches;
+  CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
+  {
+    int rc = sync(st);
+    if (rc) return rc;
+  }
+  const RunView<W> segview{X, d_lo, seg_cap, nw, 0};
   res->n_in = n_in;
   if (ev) CK(cudaEventRecord(ev[2], st));
   // ---- merge + resolve ----
@@ -615,7 +636,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     }
     CK(cudaMemsetAsync(merr, 0xFF, 8, st));
     CK(cudaMemsetAsync(merr + 1, 0, 8, st));
-    int rc = merge_runs<W>(st, scratch, X, Y, S, runs, ra, merr, merr + 1);
+    int rc = merge_runs<W>(st, scratch, X, segview, Y, S, runs, ra, merr, merr + 1);
     if (rc) return rc;
     unsigned long long hm[2];
     CK(cudaMemcpyAsync(hm, merr, 16, cudaMemcpyDeviceToHost, st));

@@ -4,12 +4,16 @@
 // of checksum.py:12-13) is computed warp-parallel: a byte range is cut into
 // END-ALIGNED 68-byte segments (17 words). In one pass a warp covers 64
 // segments (4352 B): lane d owns the segments at distance d and d+32 from the
-// pass end and runs their two byte-table chains interleaved (2-way ILP; the
-// table is replicated per bank so lanes never conflict). Segment registers are
-// combined with the GF(2) "advance over n zero bytes" operator Z_n (the
-// crc32_combine algebra: raw(A∥B) = Z_|B|(raw(A)) ^ raw(B)):
+// pass end and runs their two table chains interleaved (2-way ILP). Segment
+// registers are combined with the GF(2) "advance over n zero bytes" operator
+// Z_n (the crc32_combine algebra: raw(A∥B) = Z_|B|(raw(A)) ^ raw(B)):
 //   lane value = Z_{68d}( raw(seg d) ^ Z_2176(raw(seg d+32)) ), XOR over lanes.
-// 17 words (odd) per segment makes the 32 lanes' LDS.32 streams hit 32
+// Words go through SLICING-BY-2 tables (two 16-bit steps per word). The two
+// byte tables T1 (byte then a zero byte) and T0 are replicated once per lane
+// and interleaved so that one PRMT forms the whole shared-memory offset:
+//   offset = idx << 8 | table << 7 | lane << 2      (64 KB, bank = lane)
+// i.e. per 2 bytes: 2 PRMT + 2 LDS + SHF + LOP3, no bank conflicts.
+// 17 words (odd) per segment makes the 32 lanes' LDS.32 data streams hit 32
 // distinct banks. The ~0 preset is folded into the data: callers run
 // crc_prep() on the smem copy (zero the 72 bytes before it, complement the
 // first 4 bytes: F(~0, D) = F(0, D') and leading zeros leave a zero register
@@ -28,48 +32,70 @@ constexpr int kGroup = 64 * kSeg;    // 4352: bytes one warp covers per pass
 constexpr int kCrcLead = 72;         // zeroed bytes required before the data
 
 // ---- tables (device globals; initialised by luda_init) ---------------------
-// g_crc_tab[b]          : byte table T[b]
+// g_crc_tab[b]          : byte table T0[b]
+// g_crc_tab1[b]         : T1[b] = T0 advanced over one more (zero) byte
 // g_seg_nib[n][v][d]    : Z_{68*d}(v << 4n)    (8 x 16 x 32 words)
 // g_half_tab[k][b]      : Z_2176(b << 8k)     (4 x 256 words)
 // c_zpow[i][j]          : Z_{2^i}(1 << j)      (48 x 32 words) for arbitrary shifts
 // c_zgroup[j]           : Z_4352(1 << j)       (one warp pass)
 // (single translation unit: luda_b200.cu includes every stage header)
 __device__ uint32_t g_crc_tab[256];
+__device__ uint32_t g_crc_tab1[256];
 __device__ uint32_t g_seg_nib[8 * 16 * 32];
 __device__ uint32_t g_half_tab[4 * 256];
 __constant__ uint32_t c_zpow[48][32];
 __constant__ uint32_t c_zgroup[32];
 
-// Shared-memory CRC state: 32 bank-replicated copies of T (32 KB), the
-// per-lane nibble tables (16 KB) and the Z_2176 byte tables (4 KB).
-// Lane l reads tab[(idx<<5)|l] → bank l.
+// Shared-memory CRC state: the lane-replicated slicing-by-2 tables (64 KB),
+// the per-lane nibble tables (16 KB) and the Z_2176 byte tables (4 KB).
 struct CrcSmem {
-  uint32_t tab[256 * 32];
+  uint32_t s2[256 * 64];  // row idx: [T1 lane 0..31][T0 lane 0..31]
   uint32_t nib[8 * 16 * 32];
   uint32_t half[4 * 256];
 };
 
 __device__ __forceinline__ void crc_smem_init(CrcSmem& s) {
-  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) s.tab[i] = g_crc_tab[i >> 5];
+  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x)
+    s.s2[i] = (i & 32) ? g_crc_tab[i >> 6] : g_crc_tab1[i >> 6];
   for (int i = threadIdx.x; i < 8 * 16 * 32; i += blockDim.x) s.nib[i] = g_seg_nib[i];
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) s.half[i] = g_half_tab[i];
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
-// One word through the byte-table register update (4 dependent lookups).
-// `tl` = s.tab + lane.
-__device__ __forceinline__ uint32_t crc_word(uint32_t c, uint32_t w, const uint32_t* __restrict__ tl) {
-  c ^= w;
-  c = tl[(c & 0xFFu) << 5] ^ (c >> 8);
-  c = tl[(c & 0xFFu) << 5] ^ (c >> 8);
-  c = tl[(c & 0xFFu) << 5] ^ (c >> 8);
-  c = tl[(c & 0xFFu) << 5] ^ (c >> 8);
-  return c;
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
 }
 
-__device__ __forceinline__ uint32_t crc_byte(uint32_t c, uint32_t b, const uint32_t* __restrict__ tl) {
-  return tl[((c ^ b) & 0xFFu) << 5] ^ (c >> 8);
+// A lane's view of the slicing tables: base + the two PRMT partner words
+// (byte 0 = lane << 2 | table << 7, bytes 1-3 zero).
+struct CrcLane {
+  const uint8_t* base;
+  uint32_t a1, a0;
+};
+__device__ __forceinline__ CrcLane crc_lane(const CrcSmem& s, uint32_t lane) {
+  return CrcLane{reinterpret_cast<const uint8_t*>(s.s2), lane << 2, (lane << 2) | 0x80u};
+}
+__device__ __forceinline__ uint32_t crc_lut(const CrcLane& t, uint32_t off) {
+  return *reinterpret_cast<const uint32_t*>(t.base + off);
+}
+
+// One 16-bit step: x already holds crc ^ data in its low half.
+__device__ __forceinline__ uint32_t crc_half(uint32_t x, const CrcLane& t) {
+  const uint32_t a = crc_lut(t, prmt(x, t.a1, 0x7604u));  // T1[x & 0xFF]
+  const uint32_t b = crc_lut(t, prmt(x, t.a0, 0x7614u));  // T0[(x >> 8) & 0xFF]
+  return (x >> 16) ^ a ^ b;
+}
+
+// One word through the register update (two slicing-by-2 steps).
+__device__ __forceinline__ uint32_t crc_word(uint32_t c, uint32_t w, const CrcLane& t) {
+  return crc_half(crc_half(c ^ w, t), t);
+}
+
+__device__ __forceinline__ uint32_t crc_byte(uint32_t c, uint32_t b, const CrcLane& t) {
+  return crc_lut(t, prmt(c ^ b, t.a0, 0x7604u)) ^ (c >> 8);  // T0[(c ^ b) & 0xFF] ^ (c >> 8)
 }
 
 // Z_{68*lane}(c) via the lane's nibble tables. `nl` = s.nib + lane.
@@ -133,7 +159,7 @@ __device__ __forceinline__ SegPtr seg_ptr(const uint8_t* p) {
 __device__ __forceinline__ uint32_t pass_lane_value(const uint8_t* data, uint64_t n, uint32_t q, const CrcSmem& cs,
                                                     const uint8_t* safe) {
   const uint32_t lane = lane_id();
-  const uint32_t* tl = cs.tab + lane;
+  const CrcLane tl = crc_lane(cs, lane);
   const int64_t nseg = ((int64_t)n + kSeg - 1) / kSeg;
   const int64_t dlo = (int64_t)lane + 64 * (int64_t)q;
   const int64_t dhi = dlo + 32;
@@ -182,8 +208,8 @@ __device__ __forceinline__ uint32_t warp_crc32_smem(uint8_t* data, uint32_t n, c
   return c;
 }
 
-// Scalar CRC (any n) for tiny ranges; `tl` = table row of the calling lane.
-__device__ __forceinline__ uint32_t crc32_bytes(const uint8_t* p, uint32_t n, const uint32_t* tl) {
+// Scalar CRC (any n) for tiny ranges; `tl` = table view of the calling lane.
+__device__ __forceinline__ uint32_t crc32_bytes(const uint8_t* p, uint32_t n, const CrcLane& tl) {
   uint32_t c = 0xFFFFFFFFu;
   for (uint32_t i = 0; i < n; ++i) c = crc_byte(c, p[i], tl);
   return ~c;

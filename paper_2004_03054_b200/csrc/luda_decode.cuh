@@ -17,8 +17,12 @@
 //    passes through the same entry boundaries and yields identical keys.
 //    Otherwise lane 0 runs the exact sequential reference parse (errors
 //    included);
-//  * decoupled look-back over block order gives the block's first record
-//    index (single pass, no count kernel);
+//  * every warp owns a CONTIGUOUS range of blocks and writes their records
+//    back to back into its own segment of the record array (segment w at
+//    w * seg_cap); a block's record base is the warp's running count, so
+//    there is no inter-warp dependency at all (no count pre-pass, no
+//    look-back). The merge reads the segmented array through a logical →
+//    physical index view (luda_merge.cuh, SegRun);
 //  * warp CRC-32 of the payload (end-aligned segments, luda_common.cuh);
 //  * phase 2 — lanes take consecutive entries; each loads its key suffix and
 //    the prefix bytes it shares are filled from earlier lanes by a
@@ -46,7 +50,7 @@ enum BlockCode : uint32_t {
   B_VALUE_BIG = 9,      // (unsupported) value length >= 2^24 or arena offset >= 2^40
 };
 
-constexpr int kDecWarps = 16;
+constexpr int kDecWarps = 14;
 constexpr int kDecStage = 4352;                  // staged window bytes (block + alignment)
 constexpr int kDecPre = 160;                     // CRC lead-in before the data
 constexpr int kDecBuf = kDecPre + kDecStage + 64;
@@ -60,23 +64,30 @@ struct DecSlot {
   uint32_t sv;   // value_len << 8 | shared
 };
 
-constexpr int kSlotCap = 48;         // scan-pass slots per block
-constexpr uint32_t kScanSlots = 1u;  // block flag: slots valid (no error, cnt <= kSlotCap)
-
 template <int W>
 struct DecodeArgs {
   const uint8_t* arena;
   BlockTable bt;
   uint32_t nblk;
   uint32_t K;               // internal key length of the job
-  Rec<W>* out;
-  uint64_t cap;
-  const uint64_t* blk_base; // [nblk+1] first record index of each block (count pre-pass + scan)
-  const uint32_t* blk_flags;  // block_scan flags
-  const DecSlot* gslots;      // block_scan slots, kSlotCap per block
+  Rec<W>* out;              // segmented: warp w writes out[w * seg_cap ...]
+  uint64_t seg_cap;         // records per warp segment
+  uint32_t* blk_local;      // out [nblk]: block's first record index within its warp segment
+  uint64_t* seg_count;      // out [nwarps]: records of each warp segment (may exceed seg_cap → rerun)
   unsigned long long* err_ref;
   unsigned long long* err_unsup;
 };
+
+// Block range of warp segment w of nw: [w*nblk/nw, (w+1)*nblk/nw).
+__host__ __device__ __forceinline__ uint32_t seg_first_block(uint32_t w, uint32_t nblk, uint32_t nw) {
+  return (uint32_t)(((uint64_t)w * nblk) / nw);
+}
+__device__ __forceinline__ uint32_t seg_of_block(uint32_t b, uint32_t nblk, uint32_t nw) {
+  uint32_t w = (uint32_t)(((uint64_t)b * nw) / nblk);
+  while (w + 1 < nw && seg_first_block(w + 1, nblk, nw) <= b) ++w;
+  while (w > 0 && seg_first_block(w, nblk, nw) > b) --w;
+  return w;
+}
 
 // Walk one restart interval [start, end) under fast-path rules and call
 // emit(j, pos_suffix, shared, vlen) per entry; returns the entry count or -1
@@ -256,7 +267,8 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
 // CRC staged pass by pass through `stage`.
 template <int W, bool kStaged>
 __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, DecState& st, uint64_t base,
-                                           const uint8_t* d, DecSlot* slots, uint8_t* stage, const CrcSmem& cs) {
+                                           uint64_t cap, const uint8_t* d, DecSlot* slots, uint8_t* stage,
+                                           const CrcSmem& cs) {
   constexpr int NW = 2 * W + 2;
   const uint32_t lane = lane_id();
   const uint32_t K = a.K;
@@ -277,7 +289,7 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
     else code = st.pcode;
   }
   const uint64_t n = st.n;
-  if (code || st.unsup || base + n > a.cap) {
+  if (code || st.unsup || base + n > cap) {
     if (lane == 0 && code) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
     if (lane == 0 && !code && st.unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | st.unsup);
     return;
@@ -288,10 +300,10 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   uint32_t carry[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) carry[i] = 0;
-  const uint64_t wstep = (mode == 1 || mode == 4) ? n : (uint64_t)kDecSlots;
+  const uint64_t wstep = mode == 1 ? n : (uint64_t)kDecSlots;
   for (uint64_t w0 = 0; w0 < n; w0 += wstep) {
     const uint64_t w1 = w0 + kDecSlots;
-    if (mode != 1 && mode != 4) {
+    if (mode != 1) {
       auto put = [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
         if (j >= w0 && j < w1) slots[j - w0] = DecSlot{pos, (vl << 8) | s};
       };
@@ -380,9 +392,11 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   }
 }
 
+// `base` = physical record index of the block's first record, `cap` = end of
+// the warp's segment; returns the block's entry count.
 template <int W, bool kStaged>
-__device__ __forceinline__ void dec_block(const DecodeArgs<W>& a, uint32_t b, uint8_t* wb, int which,
-                                          uint32_t& phase, const CrcSmem& cs) {
+__device__ __forceinline__ uint64_t dec_block(const DecodeArgs<W>& a, uint32_t b, uint8_t* wb, int which,
+                                              uint32_t& phase, const CrcSmem& cs, uint64_t base, uint64_t cap) {
   uint8_t* buf = dec_buf(wb, which);
   const uint8_t* g = a.arena + a.bt.addr[b];
   const uint8_t* d;
@@ -394,81 +408,9 @@ __device__ __forceinline__ void dec_block(const DecodeArgs<W>& a, uint32_t b, ui
     d = g;
   }
   DecSlot* slots = dec_slots(wb);
-  const uint64_t base = a.blk_base[b];
-  DecState st;
-  if (a.blk_flags[b] & kScanSlots) {
-    // entries were located by the scan pass: no walk here
-    st = DecState{};
-    st.len = a.bt.len[b];
-    st.addr = a.bt.addr[b];
-    st.n = a.blk_base[b + 1] - base;
-    st.mode = 4;
-    const DecSlot* gs = a.gslots + (uint64_t)b * kSlotCap;
-    for (uint32_t e = lane_id(); e < st.n; e += 32) slots[e] = gs[e];
-    __syncwarp();
-  } else {
-    st = dec_phase1(a, b, d, slots);
-  }
-  dec_phase2<W, kStaged>(a, b, st, base, d, slots, buf, cs);
-}
-
-// ---- block scan pre-pass ---------------------------------------------------------
-// One thread per block walks the entry headers straight from global memory
-// with exactly the decision procedure of phase 1 (canonical restart-interval
-// walk, else the exact sequential walk) and records the entry count, and —
-// when the block is error-free and has <= kSlotCap entries — every entry's
-// slot (key-suffix position, shared, value length). The decode kernel then
-// skips its own walk for those blocks; counts feed the scan that places
-// every block's records (no inter-block dependency inside decode).
-__device__ __forceinline__ void block_scan(const uint8_t* d, uint32_t len, uint32_t K, DecSlot* out, uint32_t& cnt,
-                                           uint32_t& flags) {
-  cnt = 0;
-  flags = 0;
-  if (len < 12) return;
-  const uint32_t nres = ld_u32_le(d + len - 8);
-  const int64_t entries_end = (int64_t)len - 8 - 4 * (int64_t)nres;
-  if (nres < 1 || entries_end < 0) return;
-  if (nres <= 32) {
-    uint32_t total = 0;
-    uint32_t st = ld_u32_le(d + entries_end);
-    bool ok = st == 0;
-    for (uint32_t k = 0; ok && k < nres; ++k) {
-      const uint32_t en = (k + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (k + 1)) : (uint32_t)entries_end;
-      ok = st < en && (int64_t)en <= entries_end;
-      if (!ok) break;
-      const uint32_t base = total;
-      const int32_t c = interval_walk(d, st, en, K, [&](int32_t j, uint32_t pos, uint32_t s, uint32_t vl) {
-        if (base + j < (uint32_t)kSlotCap) out[base + j] = DecSlot{pos, (vl << 8) | s};
-      });
-      ok = c >= 0;
-      total += (uint32_t)c;
-      st = en;
-    }
-    if (ok) {
-      cnt = total;
-      flags = total <= (uint32_t)kSlotCap ? kScanSlots : 0u;
-      return;
-    }
-  }
-  uint64_t nn = 0;
-  uint32_t us = 0;
-  const uint32_t pc = block_walk_exact(d, len - 4, (uint64_t)entries_end, K, nn, us,
-                                       [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
-                                         if (j < (uint64_t)kSlotCap) out[j] = DecSlot{pos, (vl << 8) | s};
-                                       });
-  cnt = (uint32_t)nn;
-  flags = (pc == 0 && us == 0 && nn <= (uint64_t)kSlotCap) ? kScanSlots : 0u;
-}
-
-__global__ void __launch_bounds__(256) block_scan_kernel(const uint8_t* arena, BlockTable bt, uint32_t nblk,
-                                                         uint32_t K, uint32_t* count, uint32_t* flags,
-                                                         DecSlot* slots) {
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x) {
-    uint32_t c, f;
-    block_scan(arena + bt.addr[b], bt.len[b], K, slots + (uint64_t)b * kSlotCap, c, f);
-    count[b] = c;
-    flags[b] = f;
-  }
+  DecState st = dec_phase1(a, b, d, slots);
+  dec_phase2<W, kStaged>(a, b, st, base, cap, d, slots, buf, cs);
+  return st.n;
 }
 
 template <int W>
@@ -483,32 +425,69 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
     mbar_init(dec_bar(wb, 1), 1);
   }
   __syncthreads();
-  // Record bases come from the count pre-pass (blk_base), so blocks are
-  // independent: static round-robin assignment, the next block's TMA staging
-  // in flight while the current one is processed.
+  // Warp segment: a contiguous block range, the next block's TMA staging in
+  // flight while the current one is processed.
   const uint32_t nw = gridDim.x * kDecWarps;
-  uint32_t cur = blockIdx.x * kDecWarps + (threadIdx.x >> 5);
+  const uint32_t w = blockIdx.x * kDecWarps + (threadIdx.x >> 5);
+  const uint32_t b0 = seg_first_block(w, a.nblk, nw), b1 = seg_first_block(w + 1, a.nblk, nw);
+  const uint64_t seg0 = (uint64_t)w * a.seg_cap, seg1 = seg0 + a.seg_cap;
+  uint64_t cnt = 0;
   uint32_t phase = 0;
   int which = 0;
-  bool cur_staged = dec_prefetch(a, cur, wb, which);
-  while (cur < a.nblk) {
-    const uint32_t nxt = cur + nw;
-    const bool nxt_staged = dec_prefetch(a, nxt, wb, which ^ 1);
-    if (cur_staged) dec_block<W, true>(a, cur, wb, which, phase, cs);
-    else dec_block<W, false>(a, cur, wb, which, phase, cs);
+  bool cur_staged = b0 < b1 && dec_prefetch(a, b0, wb, which);
+  for (uint32_t cur = b0; cur < b1; ++cur) {
+    const bool nxt_staged = cur + 1 < b1 && dec_prefetch(a, cur + 1, wb, which ^ 1);
+    if (lane == 0) a.blk_local[cur] = (uint32_t)cnt;
+    cnt += cur_staged ? dec_block<W, true>(a, cur, wb, which, phase, cs, seg0 + cnt, seg1)
+                      : dec_block<W, false>(a, cur, wb, which, phase, cs, seg0 + cnt, seg1);
     fence_proxy_async_smem();  // generic smem accesses before the next TMA into this buffer
     __syncwarp();
-    cur = nxt;
     cur_staged = nxt_staged;
     which ^= 1;
   }
+  if (lane == 0) a.seg_count[w] = cnt;
 }
 
-// First record index of every file (gathered from the block bases).
-__global__ void file_entry_base_kernel(const uint64_t* blk_base, const uint32_t* file_blk_base, uint32_t nfiles,
-                                       uint64_t* out) {
+// Segment starts (logical record index): exclusive scan of the segment
+// counts (one CTA; nw <= a few thousand).
+__global__ void seg_scan_kernel(const uint64_t* count, uint32_t nw, uint64_t* lo, uint64_t* max_count) {
+  __shared__ uint64_t s_carry;
+  __shared__ uint64_t s_warp[32];
+  if (threadIdx.x == 0) s_carry = 0;
+  uint64_t mx = 0;
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < nw; c0 += blockDim.x) {
+    const uint32_t i = c0 + threadIdx.x;
+    const uint64_t v = i < nw ? count[i] : 0;
+    mx = v > mx ? v : mx;
+    const uint64_t incl = warp_incl_scan<uint64_t>(v);
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const uint64_t x = lane < blockDim.x / 32 ? s_warp[lane] : 0;
+      const uint64_t xi = warp_incl_scan<uint64_t>(x);
+      if (lane < blockDim.x / 32) s_warp[lane] = xi - x;
+    }
+    __syncthreads();
+    if (i < nw) lo[i] = s_carry + s_warp[wid] + incl - v;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry += s_warp[wid] + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lo[nw] = s_carry;
+  mx = warp_max<uint64_t>(mx);
+  if (lane_id() == 0) atomicMax(reinterpret_cast<unsigned long long*>(max_count), (unsigned long long)mx);
+}
+
+// First record index (logical) of every file: its first block's segment
+// start + the block's local base; file nfiles = total.
+__global__ void file_entry_base_kernel(const uint32_t* blk_local, const uint64_t* seg_lo, uint32_t nblk, uint32_t nw,
+                                       const uint32_t* file_blk_base, uint32_t nfiles, uint64_t* out) {
   const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f <= nfiles) out[f] = blk_base[file_blk_base[f]];
+  if (f > nfiles) return;
+  const uint32_t b = file_blk_base[f];
+  out[f] = b >= nblk ? seg_lo[nw] : seg_lo[seg_of_block(b, nblk, nw)] + blk_local[b];
 }
 
 }  // namespace luda

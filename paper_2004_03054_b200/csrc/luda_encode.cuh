@@ -25,7 +25,7 @@
 
 namespace luda {
 
-constexpr int kEncWarps = 16;
+constexpr int kEncWarps = 13;
 constexpr int kEncStage = 4608;                        // blocks up to this size are assembled in smem
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
@@ -94,7 +94,7 @@ __device__ __forceinline__ void put_key_tail(uint8_t* p, const Rec<W>& r, uint32
 __device__ __forceinline__ uint32_t cta_crc32_smem(uint8_t* data, uint32_t n, const CrcSmem& cs, uint32_t* red) {
   const uint32_t nwarps = blockDim.x >> 5, wid = threadIdx.x >> 5;
   if (n < 4) {
-    if (threadIdx.x == 0) red[0] = crc32_bytes(data, n, cs.tab);
+    if (threadIdx.x == 0) red[0] = crc32_bytes(data, n, crc_lane(cs, lane_id()));
     __syncthreads();
     const uint32_t v = red[0];
     __syncthreads();
@@ -120,7 +120,7 @@ __device__ __forceinline__ uint32_t cta_crc32_global(const uint8_t* g, uint64_t 
                                                      uint32_t* red) {
   const uint32_t nwarps = blockDim.x >> 5, wid = threadIdx.x >> 5;
   if (n < 4) {
-    if (threadIdx.x == 0) red[0] = crc32_bytes(g, (uint32_t)n, cs.tab);
+    if (threadIdx.x == 0) red[0] = crc32_bytes(g, (uint32_t)n, crc_lane(cs, lane_id()));
     __syncthreads();
     const uint32_t v = red[0];
     __syncthreads();
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
     for (uint32_t i = tid; i < (nbytes + 1 + 3) / 4; i += kMetaThreads) bits[i] = 0;
   __syncthreads();
   // ---- bloom bits ----
-  const uint32_t* tl = cs.tab + lane;
+  const CrcLane tl = crc_lane(cs, lane);
   for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
     const Rec<W> r = a.rec[e];
     uint32_t c = 0xFFFFFFFFu;

@@ -67,9 +67,60 @@ __device__ __forceinline__ bool covered_below(const Rec<W>& r, const ResolveArgs
   return false;
 }
 
+// A sorted run as seen by the merge: dense (`lo` == nullptr: element i at
+// base[off + i]) or SEGMENTED — the decoder's layout (luda_decode.cuh), where
+// logical record g lives in the segment s with lo[s] <= g < lo[s+1], at
+// physical index s * cap + (g - lo[s]).
+template <int W>
+struct RunView {
+  const Rec<W>* base;
+  const uint64_t* lo;  // [nseg+1] logical segment starts, or nullptr (dense)
+  uint64_t cap;
+  uint32_t nseg;
+  uint64_t off;        // logical index of the run's element 0
+  __device__ __forceinline__ uint32_t seg(uint64_t g) const {
+    uint32_t l = 0, h = nseg;
+    while (h - l > 1) {
+      const uint32_t mid = (l + h) >> 1;
+      if (lo[mid] <= g) l = mid;
+      else h = mid;
+    }
+    return l;
+  }
+  __device__ __forceinline__ uint64_t phys(uint64_t i) const {
+    if (!lo) return off + i;
+    const uint64_t g = off + i;
+    const uint32_t s = seg(g);
+    return (uint64_t)s * cap + (g - lo[s]);
+  }
+  __device__ __forceinline__ const Rec<W>& operator[](uint64_t i) const { return base[phys(i)]; }
+  // f(physical pointer, count, destination offset) over the contiguous pieces of [i0, i1)
+  template <typename F>
+  __device__ __forceinline__ void pieces(uint64_t i0, uint64_t i1, F f) const {
+    if (i0 >= i1) return;
+    if (!lo) {
+      f(base + off + i0, i1 - i0, 0ull);
+      return;
+    }
+    uint64_t g = off + i0;
+    const uint64_t g1 = off + i1;
+    uint32_t s = seg(g);
+    uint64_t done = 0;
+    while (g < g1) {
+      const uint64_t e = lo[s + 1] < g1 ? lo[s + 1] : g1;
+      if (e > g) {
+        f(base + (uint64_t)s * cap + (g - lo[s]), e - g, done);
+        done += e - g;
+        g = e;
+      }
+      ++s;
+    }
+  }
+};
+
 // Merge-path split: number of A elements among the first `diag` outputs.
 template <int W>
-__device__ __forceinline__ uint64_t merge_split(const Rec<W>* A, uint64_t na, const Rec<W>* B, uint64_t nb,
+__device__ __forceinline__ uint64_t merge_split(const RunView<W>& A, uint64_t na, const RunView<W>& B, uint64_t nb,
                                                 uint64_t diag) {
   uint64_t lo = diag > nb ? diag - nb : 0;
   uint64_t hi = diag < na ? diag : na;
@@ -82,7 +133,7 @@ __device__ __forceinline__ uint64_t merge_split(const Rec<W>* A, uint64_t na, co
 }
 
 template <int W>
-__global__ void merge_partition_kernel(const Rec<W>* A, uint64_t na, const Rec<W>* B, uint64_t nb, uint64_t ntiles,
+__global__ void merge_partition_kernel(RunView<W> A, uint64_t na, RunView<W> B, uint64_t nb, uint64_t ntiles,
                                        uint64_t* split) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t > ntiles) return;
@@ -93,9 +144,9 @@ __global__ void merge_partition_kernel(const Rec<W>* A, uint64_t na, const Rec<W
 
 template <int W>
 struct MergeArgs {
-  const Rec<W>* A;
+  RunView<W> A;
   uint64_t na;
-  const Rec<W>* B;
+  RunView<W> B;
   uint64_t nb;
   const uint64_t* split;  // [ntiles+1]
   uint64_t ntiles;
@@ -143,18 +194,26 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
       mbar_init(&s_bar, 1);
       const uint32_t bytes = nt * (uint32_t)sizeof(Rec<W>);
       mbar_arrive_expect_tx(&s_bar, bytes);
-      if (na_t) bulk_g2s(S, m.A + a0, na_t * (uint32_t)sizeof(Rec<W>), &s_bar);
-      if (nb_t) bulk_g2s(S + na_t, m.B + b0, nb_t * (uint32_t)sizeof(Rec<W>), &s_bar);
+      m.A.pieces(a0, a1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) {
+        bulk_g2s(S + at, src, (uint32_t)cnt * (uint32_t)sizeof(Rec<W>), &s_bar);
+      });
+      m.B.pieces(b0, b1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) {
+        bulk_g2s(S + na_t + at, src, (uint32_t)cnt * (uint32_t)sizeof(Rec<W>), &s_bar);
+      });
     }
     __syncthreads();
     mbar_wait(&s_bar, 0);
   } else {
     constexpr int RW = sizeof(Rec<W>) / 8;
-    const uint64_t* ga = reinterpret_cast<const uint64_t*>(m.A + a0);
-    const uint64_t* gb = reinterpret_cast<const uint64_t*>(m.B + b0);
     uint64_t* sw = reinterpret_cast<uint64_t*>(S);
-    for (uint32_t i = tid; i < na_t * RW; i += kMergeThreads) sw[i] = ga[i];
-    for (uint32_t i = tid; i < nb_t * RW; i += kMergeThreads) sw[na_t * RW + i] = gb[i];
+    auto copy = [&](uint32_t dst0) {
+      return [&, dst0](const Rec<W>* src, uint64_t cnt, uint64_t at) {
+        const uint64_t* gs = reinterpret_cast<const uint64_t*>(src);
+        for (uint32_t i = tid; i < cnt * RW; i += kMergeThreads) sw[(dst0 + at) * RW + i] = gs[i];
+      };
+    };
+    m.A.pieces(a0, a1, copy(0));
+    m.B.pieces(b0, b1, copy(na_t));
     __syncthreads();
   }
   // strict-order check of both slices (including the seam to the previous tile)

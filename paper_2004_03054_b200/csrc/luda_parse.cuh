@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kCrcWarps * 32) crc_ranges_kernel(const uint8_
     const uint64_t n = len[r];
     uint32_t acc = 0;
     if (n < 4) {
-      if (lane == 0) acc = crc32_bytes(g, (uint32_t)n, cs.tab);
+      if (lane == 0) acc = crc32_bytes(g, (uint32_t)n, crc_lane(cs, lane_id()));
     } else {
       const uint64_t npass = (n + kGroup - 1) / kGroup;
       uint32_t raw = 0;

@@ -2,6 +2,7 @@
 //
 // Host code computes, once per process (luda_init):
 //   g_crc_tab   byte table of the reflected polynomial 0xEDB88320
+//   g_crc_tab1  slicing-by-2 partner table (byte, then a zero byte)
 //   g_seg_nib   nibble tables of Z_{68*d}, d = 0..31 (segment combine)
 //   g_half_tab  byte tables of Z_2176 (a lane's second segment)
 //   c_zpow      columns of Z_{2^i}, i = 0..47 (arbitrary shifts)
@@ -73,6 +74,9 @@ int upload_crc_tables() {
     for (int b = 0; b < 256; ++b) half[k * 256 + b] = apply_cols(zh, (uint32_t)b << (8 * k));
   if (cudaMemcpyToSymbol(g_half_tab, half, sizeof(half)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(g_crc_tab, t, sizeof(t)) != cudaSuccess) return 1;
+  uint32_t t1[256];
+  for (int b = 0; b < 256; ++b) t1[b] = t[t[b] & 0xFF] ^ (t[b] >> 8);  // byte b, then a zero byte
+  if (cudaMemcpyToSymbol(g_crc_tab1, t1, sizeof(t1)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(g_seg_nib, nib, sizeof(nib)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(c_zpow, zpow, sizeof(zpow)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(c_zgroup, zg, sizeof(zg)) != cudaSuccess) return 1;
