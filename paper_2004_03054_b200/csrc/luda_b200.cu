@@ -17,6 +17,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -533,7 +534,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   // ---- decode ----
   (void)bound;
   GET(errs, unsigned long long, 2, false);
-  const size_t dsm = sizeof(CrcSmem) + (size_t)kDecWarps * kDecWarpBytes;
+  const size_t dsm = sizeof(CrcSmem) + (size_t)kDecPairs * sizeof(DecPairSmem) + sizeof(DecCtaSmem);
   CK(cudaFuncSetAttribute(decode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
   Rec<W>* X = nullptr;
   uint64_t n_in = 0;
@@ -542,7 +543,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   // capacity comes from the records-per-input-byte ratio of earlier jobs
   // (first job: 1 record per 48 bytes); a job whose largest segment does not
   // fit is decoded again with the exact capacity.
-  const uint32_t nw = (uint32_t)g_num_sms * kDecWarps;
+  const uint32_t nw = (uint32_t)g_num_sms * kDecPairs;  // record segments (one per warp pair)
   uint64_t blk_bytes = 0;
   for (uint32_t f = 0; f < jd->n_files; ++f) blk_bytes += jd->file_len[f];
   static double s_ratio = 1.0 / 48.0;
@@ -556,7 +557,8 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
     CK(cudaMemsetAsync(errs, 0xFF, 16, st));
     CK(cudaMemsetAsync(d_max, 0, 8, st));
-    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, errs, errs + 1};
+    static const uint32_t s_dbg = getenv("LUDA_DEC_DBG") ? (uint32_t)atoi(getenv("LUDA_DEC_DBG")) : 0u;
+    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, errs, errs + 1, s_dbg};
     KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
     ++g_launches;
@@ -597,6 +599,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     if (rc) return rc;
   }
   const RunView<W> segview{X, d_lo, seg_cap, nw, 0};
+  if (getenv("LUDA_DEC_DBG")) return LUDA_OK;  // decode ablation experiments stop here
   res->n_in = n_in;
   if (ev) CK(cudaEventRecord(ev[2], st));
   // ---- merge + resolve ----

@@ -2,18 +2,20 @@
 //
 // CRC-32/IEEE (reflected 0xEDB88320, init/xorout 0xFFFFFFFF; the zlib flavour
 // of checksum.py:12-13) is computed warp-parallel: a byte range is cut into
-// END-ALIGNED 68-byte segments (17 words). In one pass a warp covers 64
-// segments (4352 B): lane d owns the segments at distance d and d+32 from the
-// pass end and runs their two table chains interleaved (2-way ILP). Segment
+// END-ALIGNED 36-byte segments (9 words). In one pass a warp covers 128
+// segments (4608 B): lane d owns the segments at distance d, d+32, d+64, d+96
+// from the pass end and runs their four table chains interleaved (4-way ILP:
+// the chains are latency-bound, two dependent LDS per word). Segment
 // registers are combined with the GF(2) "advance over n zero bytes" operator
-// Z_n (the crc32_combine algebra: raw(A∥B) = Z_|B|(raw(A)) ^ raw(B)):
-//   lane value = Z_{68d}( raw(seg d) ^ Z_2176(raw(seg d+32)) ), XOR over lanes.
+// Z_n (the crc32_combine algebra: raw(A∥B) = Z_|B|(raw(A)) ^ raw(B)), by
+// Horner over the lane's chains with H = Z_1152:
+//   lane value = Z_{36d}( r_d ^ H(r_{d+32} ^ H(r_{d+64} ^ H(r_{d+96}))) ), XOR over lanes.
 // Words go through SLICING-BY-2 tables (two 16-bit steps per word). The two
 // byte tables T1 (byte then a zero byte) and T0 are replicated once per lane
 // and interleaved so that one PRMT forms the whole shared-memory offset:
 //   offset = idx << 8 | table << 7 | lane << 2      (64 KB, bank = lane)
 // i.e. per 2 bytes: 2 PRMT + 2 LDS + SHF + LOP3, no bank conflicts.
-// 17 words (odd) per segment makes the 32 lanes' LDS.32 data streams hit 32
+// 9 words (odd) per segment makes the 32 lanes' LDS.32 data streams hit 32
 // distinct banks. The ~0 preset is folded into the data: callers run
 // crc_prep() on the smem copy (zero the 72 bytes before it, complement the
 // first 4 bytes: F(~0, D) = F(0, D') and leading zeros leave a zero register
@@ -25,19 +27,20 @@
 namespace luda {
 
 constexpr uint32_t kCrcPoly = 0xEDB88320u;
-constexpr int kSeg = 68;             // bytes per CRC segment
-constexpr int kSegWords = kSeg / 4;  // 17
-constexpr int kHalf = 32 * kSeg;     // 2176: distance between a lane's two segments
-constexpr int kGroup = 64 * kSeg;    // 4352: bytes one warp covers per pass
+constexpr int kSeg = 36;             // bytes per CRC segment
+constexpr int kSegWords = kSeg / 4;  // 9 (odd: the lanes' word streams hit distinct banks)
+constexpr int kChains = 4;           // segments (independent table chains) per lane per pass
+constexpr int kHalf = 32 * kSeg;     // 1152: distance between a lane's consecutive segments
+constexpr int kGroup = 32 * kChains * kSeg;  // 4608: bytes one warp covers per pass
 constexpr int kCrcLead = 72;         // zeroed bytes required before the data
 
 // ---- tables (device globals; initialised by luda_init) ---------------------
 // g_crc_tab[b]          : byte table T0[b]
 // g_crc_tab1[b]         : T1[b] = T0 advanced over one more (zero) byte
-// g_seg_nib[n][v][d]    : Z_{68*d}(v << 4n)    (8 x 16 x 32 words)
-// g_half_tab[k][b]      : Z_2176(b << 8k)     (4 x 256 words)
+// g_seg_nib[n][v][d]    : Z_{36*d}(v << 4n)    (8 x 16 x 32 words)
+// g_half_tab[k][b]      : Z_1152(b << 8k)     (4 x 256 words)
 // c_zpow[i][j]          : Z_{2^i}(1 << j)      (48 x 32 words) for arbitrary shifts
-// c_zgroup[j]           : Z_4352(1 << j)       (one warp pass)
+// c_zgroup[j]           : Z_4608(1 << j)       (one warp pass)
 // (single translation unit: luda_b200.cu includes every stage header)
 __device__ uint32_t g_crc_tab[256];
 __device__ uint32_t g_crc_tab1[256];
@@ -45,6 +48,9 @@ __device__ uint32_t g_seg_nib[8 * 16 * 32];
 __device__ uint32_t g_half_tab[4 * 256];
 __constant__ uint32_t c_zpow[48][32];
 __constant__ uint32_t c_zgroup[32];
+__constant__ uint32_t c_zinv[3][8][16];  // nibble tables of Z_{-p}, p = 1..3 (inverse shifts)
+constexpr int kZoneMax = 8192;
+__device__ uint32_t g_zone[kZoneMax];    // Z_n(0xFFFFFFFF): the ~0 preset advanced over n bytes
 
 // Shared-memory CRC state: the lane-replicated slicing-by-2 tables (64 KB),
 // the per-lane nibble tables (16 KB) and the Z_2176 byte tables (4 KB).
@@ -82,11 +88,12 @@ __device__ __forceinline__ uint32_t crc_lut(const CrcLane& t, uint32_t off) {
   return *reinterpret_cast<const uint32_t*>(t.base + off);
 }
 
-// One 16-bit step: x already holds crc ^ data in its low half.
+// One 16-bit step: x already holds crc ^ data in its low half. (x >> 16 as
+// a multiply-high keeps it on the FMA pipe; PRMT/LOP3 load the ALU pipe.)
 __device__ __forceinline__ uint32_t crc_half(uint32_t x, const CrcLane& t) {
   const uint32_t a = crc_lut(t, prmt(x, t.a1, 0x7604u));  // T1[x & 0xFF]
   const uint32_t b = crc_lut(t, prmt(x, t.a0, 0x7614u));  // T0[(x >> 8) & 0xFF]
-  return (x >> 16) ^ a ^ b;
+  return __umulhi(x, 0x10000u) ^ a ^ b;
 }
 
 // One word through the register update (two slicing-by-2 steps).
@@ -98,7 +105,7 @@ __device__ __forceinline__ uint32_t crc_byte(uint32_t c, uint32_t b, const CrcLa
   return crc_lut(t, prmt(c ^ b, t.a0, 0x7604u)) ^ (c >> 8);  // T0[(c ^ b) & 0xFF] ^ (c >> 8)
 }
 
-// Z_{68*lane}(c) via the lane's nibble tables. `nl` = s.nib + lane.
+// Z_{36*lane}(c) via the lane's nibble tables. `nl` = s.nib + lane.
 __device__ __forceinline__ uint32_t seg_shift(uint32_t c, const uint32_t* __restrict__ nl) {
   uint32_t r = 0;
 #pragma unroll
@@ -106,7 +113,7 @@ __device__ __forceinline__ uint32_t seg_shift(uint32_t c, const uint32_t* __rest
   return r;
 }
 
-// Z_2176(c) (warp-uniform operator, byte tables).
+// Z_1152(c) (byte tables).
 __device__ __forceinline__ uint32_t half_shift(uint32_t c, const uint32_t* __restrict__ ht) {
   return ht[c & 0xFFu] ^ ht[256 + ((c >> 8) & 0xFFu)] ^ ht[512 + ((c >> 16) & 0xFFu)] ^ ht[768 + (c >> 24)];
 }
@@ -141,8 +148,8 @@ __device__ __forceinline__ void crc_unprep(uint8_t* data) {
   __syncwarp();
 }
 
-// Raw CRC register of the 17 words starting at smem byte address p (any
-// alignment; reads the aligned words covering [p, p+72)).
+// Segment pointer at smem byte address p (any alignment): the aligned words
+// covering [p, p + kSeg + 4) and the funnel shift.
 struct SegPtr {
   const uint32_t* wp;
   uint32_t sh;
@@ -153,39 +160,95 @@ __device__ __forceinline__ SegPtr seg_ptr(const uint8_t* p) {
   return SegPtr{reinterpret_cast<const uint32_t*>(p - mis), mis * 8u};
 }
 
+// Horner combine of a lane's chain registers r[0..kChains) (r[c] = segment at
+// distance d + 32c), then the lane's Z_{36d}.
+__device__ __forceinline__ uint32_t lane_combine(const uint32_t (&r)[kChains], const CrcSmem& cs, uint32_t lane) {
+  uint32_t v = r[kChains - 1];
+#pragma unroll
+  for (int c = kChains - 2; c >= 0; --c) v = half_shift(v, cs.half) ^ r[c];
+  return seg_shift(v, cs.nib + lane);
+}
+
 // Warp: un-combined pass value of pass q over prepared smem data of length n:
-// this lane's Z_{68 lane}( raw(seg d) ^ Z_2176(raw(seg d+32)) ) before the
-// cross-lane XOR, with d = lane + 64q (pass q covers distances [64q, 64q+64)).
+// this lane's combined chains before the cross-lane XOR, with segment
+// distances d = lane + 32c + 128q (pass q covers distances [128q, 128q+128)).
 __device__ __forceinline__ uint32_t pass_lane_value(const uint8_t* data, uint64_t n, uint32_t q, const CrcSmem& cs,
                                                     const uint8_t* safe) {
   const uint32_t lane = lane_id();
   const CrcLane tl = crc_lane(cs, lane);
   const int64_t nseg = ((int64_t)n + kSeg - 1) / kSeg;
-  const int64_t dlo = (int64_t)lane + 64 * (int64_t)q;
-  const int64_t dhi = dlo + 32;
-  const bool vlo = dlo < nseg, vhi = dhi < nseg;
-  const int64_t slo = (int64_t)n - (int64_t)kSeg * (dlo + 1);
-  const int64_t shi = (int64_t)n - (int64_t)kSeg * (dhi + 1);
-  const SegPtr a = seg_ptr(vlo ? data + slo : safe);  // `safe`: any readable smem (skipped chain)
-  const SegPtr b = seg_ptr(vhi ? data + shi : safe);
-  uint32_t ca = 0, cb = 0;
-  uint32_t la = a.wp[0], lb = b.wp[0];
-#pragma unroll 17
-  for (int j = 0; j < kSegWords; ++j) {
-    const uint32_t ha = a.wp[j + 1], hb = b.wp[j + 1];
-    ca = crc_word(ca, __funnelshift_r(la, ha, a.sh), tl);
-    cb = crc_word(cb, __funnelshift_r(lb, hb, b.sh), tl);
-    la = ha;
-    lb = hb;
+  SegPtr sp[kChains];
+  bool val[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    const int64_t dd = (int64_t)lane + 32 * c + 128 * (int64_t)q;
+    val[c] = dd < nseg;
+    sp[c] = seg_ptr(val[c] ? data + ((int64_t)n - (int64_t)kSeg * (dd + 1)) : safe);  // `safe`: any readable smem
   }
-  uint32_t r = (vlo ? ca : 0u) ^ (vhi ? half_shift(cb, cs.half) : 0u);
-  return seg_shift(r, cs.nib + lane);
+  uint32_t r[kChains], lo[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    r[c] = 0;
+    lo[c] = sp[c].wp[0];
+  }
+#pragma unroll
+  for (int j = 0; j < kSegWords; ++j) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      const uint32_t hi = sp[c].wp[j + 1];
+      r[c] = crc_word(r[c], __funnelshift_r(lo[c], hi, sp[c].sh), tl);
+      lo[c] = hi;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) r[c] = val[c] ? r[c] : 0u;
+  return lane_combine(r, cs, lane);
 }
 
 __device__ __forceinline__ uint32_t warp_xor(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v ^= __shfl_xor_sync(0xFFFFFFFFu, v, o);
   return v;
+}
+
+// Z_{-p}(c), p in 1..3, warp-uniform p and c (constant-memory broadcast).
+__device__ __forceinline__ uint32_t crc_unshift(uint32_t c, uint32_t p) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) r ^= c_zinv[p - 1][n][(c >> (4 * n)) & 0xFu];
+  return r;
+}
+
+// Z_n(~0) (the preset's contribution to the raw register after n bytes).
+__device__ __forceinline__ uint32_t crc_zone(uint32_t n) {
+  return n < (uint32_t)kZoneMax ? g_zone[n] : crc_shift(0xFFFFFFFFu, n);
+}
+
+// WORD-ALIGNED variant of pass_lane_value: `end` is 4-byte aligned, so every
+// segment is whole words (no funnel shifts). n = bytes covered before `end`.
+__device__ __forceinline__ uint32_t pass_lane_value_al(const uint8_t* end, uint32_t n, uint32_t q, const CrcSmem& cs) {
+  const uint32_t lane = lane_id();
+  const CrcLane tl = crc_lane(cs, lane);
+  const int32_t nseg = ((int32_t)n + kSeg - 1) / kSeg;
+  const uint32_t* p[kChains];
+  bool val[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    const int32_t dd = (int32_t)lane + 32 * c + 128 * (int32_t)q;
+    val[c] = dd < nseg;
+    p[c] = reinterpret_cast<const uint32_t*>(end - kSeg * (val[c] ? dd + 1 : 1));
+  }
+  uint32_t r[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) r[c] = 0;
+#pragma unroll
+  for (int j = 0; j < kSegWords; ++j) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) r[c] = crc_word(r[c], p[c][j], tl);
+  }
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) r[c] = val[c] ? r[c] : 0u;
+  return lane_combine(r, cs, lane);
 }
 
 // Warp-cooperative CRC-32 of n >= 4 bytes of PREPARED smem data (crc_prep).
@@ -200,12 +263,31 @@ __device__ __forceinline__ uint32_t warp_crc32_prepped(const uint8_t* data, uint
   return ~acc;
 }
 
-// Convenience: prep, crc, restore (data must have 72 writable bytes before it).
+// Warp CRC-32 of n >= 4 bytes of smem data (72 writable bytes before it, 3
+// after it). The range is extended with zero bytes to a word-aligned end so
+// every segment is whole words; raw(D ∥ 0^p) = Z_p(raw(D)) is undone with
+// Z_{-p}. All modified bytes are restored.
 __device__ __forceinline__ uint32_t warp_crc32_smem(uint8_t* data, uint32_t n, const CrcSmem& cs) {
-  crc_prep(data);
-  const uint32_t c = warp_crc32_prepped(data, n, cs);
+  const uint32_t lane = lane_id();
+  const uint32_t pad = (uint32_t)(0u - (uint32_t)reinterpret_cast<uintptr_t>(data + n)) & 3u;
+  uint8_t saved = 0;
+  if (lane < pad) saved = data[n + lane];
+  __syncwarp();
+  crc_prep(data);  // (syncs)
+  if (lane < pad) data[n + lane] = 0;
+  __syncwarp();
+  const uint32_t m = n + pad;
+  const uint8_t* end = data + m;
+  const uint32_t npass = (m + kGroup - 1) / kGroup;
+  uint32_t acc = 0;
+  for (int q = (int)npass - 1; q >= 0; --q) {
+    const uint32_t v = warp_xor(pass_lane_value_al(end, m, (uint32_t)q, cs));
+    acc = (q == (int)npass - 1) ? v : (gf2_apply(c_zgroup, acc) ^ v);
+  }
+  __syncwarp();
+  if (lane < pad) data[n + lane] = saved;
   crc_unprep(data);
-  return c;
+  return ~(pad ? crc_unshift(acc, pad) : acc);
 }
 
 // Scalar CRC (any n) for tiny ranges; `tl` = table view of the calling lane.
@@ -234,6 +316,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -280,6 +365,21 @@ __device__ __forceinline__ void warp_smem_copy(uint8_t* dst, const uint8_t* src,
 }
 
 // ---- small helpers ------------------------------------------------------------
+// 4 bytes at any address (smem or global): two aligned words + byte funnel.
+__device__ __forceinline__ uint32_t ld_u32_any(const uint8_t* p) {
+  const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(p) & 3u);
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(p - mis);
+  uint32_t r;
+  asm("prmt.b32.f4e %0, %1, %2, %3;" : "=r"(r) : "r"(wp[0]), "r"(wp[1]), "r"(mis));
+  return r;
+}
+
+// Little-endian word i of a byte string: mask of its bytes at index >= v.
+__device__ __forceinline__ uint32_t byte_keep_mask(uint32_t v, int i) {
+  const int32_t sh = (int32_t)(8 * v) - 32 * i;
+  return __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)(sh > 0 ? sh : 0));
+}
+
 __device__ __forceinline__ uint32_t varint_size(uint64_t v) {
   uint32_t n = 1;
   while (v >= 0x80) { v >>= 7; ++n; }

@@ -50,14 +50,37 @@ enum BlockCode : uint32_t {
   B_VALUE_BIG = 9,      // (unsupported) value length >= 2^24 or arena offset >= 2^40
 };
 
-constexpr int kDecWarps = 14;
-constexpr int kDecStage = 4352;                  // staged window bytes (block + alignment)
-constexpr int kDecPre = 160;                     // CRC lead-in before the data
-constexpr int kDecBuf = kDecPre + kDecStage + 64;
-constexpr int kDecSlots = 128;
+// Paired warps: a PARSE warp (producer + walk + records) and a CRC warp share
+// a pair of staging slots; both consume every block of the pair's contiguous
+// block range concurrently (the CRC never modifies bytes the parse warp reads).
+constexpr int kDecPairs = 10;
+constexpr int kDecWarps = 2 * kDecPairs;
+constexpr int kDecNSlot = 3;                     // staging slots per pair (2 blocks in flight)
+constexpr int kDecLead = 48;                     // zero lead before the TMA window (never written by TMA)
+constexpr int kDecStage = 4352;                  // TMA window capacity
+constexpr int kDecSlot = kDecLead + kDecStage;   // bytes per staging slot
+constexpr int kDecSlots = 104;
 constexpr int kDecStride = 16;                   // slots per restart interval (single-walk path)
-constexpr int kDecWarpBytes = 2 * kDecBuf + kDecSlots * 8 + 16;  // 2 staging buffers, 1 slot array
-static_assert(sizeof(CrcSmem) + kDecWarps * kDecWarpBytes <= 232448, "decode smem over the 227 KB limit");
+constexpr int kDecBig = kGroup + 192;            // CTA staging for CRC passes of unstaged (large) blocks
+struct DecSlotMeta {
+  uint64_t addr;  // arena offset of the block
+  uint32_t len;   // block length
+  uint32_t staged;
+};
+struct DecPairSmem {
+  uint8_t slot[kDecNSlot][kDecSlot];
+  uint64_t full[kDecNSlot], empty[kDecNSlot];
+  DecSlotMeta meta[kDecNSlot];  // written by the producer before it arrives on full
+  uint8_t entries[kDecSlots * 8];  // DecSlot array of the parse warp
+};
+struct DecCtaSmem {
+  uint8_t big[kDecBig];
+  int lock;
+};
+static_assert(sizeof(CrcSmem) + kDecPairs * sizeof(DecPairSmem) + sizeof(DecCtaSmem) <= 232448,
+              "decode smem over the 227 KB limit");
+static_assert(kDecLead >= kSeg && kDecLead % 16 == 0, "CRC segments may start kSeg-1 bytes before the data");
+static_assert(kDecSlot % 16 == 0 && sizeof(DecPairSmem) % 16 == 0, "TMA destinations must be 16-byte aligned");
 
 struct DecSlot {
   uint32_t pos;  // block-relative offset of the key suffix
@@ -76,6 +99,7 @@ struct DecodeArgs {
   uint64_t* seg_count;      // out [nwarps]: records of each warp segment (may exceed seg_cap → rerun)
   unsigned long long* err_ref;
   unsigned long long* err_unsup;
+  uint32_t dbg;             // experiment switches (0 in production)
 };
 
 // Block range of warp segment w of nw: [w*nblk/nw, (w+1)*nblk/nw).
@@ -95,31 +119,49 @@ __device__ __forceinline__ uint32_t seg_of_block(uint32_t b, uint32_t nblk, uint
 // Fast form: 1-byte shared/unshared varints, 1–2-byte value length,
 // shared + unshared == K (so shared <= len(prev key) == K), shared == 0 on the
 // interval's first entry, entries tiling [start, end) exactly.
+// Branch-free per entry: errors are OR-ed into `bad` and decided once at the
+// end (every step advances >= 3 bytes, so garbage still terminates).
 template <typename Emit>
 __device__ __forceinline__ int32_t interval_walk(const uint8_t* d, uint32_t start, uint32_t end, uint32_t K,
                                                  Emit emit) {
   uint32_t pos = start;
   int32_t j = 0;
+  uint32_t bad = 0;
   while (pos < end) {
-    const uint32_t b0 = d[pos], b1 = d[pos + 1], b2 = d[pos + 2], b3 = d[pos + 3];
-    uint32_t vl, hl;
-    if (((b0 | b1 | b2) & 0x80u) == 0) {
-      vl = b2;
-      hl = 3;
-    } else if (((b0 | b1 | b3) & 0x80u) == 0) {
-      vl = (b2 & 0x7Fu) | (b3 << 7);
-      hl = 4;
-    } else {
-      return -1;
-    }
-    if ((j == 0 && b0 != 0) || b0 + b1 != K) return -1;
-    const uint32_t np = pos + hl + b1 + vl;
-    if (np > end) return -1;
-    emit(j, pos + hl, b0, vl);
-    pos = np;
+    const uint32_t w = ld_u32_any(d + pos);  // shared | unshared | vlen byte 0 | vlen byte 1
+    const uint32_t s = w & 0xFFu;
+    const uint32_t u = prmt(w, 0u, 0x4441u);
+    const uint32_t v1 = prmt(w, 0u, 0x4442u);
+    const uint32_t two = (w >> 23) & 1u;  // 2-byte value length
+    const uint32_t vl = two ? ((v1 & 0x7Fu) | ((w >> 17) & 0x7F80u)) : v1;
+    bad |= (w & 0x8080u) | (two & (w >> 31)) | ((s + u) ^ K) | (j == 0 ? s : 0u);
+    emit(j, pos + 3u + two, s, vl);
+    pos += 3u + two + u + vl;
     ++j;
   }
-  return j;
+  return (bad || pos != end) ? -1 : j;
+}
+
+// Entry-header positions of one restart interval (no validation: every
+// header is checked afterwards, lane per entry). Value-length varints of 1 or
+// 2 bytes are assumed; any other header makes the chain miss `end` or fail the
+// later check. Returns the entry count, or -1 if the chain does not end
+// exactly at `end`.
+template <typename Emit>
+__device__ __forceinline__ int32_t interval_positions(const uint8_t* d, uint32_t start, uint32_t end, Emit emit) {
+  uint32_t pos = start;
+  int32_t j = 0;
+  while (pos < end) {
+    const uint32_t w = ld_u32_any(d + pos);
+    emit(j, pos);
+    const uint32_t u = prmt(w, 0u, 0x4441u);
+    const uint32_t b2 = prmt(w, 0u, 0x4442u);
+    const uint32_t b3 = __umulhi(w, 0x100u);        // w >> 24
+    const uint32_t two = __umulhi(b2, 1u << 25);    // b2 >> 7
+    pos += 3u + u + b2 + two * (b3 * 128u - 127u);  // 2-byte: 4 + u + (b2 & 0x7F) + (b3 << 7)
+    ++j;
+  }
+  return pos == end ? j : -1;
 }
 
 // Exact sequential decode_data_block walk (blocks.py:151-164). Returns the
@@ -152,20 +194,6 @@ __device__ uint32_t block_walk_exact(const uint8_t* d, uint64_t payload, uint64_
   return pos != entries_end ? B_TRAILING : B_OK;
 }
 
-constexpr int kDecTile = 2;  // staging buffers per warp (double buffer)
-
-// Per-warp smem layout (offsets from the warp's base `wb`, all smem-derived
-// pointers so the compiler emits LDS/STS):
-//   [0, kDecBuf)            staging buffer 0
-//   [kDecBuf, 2 kDecBuf)    staging buffer 1
-//   [2 kDecBuf, +1 KB)      entry slots
-//   then 2 mbarriers
-__device__ __forceinline__ uint8_t* dec_buf(uint8_t* wb, int which) { return wb + which * kDecBuf; }
-__device__ __forceinline__ DecSlot* dec_slots(uint8_t* wb) { return reinterpret_cast<DecSlot*>(wb + kDecTile * kDecBuf); }
-__device__ __forceinline__ uint64_t* dec_bar(uint8_t* wb, int which) {
-  return reinterpret_cast<uint64_t*>(wb + kDecTile * kDecBuf + kDecSlots * 8) + which;
-}
-
 __device__ __forceinline__ uint32_t dec_window(const uint8_t* g, uint32_t len) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(g);
   return (uint32_t)(((a + len + 15) & ~uintptr_t(15)) - (a & ~uintptr_t(15)));
@@ -186,33 +214,14 @@ struct DecState {
   uint32_t my_st, my_en;
 };
 
-// Issue the TMA staging of block b into buffer `which` (lane 0). Returns
-// whether the block is staged (else it is read in place).
-template <int W>
-__device__ __forceinline__ bool dec_prefetch(const DecodeArgs<W>& a, uint32_t b, uint8_t* wb, int which) {
-  if (b >= a.nblk) return false;
-  const uint32_t len = a.bt.len[b];
-  const uint8_t* g = a.arena + a.bt.addr[b];
-  const uint32_t win = dec_window(g, len);
-  if (len < 12 || win > (uint32_t)kDecStage) return false;
-  if (lane_id() == 0) {
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(dec_bar(wb, which), win);
-    bulk_g2s(dec_buf(wb, which) + kDecPre,
-             reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(g) & ~uintptr_t(15)), win,
-             dec_bar(wb, which));
-  }
-  return true;
-}
-
 // Phase 1: structural checks + entry walk (counts; single-walk fills slots).
 template <int W>
-__device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t b, const uint8_t* d,
-                                               DecSlot* slots) {
+__device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t b, uint64_t addr, uint32_t blen,
+                                               const uint8_t* d, DecSlot* slots) {
   const uint32_t lane = lane_id();
   DecState st{};
-  st.len = a.bt.len[b];
-  st.addr = a.bt.addr[b];
+  st.len = blen;
+  st.addr = addr;
   const uint32_t K = a.K;
   const uint32_t len = st.len;
   st.code = len < 12 ? (uint32_t)B_SHORT : 0u;
@@ -232,20 +241,59 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
         st.my_st = ld_u32_le(d + entries_end + 4 * lane);
         st.my_en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint32_t)entries_end;
         ok = (lane != 0 || st.my_st == 0) && st.my_st < st.my_en && (int64_t)st.my_en <= entries_end;
-        if (ok) {
+      }
+      bool fast = false;
+      if (single) {
+        // Positions-only walk (lane per interval), then every entry header is
+        // validated and decoded in parallel (lane per entry).
+        if (lane < nres && ok) {
           DecSlot* mine = slots + kDecStride * lane;
-          st.my_cnt = interval_walk(d, st.my_st, st.my_en, K, [&](int32_t j, uint32_t pos, uint32_t s, uint32_t vl) {
-            if (single && j < kDecStride) mine[j] = DecSlot{pos, (vl << 8) | s};
+          st.my_cnt = interval_positions(d, st.my_st, st.my_en, [&](int32_t j, uint32_t pos) {
+            if (j < kDecStride) mine[j].pos = pos;
           });
-          ok = st.my_cnt >= 0;
+          ok = st.my_cnt >= 0 && st.my_cnt <= kDecStride;
+        }
+        if (__all_sync(0xFFFFFFFFu, ok)) {
+          __syncwarp();
+          uint32_t bad = 0;
+          for (uint32_t i0 = 0; i0 < kDecStride * nres; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const uint32_t k = i >> 4, j = i & (kDecStride - 1);
+            const int32_t ck = __shfl_sync(0xFFFFFFFFu, st.my_cnt, k < 32 ? k : 31);
+            if (k < nres && (int32_t)j < ck) {
+              const uint32_t pos = slots[i].pos;
+              const uint32_t w = ld_u32_any(d + pos);
+              const uint32_t sh = w & 0xFFu;
+              const uint32_t u = prmt(w, 0u, 0x4441u);
+              const uint32_t v1 = prmt(w, 0u, 0x4442u);
+              const uint32_t two = (w >> 23) & 1u;
+              const uint32_t vl = two ? ((v1 & 0x7Fu) | ((w >> 17) & 0x7F80u)) : v1;
+              bad |= (w & 0x8080u) | (two & (w >> 31)) | ((sh + u) ^ K) | (j == 0 ? sh : 0u);
+              slots[i] = DecSlot{pos + 3u + two, (vl << 8) | sh};
+            }
+          }
+          fast = !__any_sync(0xFFFFFFFFu, bad != 0);
+          __syncwarp();
+          if (fast) st.mode = 1;
         }
       }
-      if (__all_sync(0xFFFFFFFFu, ok)) {
+      if (!fast) {
+        // general canonical walk (validating); mode 2 re-walks it window by window
+        ok = true;
+        if (lane < nres) {
+          ok = (lane != 0 || st.my_st == 0) && st.my_st < st.my_en && (int64_t)st.my_en <= entries_end;
+          if (ok) {
+            st.my_cnt = interval_walk(d, st.my_st, st.my_en, K, [](int32_t, uint32_t, uint32_t, uint32_t) {});
+            ok = st.my_cnt >= 0;
+          }
+        }
+        if (__all_sync(0xFFFFFFFFu, ok)) st.mode = 2;
+      }
+      if (st.mode != 3) {
         const int32_t c = lane < nres ? st.my_cnt : 0;
         const int32_t incl = warp_incl_scan<int32_t>(c);
         st.my_pre = incl - c;
         st.n = (uint64_t)(uint32_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
-        st.mode = (single && __all_sync(0xFFFFFFFFu, c <= kDecStride)) ? 1 : 2;
       }
     }
     if (st.mode == 3) {
@@ -262,38 +310,26 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
   return st;
 }
 
-// Phase 2: CRC verify, then records at out[base ...]. kStaged: `d` is the
-// smem copy (CRC in place); else the block is read from global memory and its
-// CRC staged pass by pass through `stage`.
+// Phase 2 (parse warp): reference errors of the walk, then records at
+// out[base ...]. The CRC is verified concurrently by the pair's CRC warp
+// (B_CRC ranks before every parse error of the same block, so the min-reduced
+// error code keeps the reference order: length, CRC, restarts, entries).
 template <int W, bool kStaged>
 __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, DecState& st, uint64_t base,
-                                           uint64_t cap, const uint8_t* d, DecSlot* slots, uint8_t* stage,
-                                           const CrcSmem& cs) {
+                                           uint64_t cap, const uint8_t* d, DecSlot* slots) {
   constexpr int NW = 2 * W + 2;
   const uint32_t lane = lane_id();
   const uint32_t K = a.K;
   const uint32_t len = st.len;
   uint32_t code = st.code;
-  if (!code) {
-    uint32_t crc;
-    if (kStaged) {
-      crc = warp_crc32_smem(const_cast<uint8_t*>(d), len - 4, cs);
-    } else {
-      const uint64_t np = ((uint64_t)len - 4 + kGroup - 1) / kGroup;
-      uint32_t raw = 0;
-      for (uint64_t q = 0; q < np; ++q) raw ^= warp_crc_pass_global(d, len - 4, q, stage, cs);
-      crc = ~raw;
-    }
-    if (crc != ld_u32_le(d + len - 4)) code = B_CRC;
-    else if (st.restart_bad) code = B_RESTART;
-    else code = st.pcode;
-  }
+  if (!code) code = st.restart_bad ? (uint32_t)B_RESTART : st.pcode;
   const uint64_t n = st.n;
   if (code || st.unsup || base + n > cap) {
     if (lane == 0 && code) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
     if (lane == 0 && !code && st.unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | st.unsup);
     return;
   }
+  if (a.dbg & 2) return;
   const uint32_t L = K - 8;
   const int mode = st.mode;
   const uint32_t nres = st.nres;
@@ -353,11 +389,12 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
         }
       }
       uint32_t v = act ? s : 0u;  // bytes [v, K) valid
+      // only words below the largest shared prefix of the chunk need filling
+      const uint32_t nwf = (__reduce_max_sync(0xFFFFFFFFu, v) + 3u) >> 2;
       if (lane == 0 && v) {
 #pragma unroll
         for (int i = 0; i < NW; ++i) {
-          const int32_t bi = (int32_t)v - 4 * i;
-          const uint32_t keep = bi <= 0 ? 0xFFFFFFFFu : (bi >= 4 ? 0u : (0xFFFFFFFFu << (8 * bi)));
+          const uint32_t keep = byte_keep_mask(v, i);
           kw[i] = (kw[i] & keep) | (carry[i] & ~keep);
         }
         v = 0;
@@ -366,21 +403,19 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
       for (int dd = 1; dd < 32; dd <<= 1) {
         if (!__any_sync(0xFFFFFFFFu, v != 0)) break;
         const uint32_t ov = __shfl_up_sync(0xFFFFFFFFu, v, dd);
-        uint32_t ow[NW];
+        const bool take = lane >= (uint32_t)dd && v;
 #pragma unroll
-        for (int i = 0; i < NW; ++i) ow[i] = __shfl_up_sync(0xFFFFFFFFu, kw[i], dd);
-        if (lane >= (uint32_t)dd && v) {
-#pragma unroll
-          for (int i = 0; i < NW; ++i) {
-            const int32_t bi = (int32_t)v - 4 * i;
-            const uint32_t keep = bi <= 0 ? 0xFFFFFFFFu : (bi >= 4 ? 0u : (0xFFFFFFFFu << (8 * bi)));
-            kw[i] = (kw[i] & keep) | (ow[i] & ~keep);
+        for (int i = 0; i < NW; ++i) {
+          if ((uint32_t)i < nwf) {  // warp-uniform
+            const uint32_t ow = __shfl_up_sync(0xFFFFFFFFu, kw[i], dd);
+            const uint32_t keep = byte_keep_mask(v, i);
+            if (take) kw[i] = (kw[i] & keep) | (ow & ~keep);
           }
-          v = ov < v ? ov : v;
         }
+        if (take) v = ov < v ? ov : v;
       }
 #pragma unroll
-      for (int i = 0; i < NW; ++i) carry[i] = __shfl_sync(0xFFFFFFFFu, kw[i], 31);
+      for (int i = 0; i < NW; ++i) carry[i] = __shfl_sync(0xFFFFFFFFu, kw[i], wn - c0 >= 32 ? 31 : wn - c0 - 1);
       if (act) {
         Rec<W> r;
         words_to_rec<W, NW>(kw, L, r);
@@ -392,60 +427,161 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   }
 }
 
-// `base` = physical record index of the block's first record, `cap` = end of
-// the warp's segment; returns the block's entry count.
-template <int W, bool kStaged>
-__device__ __forceinline__ uint64_t dec_block(const DecodeArgs<W>& a, uint32_t b, uint8_t* wb, int which,
-                                              uint32_t& phase, const CrcSmem& cs, uint64_t base, uint64_t cap) {
-  uint8_t* buf = dec_buf(wb, which);
-  const uint8_t* g = a.arena + a.bt.addr[b];
-  const uint8_t* d;
-  if (kStaged) {
-    mbar_wait(dec_bar(wb, which), (phase >> which) & 1u);
-    phase ^= 1u << which;
-    d = buf + kDecPre + (reinterpret_cast<uintptr_t>(g) & 15);
-  } else {
-    d = g;
+// CRC-32 of a staged block's payload [data, data + n), n >= 4, WITHOUT
+// touching any byte the parse warp reads: the <= 15 garbage bytes between
+// the TMA window start and `data` and the <= 3 stored-CRC bytes after the
+// payload are zeroed (the slot lead before the window is always zero), the
+// range is extended to a word-aligned end, raw(0, D) is recovered with
+// Z_{-pad}, and the ~0 preset is added back as Z_n(~0) (g_zone table).
+__device__ __forceinline__ uint32_t dec_crc_staged(uint8_t* win, uint8_t* data, uint32_t n, const CrcSmem& cs) {
+  const uint32_t lane = lane_id();
+  const uint32_t pre = (uint32_t)(data - win);
+  if (lane < pre) win[lane] = 0;
+  const uint32_t pad = (uint32_t)(0u - (uint32_t)reinterpret_cast<uintptr_t>(data + n)) & 3u;
+  if (lane < pad) data[n + lane] = 0;
+  __syncwarp();
+  const uint32_t m = n + pad;
+  const uint8_t* end = data + m;
+  const uint32_t npass = (m + kGroup - 1) / kGroup;
+  uint32_t acc = 0;
+  for (int q = (int)npass - 1; q >= 0; --q) {
+    const uint32_t v = warp_xor(pass_lane_value_al(end, m, (uint32_t)q, cs));
+    acc = (q == (int)npass - 1) ? v : (gf2_apply(c_zgroup, acc) ^ v);
   }
-  DecSlot* slots = dec_slots(wb);
-  DecState st = dec_phase1(a, b, d, slots);
-  dec_phase2<W, kStaged>(a, b, st, base, cap, d, slots, buf, cs);
-  return st.n;
+  if (pad) acc = crc_unshift(acc, pad);
+  return ~(acc ^ crc_zone(n));
 }
 
 template <int W>
 __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W> a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
-  uint8_t* wb = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kDecWarpBytes;
+  DecPairSmem* pairs = reinterpret_cast<DecPairSmem*>(smem_raw + sizeof(CrcSmem));
+  DecCtaSmem& cta = *reinterpret_cast<DecCtaSmem*>(smem_raw + sizeof(CrcSmem) + kDecPairs * sizeof(DecPairSmem));
   const uint32_t lane = lane_id();
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t p = warp % kDecPairs;
+  const bool parse = warp < kDecPairs;
+  DecPairSmem& ps = pairs[p];
   crc_smem_init(cs);
-  if (lane == 0) {
-    mbar_init(dec_bar(wb, 0), 1);
-    mbar_init(dec_bar(wb, 1), 1);
+  constexpr int kLeadChunks = kDecLead / 16;
+  for (uint32_t i = threadIdx.x; i < kDecPairs * kDecNSlot * kLeadChunks; i += blockDim.x) {
+    const uint32_t q = i / (kDecNSlot * kLeadChunks), r = i % (kDecNSlot * kLeadChunks);
+    reinterpret_cast<uint4*>(pairs[q].slot[r / kLeadChunks])[r % kLeadChunks] = make_uint4(0, 0, 0, 0);
+  }
+  if (threadIdx.x == 0) cta.lock = 0;
+  if (parse && lane == 0) {
+    for (int s = 0; s < kDecNSlot; ++s) {
+      mbar_init(&ps.full[s], 1);
+      mbar_init(&ps.empty[s], 2);
+    }
   }
   __syncthreads();
-  // Warp segment: a contiguous block range, the next block's TMA staging in
-  // flight while the current one is processed.
-  const uint32_t nw = gridDim.x * kDecWarps;
-  const uint32_t w = blockIdx.x * kDecWarps + (threadIdx.x >> 5);
-  const uint32_t b0 = seg_first_block(w, a.nblk, nw), b1 = seg_first_block(w + 1, a.nblk, nw);
-  const uint64_t seg0 = (uint64_t)w * a.seg_cap, seg1 = seg0 + a.seg_cap;
-  uint64_t cnt = 0;
-  uint32_t phase = 0;
-  int which = 0;
-  bool cur_staged = b0 < b1 && dec_prefetch(a, b0, wb, which);
-  for (uint32_t cur = b0; cur < b1; ++cur) {
-    const bool nxt_staged = cur + 1 < b1 && dec_prefetch(a, cur + 1, wb, which ^ 1);
-    if (lane == 0) a.blk_local[cur] = (uint32_t)cnt;
-    cnt += cur_staged ? dec_block<W, true>(a, cur, wb, which, phase, cs, seg0 + cnt, seg1)
-                      : dec_block<W, false>(a, cur, wb, which, phase, cs, seg0 + cnt, seg1);
-    fence_proxy_async_smem();  // generic smem accesses before the next TMA into this buffer
-    __syncwarp();
-    cur_staged = nxt_staged;
-    which ^= 1;
+  // The pair's contiguous block range; its records form one segment.
+  const uint32_t np = gridDim.x * kDecPairs;
+  const uint32_t g = blockIdx.x * kDecPairs + p;
+  const uint32_t b0 = seg_first_block(g, a.nblk, np), b1 = seg_first_block(g + 1, a.nblk, np);
+  const uint32_t nb = b1 - b0;
+  if (parse) {
+    // Producer: TMA of local block k into slot k % 3 once both consumers
+    // released it. Block-table entries are fetched 32 blocks at a time (lane
+    // j holds block kb + j) so no global load sits on the per-block path.
+    uint32_t kb = 0xFFFFFFFFu;
+    uint64_t t_addr = 0;
+    uint32_t t_len = 0;
+    auto issue = [&](uint32_t k) {
+      if (kb == 0xFFFFFFFFu || k >= kb + 32) {
+        kb = k;
+        const uint32_t bj = b0 + k + lane;
+        t_addr = bj < b1 ? a.bt.addr[bj] : 0;
+        t_len = bj < b1 ? a.bt.len[bj] : 0;
+      }
+      const uint64_t addr = __shfl_sync(0xFFFFFFFFu, t_addr, k - kb);
+      const uint32_t len = __shfl_sync(0xFFFFFFFFu, t_len, k - kb);
+      if (lane == 0) {
+        const uint32_t s = k % kDecNSlot;
+        if (k >= kDecNSlot) mbar_wait(&ps.empty[s], ((k - kDecNSlot) / kDecNSlot) & 1u);
+        const uint8_t* gp = a.arena + addr;
+        const uint32_t win = dec_window(gp, len);
+        const bool st = len >= 12 && win <= (uint32_t)kDecStage;
+        ps.meta[s] = DecSlotMeta{addr, len, st ? 1u : 0u};
+        if (st) {
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&ps.full[s], win);
+          bulk_g2s(ps.slot[s] + kDecLead, reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(gp) & ~uintptr_t(15)),
+                   win, &ps.full[s]);
+        } else {
+          mbar_arrive(&ps.full[s]);
+        }
+      }
+    };
+    for (uint32_t k = 0; k < nb && k < (uint32_t)kDecNSlot; ++k) issue(k);
+    DecSlot* slots = reinterpret_cast<DecSlot*>(ps.entries);
+    const uint64_t seg0 = (uint64_t)g * a.seg_cap, seg1 = seg0 + a.seg_cap;
+    uint64_t cnt = 0;
+    for (uint32_t k = 0; k < nb; ++k) {
+      const uint32_t s = k % kDecNSlot, b = b0 + k;
+      mbar_wait(&ps.full[s], (k / kDecNSlot) & 1u);
+      const DecSlotMeta mt = ps.meta[s];
+      const uint8_t* gp = a.arena + mt.addr;
+      if (lane == 0) a.blk_local[b] = (uint32_t)cnt;
+      uint64_t n = 0;
+      if (!(a.dbg & 4)) {
+        if (mt.staged) {
+          const uint8_t* d = ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15);
+          DecState stt = dec_phase1(a, b, mt.addr, mt.len, d, slots);
+          dec_phase2<W, true>(a, b, stt, seg0 + cnt, seg1, d, slots);
+          n = stt.n;
+        } else {
+          DecState stt = dec_phase1(a, b, mt.addr, mt.len, gp, slots);
+          dec_phase2<W, false>(a, b, stt, seg0 + cnt, seg1, gp, slots);
+          n = stt.n;
+        }
+      }
+      cnt += n;
+      fence_proxy_async_smem();  // this lane's generic slot accesses before the next TMA into it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps.empty[s]);
+      if (k + kDecNSlot < nb) issue(k + kDecNSlot);
+    }
+    if (lane == 0) a.seg_count[g] = cnt;
+  } else {
+    // CRC warp: verify every block of the range (reference: before parsing)
+    for (uint32_t k = 0; k < nb; ++k) {
+      const uint32_t s = k % kDecNSlot, b = b0 + k;
+      mbar_wait(&ps.full[s], (k / kDecNSlot) & 1u);
+      const DecSlotMeta mt = ps.meta[s];
+      const bool st_ok = mt.staged != 0;
+      const uint32_t len = mt.len;
+      if (len >= 12 && !(a.dbg & 1)) {
+        const uint8_t* gp = a.arena + mt.addr;
+        uint32_t crc, stored;
+        if (st_ok) {
+          uint8_t* wstart = ps.slot[s] + kDecLead;
+          uint8_t* d = wstart + (reinterpret_cast<uintptr_t>(gp) & 15);
+          stored = ld_u32_le(d + len - 4);
+          __syncwarp();
+          crc = dec_crc_staged(wstart, d, len - 4, cs);
+        } else {
+          // rare large block: CRC passes staged through the CTA's shared buffer
+          stored = ld_u32_le(gp + len - 4);
+          if (lane == 0)
+            while (atomicCAS(&cta.lock, 0, 1) != 0) __nanosleep(64);
+          __syncwarp();
+          const uint64_t npass = ((uint64_t)len - 4 + kGroup - 1) / kGroup;
+          uint32_t raw = 0;
+          for (uint64_t q = 0; q < npass; ++q) raw ^= warp_crc_pass_global(gp, len - 4, q, cta.big, cs);
+          crc = ~raw;
+          __syncwarp();
+          if (lane == 0) atomicExch(&cta.lock, 0);
+        }
+        if (lane == 0 && crc != stored) atomicMin(a.err_ref, ((unsigned long long)b << 8) | B_CRC);
+      }
+      fence_proxy_async_smem();  // this lane's generic slot accesses before the next TMA into it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps.empty[s]);
+    }
   }
-  if (lane == 0) a.seg_count[w] = cnt;
 }
 
 // Segment starts (logical record index): exclusive scan of the segment

@@ -125,6 +125,12 @@ __device__ __forceinline__ void rec_to_words(const Rec<W>& r, uint32_t L, uint32
 // LE u32 key words (internal key of length K = L + 8) → record key fields.
 template <int W, int NW>
 __device__ __forceinline__ void words_to_rec(const uint32_t (&kw)[NW], uint32_t L, Rec<W>& r) {
+  if (L == 8 * W) {  // user key fills the words exactly (warp-uniform)
+#pragma unroll
+    for (int j = 0; j < W; ++j) r.k[j] = ((uint64_t)bswap32(kw[2 * j]) << 32) | bswap32(kw[2 * j + 1]);
+    r.t = ~(((uint64_t)kw[2 * W + 1] << 32) | kw[2 * W]);
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < W; ++j) {
     uint64_t v = ((uint64_t)bswap32(kw[2 * j]) << 32) | bswap32(kw[2 * j + 1]);

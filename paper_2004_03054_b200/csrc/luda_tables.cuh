@@ -3,8 +3,8 @@
 // Host code computes, once per process (luda_init):
 //   g_crc_tab   byte table of the reflected polynomial 0xEDB88320
 //   g_crc_tab1  slicing-by-2 partner table (byte, then a zero byte)
-//   g_seg_nib   nibble tables of Z_{68*d}, d = 0..31 (segment combine)
-//   g_half_tab  byte tables of Z_2176 (a lane's second segment)
+//   g_seg_nib   nibble tables of Z_{36*d}, d = 0..31 (segment combine)
+//   g_half_tab  byte tables of Z_1152 (between a lane's segments)
 //   c_zpow      columns of Z_{2^i}, i = 0..47 (arbitrary shifts)
 //   c_zgroup    columns of Z_4352 (one warp pass)
 // where Z_n advances a raw CRC register over n zero bytes (the operator
@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+
+#include <utility>
 
 #include "luda_common.cuh"
 
@@ -47,7 +49,7 @@ using namespace tables_detail;
 int upload_crc_tables() {
   uint32_t t[256];
   host_table(t);
-  // Z_68 columns, then Z_{68 d} by repeated application.
+  // Z_kSeg columns, then Z_{kSeg d} by repeated application.
   uint32_t z132[32];
   for (int j = 0; j < 32; ++j) z132[j] = zero_bytes(t, 1u << j, kSeg);
   static uint32_t nib[8 * 16 * 32];
@@ -80,6 +82,57 @@ int upload_crc_tables() {
   if (cudaMemcpyToSymbol(g_seg_nib, nib, sizeof(nib)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(c_zpow, zpow, sizeof(zpow)) != cudaSuccess) return 1;
   if (cudaMemcpyToSymbol(c_zgroup, zg, sizeof(zg)) != cudaSuccess) return 1;
+  // Z_{-p}: Z_1 is invertible (x is a unit mod the CRC polynomial); find the
+  // inverse columns by solving Z_1 * v = e_j over GF(2) (Gaussian elimination).
+  uint32_t inv1[32];
+  {
+    uint32_t m[32], rhs[32];
+    for (int i = 0; i < 32; ++i) { m[i] = 0; rhs[i] = 0; }
+    // row i of Z_1: bit i of each column
+    for (int i = 0; i < 32; ++i)
+      for (int j = 0; j < 32; ++j)
+        if ((zpow[0][j] >> i) & 1) m[i] |= 1u << j;
+    for (int i = 0; i < 32; ++i) rhs[i] = 1u << i;  // rhs columns packed per row: solve Z_1 X = I
+    for (int col = 0; col < 32; ++col) {
+      int piv = -1;
+      for (int r = col; r < 32; ++r)
+        if ((m[r] >> col) & 1) { piv = r; break; }
+      if (piv < 0) return 1;
+      std::swap(m[piv], m[col]);
+      std::swap(rhs[piv], rhs[col]);
+      for (int r = 0; r < 32; ++r)
+        if (r != col && ((m[r] >> col) & 1)) { m[r] ^= m[col]; rhs[r] ^= rhs[col]; }
+    }
+    // now X = rhs as rows: X[i] row i, bit j = X(i, j); column j of X
+    for (int j = 0; j < 32; ++j) {
+      uint32_t c = 0;
+      for (int i = 0; i < 32; ++i)
+        if ((rhs[i] >> j) & 1) c |= 1u << i;
+      inv1[j] = c;
+    }
+    for (int j = 0; j < 32; ++j)
+      if (apply_cols(zpow[0], inv1[j]) != (1u << j)) return 1;
+  }
+  static uint32_t zinv[3][8][16];
+  uint32_t cur[32];
+  memcpy(cur, inv1, sizeof(cur));
+  for (int p = 0; p < 3; ++p) {
+    for (int nb = 0; nb < 8; ++nb)
+      for (int v = 0; v < 16; ++v) zinv[p][nb][v] = apply_cols(cur, (uint32_t)v << (4 * nb));
+    uint32_t next[32];
+    for (int j = 0; j < 32; ++j) next[j] = apply_cols(inv1, cur[j]);
+    memcpy(cur, next, sizeof(cur));
+  }
+  if (cudaMemcpyToSymbol(c_zinv, zinv, sizeof(zinv)) != cudaSuccess) return 1;
+  static uint32_t zone[kZoneMax];
+  {
+    uint32_t c = 0xFFFFFFFFu;
+    for (int n = 0; n < kZoneMax; ++n) {
+      zone[n] = c;
+      c = t[c & 0xFF] ^ (c >> 8);
+    }
+  }
+  if (cudaMemcpyToSymbol(g_zone, zone, sizeof(zone)) != cudaSuccess) return 1;
   return 0;
 }
 

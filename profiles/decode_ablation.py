@@ -1,0 +1,37 @@
+"""Decode-kernel ablation on the c3 bench job (experiment, not a bench):
+LUDA_DEC_DBG bits: 1 = skip CRC, 2 = skip record build/write, 4 = skip parse
+(TMA streaming + loop only). Prints decode kernel ms per variant.
+    python profiles/decode_ablation.py            (spawns one process per variant)"""
+import ctypes, json, os, subprocess, sys
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+def one():
+    import torch
+    import bench
+    from paper_2004_03054_b200 import _native
+    torch.cuda.set_device(0)
+    L = _native.lib(0)
+    w = bench.synth_c3(int(os.environ.get("KEYS", 1 << 25)), seed=0xC3, device_index=0)
+    desc, keep = bench.job_desc(w, w.arena.data_ptr())
+    ts = []
+    for i in range(6):
+        res = _native.JobResult()
+        rc = L.luda_compact(ctypes.byref(desc), ctypes.byref(res), w.stream)
+        if rc:
+            print("status", rc, L.luda_last_error())
+        ts.append(res.k_ms[0])
+        L.luda_job_release(ctypes.byref(res))
+    print(json.dumps({"dbg": os.environ.get("LUDA_DEC_DBG", "0"), "decode_ms": sorted(ts[2:])}), flush=True)
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        one()
+    else:
+        for v in ["", "1", "2", "3", "7", "4"]:
+            env = dict(os.environ)
+            if v:
+                env["LUDA_DEC_DBG"] = v
+            else:
+                env.pop("LUDA_DEC_DBG", None)
+            subprocess.run([sys.executable, __file__, "one"], env=env)
