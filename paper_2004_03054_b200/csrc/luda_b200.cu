@@ -509,7 +509,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
                  blk_first, blk_n, blk_size, blk_pos, res->out, bigs, d_soff, d_keys};
   CK(cudaFuncSetAttribute(sst_meta_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMetaSmem));
   KT_START(4, st);
-  sst_meta_kernel<W><<<nsst, kMetaThreads, kMetaSmem, st>>>(ma);
+  sst_meta_kernel<W><<<std::min<uint32_t>(nsst, (uint32_t)g_num_sms), kMetaThreads, kMetaSmem, st>>>(ma);
   ++g_launches;
   KT_STOP(4, st);
   CK(cudaGetLastError());

@@ -115,6 +115,8 @@ __device__ __forceinline__ uint32_t cta_crc32_smem(uint8_t* data, uint32_t n, co
   return ~v;
 }
 
+constexpr int kMetaBufBytes = 48 * 1024;  // staging available to cta_crc32_global (sst_meta's buffer)
+
 // CTA-wide CRC-32 of a global range, staging passes through per-warp smem.
 __device__ __forceinline__ uint32_t cta_crc32_global(const uint8_t* g, uint64_t n, const CrcSmem& cs, uint8_t* stage,
                                                      uint32_t* red) {
@@ -128,8 +130,12 @@ __device__ __forceinline__ uint32_t cta_crc32_global(const uint8_t* g, uint64_t 
   }
   uint32_t acc = 0;
   const uint64_t npass = (n + kGroup - 1) / kGroup;
+  constexpr uint32_t kStageWarps = kMetaBufBytes / (kGroup + 192);  // warps whose staging fits `stage`
+  static_assert(kStageWarps >= 1, "meta staging buffer too small");
+  const uint32_t sw = nwarps < kStageWarps ? nwarps : kStageWarps;
   uint8_t* my = stage + wid * (kGroup + 192);
-  for (uint64_t q = wid; q < npass; q += nwarps) acc ^= warp_crc_pass_global(g, n, q, my, cs);
+  if (wid < sw)
+    for (uint64_t q = wid; q < npass; q += sw) acc ^= warp_crc_pass_global(g, n, q, my, cs);
   if (lane_id() == 0) red[wid] = acc;
   __syncthreads();
   uint32_t v = 0;
@@ -321,8 +327,8 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
 }
 
 // ---- per-SST filter + index + footer -----------------------------------------------------
-constexpr int kMetaThreads = 256;
-constexpr int kMetaBuf = 48 * 1024;
+constexpr int kMetaThreads = 512;
+constexpr int kMetaBuf = kMetaBufBytes;
 constexpr int kMetaSmem = (int)sizeof(CrcSmem) + kEncPre + kMetaBuf + 64;
 
 template <int W>
@@ -348,6 +354,24 @@ struct MetaArgs {
   uint8_t* sst_keys;           // [nsst][2][K]
 };
 
+// Bloom hash h = crc32(user key) (bloom.py:28-29): 4-byte words of the key
+// through the slicing-by-2 update, the tail bytewise.
+template <int W>
+__device__ __forceinline__ uint32_t user_key_crc(const Rec<W>& r, uint32_t L, const CrcLane& tl) {
+  uint32_t c = 0xFFFFFFFFu;
+#pragma unroll
+  for (int w = 0; w < 2 * W; ++w) {
+    if ((uint32_t)(4 * w + 4) <= L) {
+      const uint32_t be = (uint32_t)(r.k[w >> 1] >> ((w & 1) ? 0 : 32));
+      c = crc_word(c, bswap32(be), tl);
+    }
+  }
+  for (uint32_t j = L & ~3u; j < L; ++j) c = crc_byte(c, (uint32_t)(r.k[j >> 3] >> (56 - 8 * (j & 7))) & 0xFFu, tl);
+  return ~c;
+}
+
+// Persistent: one CTA per SM loops over the output SSTs (the CRC tables are
+// loaded into shared memory once per CTA).
 template <int W>
 __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -355,91 +379,103 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
   uint8_t* buf = smem_raw + sizeof(CrcSmem) + kEncPre;  // 16-aligned, 160 B lead-in
   __shared__ uint32_t red[32];
   crc_smem_init(cs);
-  const uint32_t s = blockIdx.x;
+  __syncthreads();
   const uint32_t tid = threadIdx.x, lane = lane_id();
   const uint32_t K = a.K, L = K - 8;
-  const uint32_t fb = a.sst_first_blk[s], eb = a.sst_last_blk[s];
-  const uint64_t fe = a.blk_first[fb];
-  const uint64_t ne = a.sst_nent[s];
-  const uint64_t data = a.sst_data[s];
-  uint8_t* fout = a.out + a.sst_off[s];
-  uint64_t nbits = ne * a.bits_per_key;
-  if (nbits < 64) nbits = 64;
-  nbits = (nbits + 7) & ~7ull;
-  const uint64_t nbytes = nbits / 8;
-  const bool small = nbytes + 1 <= (uint64_t)kMetaBuf;
-  uint32_t* bits = small ? reinterpret_cast<uint32_t*>(buf) : a.scratch + a.scratch_off[s];
-  if (small)
-    for (uint32_t i = tid; i < (nbytes + 1 + 3) / 4; i += kMetaThreads) bits[i] = 0;
-  __syncthreads();
-  // ---- bloom bits ----
   const CrcLane tl = crc_lane(cs, lane);
-  for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
-    const Rec<W> r = a.rec[e];
-    uint32_t c = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = 0; j < 8 * W; ++j)
-      if ((uint32_t)j < L) c = crc_byte(c, (uint32_t)(r.k[j >> 3] >> (56 - 8 * (j & 7))) & 0xFFu, tl);
-    const uint32_t h = ~c;
-    const uint32_t delta = (h >> 17) | (h << 15);
-    const uint64_t nb64 = nbits;
-    uint64_t p = (uint64_t)h % nb64;
-    const uint64_t step = (uint64_t)delta % nb64;
-    for (uint32_t j = 0; j < a.kprobes; ++j) {
-      atomicOr(bits + (p >> 5), 1u << (p & 31));
-      p += step;
-      if (p >= nb64) p -= nb64;
+  for (uint32_t s = blockIdx.x; s < a.nsst; s += gridDim.x) {
+    const uint32_t fb = a.sst_first_blk[s], eb = a.sst_last_blk[s];
+    const uint64_t fe = a.blk_first[fb];
+    const uint64_t ne = a.sst_nent[s];
+    const uint64_t data = a.sst_data[s];
+    uint8_t* fout = a.out + a.sst_off[s];
+    uint64_t nbits = ne * a.bits_per_key;
+    if (nbits < 64) nbits = 64;
+    nbits = (nbits + 7) & ~7ull;
+    const uint64_t nbytes = nbits / 8;
+    const bool small = nbytes + 1 <= (uint64_t)kMetaBuf;
+    uint32_t* bits = small ? reinterpret_cast<uint32_t*>(buf) : a.scratch + a.scratch_off[s];
+    if (small)
+      for (uint32_t i = tid; i < (nbytes + 1 + 3) / 4; i += kMetaThreads) bits[i] = 0;
+    __syncthreads();
+    // ---- bloom bits: positions (h + j*delta) mod n_bits, 64-bit (bloom.py:81-87) ----
+    if (nbits < (1ull << 31)) {
+      const uint32_t nb32 = (uint32_t)nbits;
+      for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
+        const uint32_t h = user_key_crc<W>(a.rec[e], L, tl);
+        const uint32_t delta = (h >> 17) | (h << 15);
+        uint32_t p = h % nb32;
+        const uint32_t step = delta % nb32;
+        for (uint32_t j = 0; j < a.kprobes; ++j) {
+          atomicOr(bits + (p >> 5), 1u << (p & 31));
+          p += step;
+          if (p >= nb32) p -= nb32;
+        }
+      }
+    } else {
+      for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
+        const uint32_t h = user_key_crc<W>(a.rec[e], L, tl);
+        const uint32_t delta = (h >> 17) | (h << 15);
+        uint64_t p = (uint64_t)h % nbits;
+        const uint64_t step = (uint64_t)delta % nbits;
+        for (uint32_t j = 0; j < a.kprobes; ++j) {
+          atomicOr(bits + (p >> 5), 1u << (p & 31));
+          p += step;
+          if (p >= nbits) p -= nbits;
+        }
+      }
     }
-  }
-  __syncthreads();
-  // ---- filter block: bits ∥ k ∥ crc ----
-  uint8_t* fb8 = reinterpret_cast<uint8_t*>(bits);
-  if (tid == 0) fb8[nbytes] = (uint8_t)a.kprobes;
-  __syncthreads();
-  const uint32_t fcrc = small ? cta_crc32_smem(fb8, (uint32_t)(nbytes + 1), cs, red)
-                              : cta_crc32_global(fb8, nbytes + 1, cs, buf, red);
-  coop_copy(fout + data, fb8, nbytes + 1, tid, kMetaThreads);
-  if (tid == 0) put_u32(fout + data + nbytes + 1, fcrc);
-  __syncthreads();
-  // ---- index block ----
-  const uint64_t flen = nbytes + 5;
-  const uint32_t vK = varint_size(K);
-  const uint64_t E = vK + K + 8;
-  const uint32_t nb = eb - fb;
-  const uint64_t ibody = (uint64_t)nb * E + 4;  // entries ∥ count
-  const bool ismall = ibody <= (uint64_t)kMetaBuf;
-  uint8_t* ib = ismall ? buf : fout + data + flen;
-  for (uint32_t i = tid; i < nb; i += kMetaThreads) {
-    const uint32_t b = fb + i;
-    uint8_t* p = ib + (uint64_t)i * E;
-    put_varint(p, K);
-    const Rec<W> last = a.rec[(uint64_t)a.blk_first[b] + a.blk_n[b] - 1];
-    put_key_tail<W>(p + vK, last, L, 0);
-    put_u32(p + vK + K, (uint32_t)(a.blk_pos[b] - a.blk_pos[fb]));
-    put_u32(p + vK + K + 4, a.blk_size[b]);
-  }
-  if (tid == 0) put_u32(ib + (uint64_t)nb * E, nb);
-  __syncthreads();
-  if (!ismall) __threadfence();
-  __syncthreads();
-  const uint32_t icrc = ismall ? cta_crc32_smem(ib, (uint32_t)ibody, cs, red)
-                               : cta_crc32_global(ib, ibody, cs, buf, red);
-  if (ismall) coop_copy(fout + data + flen, ib, ibody, tid, kMetaThreads);
-  if (tid == 0) {
-    put_u32(fout + data + flen + ibody, icrc);
-    // footer <IIIIQ>: filter_off, filter_len, index_off, index_len, magic
-    uint8_t* ft = fout + a.sst_size[s] - 24;
-    put_u32(ft, (uint32_t)data);
-    put_u32(ft + 4, (uint32_t)flen);
-    put_u32(ft + 8, (uint32_t)(data + flen));
-    put_u32(ft + 12, (uint32_t)(ibody + 4));
-    put_u32(ft + 16, (uint32_t)kMagic);
-    put_u32(ft + 20, (uint32_t)(kMagic >> 32));
-  }
-  // smallest / largest internal keys
-  if (tid < 2 && ne > 0) {
-    const Rec<W> r = a.rec[tid == 0 ? fe : fe + ne - 1];
-    put_key_tail<W>(a.sst_keys + ((uint64_t)s * 2 + tid) * K, r, L, 0);
+    __syncthreads();
+    // ---- filter block: bits ∥ k ∥ crc ----
+    uint8_t* fb8 = reinterpret_cast<uint8_t*>(bits);
+    if (tid == 0) fb8[nbytes] = (uint8_t)a.kprobes;
+    __syncthreads();
+    const uint32_t fcrc = small ? cta_crc32_smem(fb8, (uint32_t)(nbytes + 1), cs, red)
+                                : cta_crc32_global(fb8, nbytes + 1, cs, buf, red);
+    coop_copy(fout + data, fb8, nbytes + 1, tid, kMetaThreads);
+    if (tid == 0) put_u32(fout + data + nbytes + 1, fcrc);
+    __syncthreads();
+    // ---- index block ----
+    const uint64_t flen = nbytes + 5;
+    const uint32_t vK = varint_size(K);
+    const uint64_t E = vK + K + 8;
+    const uint32_t nb = eb - fb;
+    const uint64_t ibody = (uint64_t)nb * E + 4;  // entries ∥ count
+    const bool ismall = ibody <= (uint64_t)kMetaBuf;
+    uint8_t* ib = ismall ? buf : fout + data + flen;
+    for (uint32_t i = tid; i < nb; i += kMetaThreads) {
+      const uint32_t b = fb + i;
+      uint8_t* p = ib + (uint64_t)i * E;
+      put_varint(p, K);
+      const Rec<W> last = a.rec[(uint64_t)a.blk_first[b] + a.blk_n[b] - 1];
+      put_key_tail<W>(p + vK, last, L, 0);
+      put_u32(p + vK + K, (uint32_t)(a.blk_pos[b] - a.blk_pos[fb]));
+      put_u32(p + vK + K + 4, a.blk_size[b]);
+    }
+    if (tid == 0) put_u32(ib + (uint64_t)nb * E, nb);
+    __syncthreads();
+    if (!ismall) __threadfence();
+    __syncthreads();
+    const uint32_t icrc = ismall ? cta_crc32_smem(ib, (uint32_t)ibody, cs, red)
+                                 : cta_crc32_global(ib, ibody, cs, buf, red);
+    if (ismall) coop_copy(fout + data + flen, ib, ibody, tid, kMetaThreads);
+    if (tid == 0) {
+      put_u32(fout + data + flen + ibody, icrc);
+      // footer <IIIIQ>: filter_off, filter_len, index_off, index_len, magic
+      uint8_t* ft = fout + a.sst_size[s] - 24;
+      put_u32(ft, (uint32_t)data);
+      put_u32(ft + 4, (uint32_t)flen);
+      put_u32(ft + 8, (uint32_t)(data + flen));
+      put_u32(ft + 12, (uint32_t)(ibody + 4));
+      put_u32(ft + 16, (uint32_t)kMagic);
+      put_u32(ft + 20, (uint32_t)(kMagic >> 32));
+    }
+    // smallest / largest internal keys
+    if (tid < 2 && ne > 0) {
+      const Rec<W> r = a.rec[tid == 0 ? fe : fe + ne - 1];
+      put_key_tail<W>(a.sst_keys + ((uint64_t)s * 2 + tid) * K, r, L, 0);
+    }
+    __syncthreads();  // buf is reused by the next SST
   }
 }
 
