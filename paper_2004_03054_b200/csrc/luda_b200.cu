@@ -28,6 +28,7 @@
 #include "../../include/luda_b200.h"
 #include "luda_common.cuh"
 #include "luda_decode.cuh"
+#include "luda_dispatch.cuh"
 #include "luda_encode.cuh"
 #include "luda_merge.cuh"
 #include "luda_parse.cuh"
@@ -758,7 +759,9 @@ int luda_shutdown(void) {
 }
 
 int luda_region_alloc(uint64_t nbytes, void** dev_ptr) {
+  // regions start zero-filled like the reference's shared-memory regions
   CK(cudaMalloc(dev_ptr, std::max<uint64_t>(nbytes, 1) + 512));
+  CK(cudaMemset(*dev_ptr, 0, std::max<uint64_t>(nbytes, 1) + 512));
   return LUDA_OK;
 }
 int luda_region_free(void* p) {
@@ -920,10 +923,59 @@ int luda_build_from_sorted(const uint8_t* keys, uint32_t L, const uint64_t* trai
 int luda_dispatch(int kind, const int64_t* items, uint32_t n_items, void* const* region_ptr,
                   const uint64_t* region_cap, uint32_t n_regions, int64_t* results, int64_t* fail_item,
                   void* stream) {
-  (void)kind; (void)items; (void)n_items; (void)region_ptr; (void)region_cap; (void)n_regions; (void)results;
-  (void)stream;
-  *fail_item = 0;
-  return fail(LUDA_DEVICE, "luda_dispatch: not implemented yet");
+  static const uint32_t kCols[4] = {9, 6, 10, 7};
+  static const uint32_t kRcols[4] = {4, 1, 2, 1};
+  *fail_item = -1;
+  if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
+  if (kind < 0 || kind > 3) return fail(LUDA_DEVICE, "unknown kernel kind");
+  if (n_items == 0) return LUDA_OK;
+  std::lock_guard<std::mutex> lock(g_job_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch scratch(st);
+  const uint32_t cols = kCols[kind], rcols = kRcols[kind];
+  GET(d_items, int64_t, (uint64_t)n_items * cols, false);
+  GET(d_ptr, uint8_t*, std::max<uint32_t>(n_regions, 1), false);
+  GET(d_cap, uint64_t, std::max<uint32_t>(n_regions, 1), false);
+  GET(d_res, int64_t, (uint64_t)n_items * rcols, true);
+  GET(d_status, uint32_t, n_items, false);
+  GET(d_msg, uint32_t, n_items, false);
+  GET(d_off, int64_t, n_items, false);
+  CK(cudaMemcpyAsync(d_items, items, 8ull * n_items * cols, cudaMemcpyHostToDevice, st));
+  if (n_regions) {
+    CK(cudaMemcpyAsync(d_ptr, region_ptr, sizeof(void*) * n_regions, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_cap, region_cap, 8ull * n_regions, cudaMemcpyHostToDevice, st));
+  }
+  DispatchArgs da{kind, d_items, n_items, cols, d_ptr, d_cap, n_regions, d_res, rcols, d_status, d_msg, d_off};
+  const size_t sm = sizeof(CrcSmem) + (size_t)kDispWarps * (kDispStage + 256);
+  CK(cudaFuncSetAttribute(dispatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  const unsigned grid = (unsigned)std::min<uint64_t>((n_items + kDispWarps - 1) / kDispWarps, 2ull * g_num_sms);
+  dispatch_kernel<<<grid, kDispWarps * 32, sm, st>>>(da);
+  ++g_launches;
+  CK(cudaGetLastError());
+  std::vector<uint32_t> hst(n_items), hmsg(n_items);
+  std::vector<int64_t> hoff(n_items);
+  CK(cudaMemcpyAsync(results, d_res, 8ull * n_items * rcols, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hst.data(), d_status, 4ull * n_items, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hmsg.data(), d_msg, 4ull * n_items, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hoff.data(), d_off, 8ull * n_items, cudaMemcpyDeviceToHost, st));
+  int rc = sync(st);
+  if (rc) return rc;
+  static const char* kMsg[] = {"ok", "block too short", "data block checksum mismatch", "bad restart array",
+                               "truncated varint", "varint too long", "truncated block entry",
+                               "trailing garbage in block entries", "BufferError: pair slot overflow",
+                               "BufferError: tuple slot overflow", "error: ushort format requires 0 <= number <= 65535",
+                               "region range outside the dispatch's regions",
+                               "ValueError: restart_interval must be >= 1", "BufferError: encode slot overflow",
+                               "BufferError: filter slot overflow", "ValueError: bits_per_key must be >= 1",
+                               "error: tuple runs past its region"};
+  for (uint32_t i = 0; i < n_items; ++i) {
+    if (hst[i] == D_OK) continue;
+    *fail_item = i;  // first failing item in dispatch order (device.py:445-447, 589-591)
+    const char* m = hmsg[i] < sizeof(kMsg) / sizeof(kMsg[0]) ? kMsg[hmsg[i]] : "error";
+    if (hst[i] == D_CORRUPT) return fail(LUDA_CORRUPT, m, hoff[i]);
+    return fail(LUDA_DEVICE, m);
+  }
+  return LUDA_OK;
 }
 
 int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {

@@ -179,6 +179,7 @@ __global__ void parse_files_a(ParseArgs a) {
 // Z_{4352 q}(pass raw); the XOR over all passes of a range is its raw
 // register with the ~0 preset folded in (the staged copy is prepared:
 // bytes before the range are zeroed, its first 4 bytes complemented).
+template <bool kCg = false>
 __device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint64_t n, uint64_t q,
                                                          uint8_t* stage, const CrcSmem& cs) {
   const uint32_t lane = lane_id();
@@ -196,7 +197,7 @@ __device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint6
   for (uint32_t c = lane; c < nchunks; c += 32) {
     const uintptr_t ad = w0 + 16ull * c;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (ad >= l0 && ad < l1) v = *reinterpret_cast<const uint4*>(ad);
+    if (ad >= l0 && ad < l1) v = kCg ? __ldcg(reinterpret_cast<const uint4*>(ad)) : *reinterpret_cast<const uint4*>(ad);
     reinterpret_cast<uint4*>(stage)[c] = v;
   }
   __syncwarp();
