@@ -570,14 +570,20 @@ def merge_resolve(runs, deeper=()):
 
 
 def reference_compact(files, *, deeper=(), block_size=4096, restart_interval=16,
-                      bits_per_key=10, sst_size_target=4 * 2**20):
+                      bits_per_key=10, sst_size_target=4 * 2**20, key_range=None):
     """Compact input files (bytes, lower first then upper) into output SSTs.
 
     Returns a list of (sst_bytes, smallest_ikey, largest_ikey) in key order.
+    ``key_range=(lo, hi)`` (None = open end) keeps user keys in [lo, hi): the
+    per-range reference of a subcompaction.
     """
     opened = [open_table(f) for f in files]          # all footers/filters/indexes first
     runs = [list(scan_table(f, idx)) for f, (_, idx) in zip(files, opened)]
     survivors = merge_resolve(runs, deeper)
+    if key_range is not None:
+        lo, hi = key_range
+        survivors = (kv for kv in survivors
+                     if (lo is None or ukey(kv[0]) >= lo) and (hi is None or ukey(kv[0]) < hi))
     return build_tables_split(survivors, block_size=block_size,
                               restart_interval=restart_interval,
                               bits_per_key=bits_per_key, sst_size_target=sst_size_target)

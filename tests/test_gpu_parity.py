@@ -145,3 +145,21 @@ def test_format_errors(dev, mutate, exc):
         O.reference_compact(lower + upper)
     with pytest.raises(getattr(P, exc)):
         gpu_compact(dev, job, lower, upper, {})
+
+
+def test_subcompactions_match_per_range_oracle(dev):
+    """Key-range subcompactions on the GPU vs the per-range
+    reference compaction, byte for byte, range by range."""
+    from paper_2004_03054_b200 import subcompact as SC
+    from paper_2004_03054_b200.config import StoreConfig
+    from tests.test_subcompact import job_with_inputs
+    job, inputs = job_with_inputs()
+    cfg = StoreConfig(sst_size_target=64 * 1024)
+    plan, res = SC.run_subcompactions(job, dev, inputs=inputs, config=cfg, nranges=8)
+    assert len(res) == len(plan.ranges) > 1
+    for r, outs, _ in res:
+        lo, hi = plan.ranges[r]
+        sub = SC.range_job(job, lo, hi)
+        want = O.reference_compact([inputs[m.file_id] for m in sub.lower + sub.upper],
+                                   sst_size_target=64 * 1024, key_range=(lo, hi))
+        assert [o[0] for o in outs] == [w[0] for w in want], r
