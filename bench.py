@@ -108,7 +108,7 @@ class Workload:
     pass
 
 
-def synth_c3(n_keys, seed, device_index, del_frac=0.2, vlen=128, klen=16, sst_target=MIB4):
+def synth_c3(n_keys, seed, device_index, del_frac=0.2, vlen=128, klen=16, sst_target=MIB4, shard=0, nshards=1):
     import torch
 
     from paper_2004_03054_b200 import _native
@@ -118,13 +118,23 @@ def synth_c3(n_keys, seed, device_index, del_frac=0.2, vlen=128, klen=16, sst_ta
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     n = n_keys
-    # sorted distinct 16-byte keys: sorted random 64-bit prefix (sign-flipped → unsigned order) + random suffix
+    # sorted distinct 16-byte keys: sorted random 64-bit prefix (sign-flipped → unsigned order) + random suffix.
+    # With nshards > 1 (multi-GPU weak scaling) the prefix's top log2(nshards) bits are the shard index, so the
+    # ranks hold disjoint key ranges of one global job.
+    b = nshards.bit_length() - 1
+    assert 1 << b == nshards
     while True:
         hi = torch.randint(-2**63, 2**63 - 1, (n,), generator=g, device=dev, dtype=torch.int64)
+        if b:
+            hi = (hi >> b) & ((1 << (64 - b)) - 1)   # logical shift: [0, 2^(64-b)), sorts as signed == unsigned
         hi, _ = torch.sort(hi)
         if bool((hi[1:] != hi[:-1]).all()):
             break
-    hi = hi ^ torch.tensor(-2**63, dtype=torch.int64, device=dev)
+    if b:
+        prefix = shard << (64 - b)
+        hi = hi | (prefix - 2**64 if prefix >= 2**63 else prefix)
+    else:
+        hi = hi ^ torch.tensor(-2**63, dtype=torch.int64, device=dev)
     lo = torch.randint(-2**63, 2**63 - 1, (n,), generator=g, device=dev, dtype=torch.int64)
     words = torch.stack([hi, lo], 1).contiguous()
     keys = words.view(torch.uint8).view(n, 2, 8).flip(2).reshape(n * 16).contiguous()
@@ -182,6 +192,78 @@ def synth_c3(n_keys, seed, device_index, del_frac=0.2, vlen=128, klen=16, sst_ta
     del values, keys, words, hi, lo, tr_up, tr_lo, voff_up, voff_lo, vlen_up, vlen_lo, is_del, idx
     torch.cuda.empty_cache()
     return w
+
+
+def _d2h(L, dptr, n):
+    buf = (ctypes.c_uint8 * n)()
+    from paper_2004_03054_b200 import _native
+    _native.check(L.luda_stage_out_async(ctypes.addressof(buf), dptr, n, None))
+    _native.check(L.luda_stream_sync(None))
+    return bytes(buf)
+
+
+def plan_subcompaction(w, L, rank, world, n_keys, per_file=1):
+    """The §8e plan with P = world ranges (weak scaling: one range per GPU).
+    Host-cached SST metadata (footer + index block + first key of each local
+    file) → samples → NCCL all-gather → splitters; returns this rank's range
+    and the wall time of the plan (reported, not in the timed steps)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2004_03054_b200 import subcompact as SC
+    base = w.arena.data_ptr()
+    idx_keys, upper_first = [], []
+    for i, (off, ln) in enumerate(zip(w.file_off, w.file_len)):
+        foot = _d2h(L, base + off + ln - 24, 24)
+        _, _, ioff, ilen, _ = SC.FOOTER.unpack(foot)
+        blob = _d2h(L, base + off + ioff, ilen)
+        fake = blob + SC.FOOTER.pack(0, 0, 0, ilen, 0)  # footer pointing at the index copy
+        keys = SC.index_user_keys(fake)
+        idx_keys.append(keys)
+        if i >= w.n_lower:  # Li+1 file: smallest user key from the first entry of its first block
+            head = _d2h(L, base + off, 64)
+            pos = 0
+            shared, pos = SC._varint(head, pos)
+            unshared, pos = SC._varint(head, pos)
+            _, pos = SC._varint(head, pos)
+            upper_first.append(head[pos:pos + unshared][:unshared - 8])
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    local = []
+    for keys in idx_keys:
+        step = max(1, len(keys) // per_file)
+        local += keys[::step][:per_file]
+    nfiles = torch.tensor([len(w.file_off)], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(nfiles, op=dist.ReduceOp.MAX)
+    rows = int(nfiles.item()) * per_file
+    samples = [k for g in SC.allgather_bytes(SC.encode_samples(local, rows), world) for k in SC.decode_samples(g)]
+    bnd_rows = int(nfiles.item())
+    gathered_b = SC.allgather_bytes(SC.encode_samples(upper_first, bnd_rows), world)
+    boundaries = [k for g in gathered_b for k in SC.decode_samples(g)]
+    first_of_rank = [SC.decode_samples(g)[0] for g in gathered_b]
+    spl = SC.choose_splitters(samples, sorted(boundaries)[1:], world)
+    rng = SC.ranges_from_splitters(spl)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    aligned = len(rng) == world and all(rng[r][0] == (None if r == 0 else first_of_rank[r]) for r in range(world))
+    if aligned:
+        lo, hi = rng[rank]
+    else:  # ranges must match the locally held shard in this device-resident benchmark
+        lo = None if rank == 0 else first_of_rank[rank]
+        hi = None if rank == world - 1 else first_of_rank[rank + 1]
+    return {"lo": lo, "hi": hi, "aligned": aligned, "plan_ms": plan_ms, "samples": len(samples),
+            "splitters": len(spl)}
+
+
+def set_range(desc, lo, hi):
+    from paper_2004_03054_b200 import _native
+    keep = []
+    for name, key in (("range_lo", lo), ("range_hi", hi)):
+        if key is not None:
+            kb = (ctypes.c_uint8 * len(key)).from_buffer_copy(key)
+            keep.append(kb)
+            setattr(desc, name, ctypes.cast(kb, _native.c_u8p))
+            setattr(desc, name + "_len", len(key))
+    return keep
 
 
 def job_desc(w, arena_ptr):
@@ -292,14 +374,26 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; BENCH_DIST_BACKEND=gloo lets a multi-rank run share one GPU (functional test only)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2004_03054_b200 import _native
     L = _native.lib(local)
-    w = synth_c3(args.keys, seed=0xC3 + 7919 * rank, device_index=local)
+    w = synth_c3(args.keys, seed=0xC3 + 7919 * rank, device_index=local, shard=rank, nshards=world)
     desc, keep = job_desc(w, w.arena.data_ptr())
     st = w.stream
+    plan = None
+    if world > 1:
+        # Subcompaction plan of the global job: index-key samples of the local files,
+        # NCCL all-gather, splitters snapped to Li+1 file boundaries; this rank compacts range `rank`.
+        plan = plan_subcompaction(w, L, rank, world, args.keys)
+        keep = list(keep) + [set_range(desc, plan["lo"], plan["hi"])]
 
     def one_step():
         res = _native.JobResult()
@@ -343,7 +437,7 @@ def main():
     _native.check(L.luda_event_elapsed_ms(ev0.value, ev1.value, ctypes.byref(ms)))
     t_step = ms.value / args.steps
     if world > 1:
-        tt = torch.tensor([t_step], device="cuda")
+        tt = torch.tensor([t_step], device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dist.barrier()
         t_step = float(tt.item())
@@ -359,6 +453,8 @@ def main():
         _native.check(L.luda_stream_sync(st))
         arena2 = torch.empty(w.total, dtype=torch.uint8, device="cuda")
         desc2, keep2 = job_desc(w, arena2.data_ptr())
+        if plan is not None:
+            keep2 = list(keep2) + [set_range(desc2, plan["lo"], plan["hi"])]
         s_lo, s_up, s_o = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         for sp in (s_lo, s_up, s_o):
             _native.check(L.luda_stream_create(ctypes.byref(sp)))
@@ -388,7 +484,7 @@ def main():
             L.luda_job_release(ctypes.byref(res))
         dt = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
-            tt = torch.tensor([dt], device="cuda")
+            tt = torch.tensor([dt], device="cuda" if backend == "nccl" else "cpu")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
         e2e = {"value": round(world * w.s_in / dt / 1e6, 3), "unit": "MB/s", "h2d_bytes_per_step": w.total,
@@ -433,10 +529,15 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "MB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": CONFIGS["c3"], "keys_per_run": args.keys, "n_in": n_in, "n_out": n_out,
+        "config": {"workload": CONFIGS["c3"] if world == 1 else
+                   CONFIGS["c3"].replace(", 1 B200", "") + f" per GPU; global job = {world} key-range shards "
+                   f"(5th BASELINE config's subcompaction scheme)", "keys_per_run": args.keys, "n_in": n_in, "n_out": n_out,
                    "input_bytes": s_in, "output_bytes": int(s_out), "input_ssts": len(w.file_off),
                    "output_ssts": int(n_sst), "block_size": 4096, "sst_size_target": MIB4,
-                   "l2": "inputs (%.1f GB) larger than L2; no flush" % (s_in / 1e9)},
+                   "l2": "inputs (%.1f GB) larger than L2; no flush" % (s_in / 1e9),
+                   "parallelism": f"key-range subcompactions x{world}" if world > 1 else "1 GPU",
+                   "subcompaction_plan": None if plan is None else {
+                       k: (v.hex() if isinstance(v, bytes) else v) for k, v in plan.items()}},
         "keys_per_s": round(world * n_in / (t_step * 1e-3), 1),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(ach / hbm, 4), "traffic": None, "peak_kind": peak_kind,
