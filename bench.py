@@ -294,48 +294,60 @@ def _cpu_sample_job(n_keys, seed):
     return lower + upper
 
 
-def _cpu_worker(args):
-    n_keys, seed, reps = args
+_CPU_FILES = None
+
+
+def _cpu_init(n_keys, seed):
+    """Pool initializer: each worker builds its own c3-shaped input once (untimed)."""
+    global _CPU_FILES
+    import multiprocessing as mp
+    ident = mp.current_process()._identity
+    _CPU_FILES = _cpu_sample_job(n_keys, seed + (ident[0] if ident else 0))
+
+
+def _cpu_compact(_):
     from oracle import luda_oracle as O
-    files = _cpu_sample_job(n_keys, seed)
     t0 = time.perf_counter()
-    for _ in range(reps):
-        O.reference_compact(files)
+    O.reference_compact(_CPU_FILES)
     dt = time.perf_counter() - t0
-    return sum(len(f) for f in files) * reps, dt, 2 * n_keys * reps
+    return sum(len(f) for f in _CPU_FILES), dt
 
 
-def cpu_baseline(n_keys=1 << 15, workers=1, reps=1, seed=0xC3):
-    """Oracle (pure-Python restatement of the reference) on a bounded c3-shaped
-    sample; `workers` independent processes = all host cores."""
+def cpu_baseline(n_keys=1 << 19, workers=1, reps=1, seed=0xC3):
+    """Oracle (pure-Python restatement of the reference, pinned to its golden
+    outputs) on a bounded c3-shaped sample of 2 x n_keys entries; `workers`
+    independent processes (one job each) = the host cores. Returns
+    (MB/s, keys/s, seconds of the slowest worker)."""
     if workers <= 1:
-        b, dt, k = _cpu_worker((n_keys, seed, reps))
-        return b / dt / 1e6, k / dt, dt
+        _cpu_init(n_keys, seed)
+        b, dt = _cpu_compact(0)
+        return b / dt / 1e6, 2 * n_keys / dt, dt
     import multiprocessing as mp
     ctx = mp.get_context("fork")
-    with ctx.Pool(workers) as pool:
-        # build the inputs in the workers first (untimed), then time the compactions
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, [(n_keys, seed + i, reps) for i in range(workers)])
-        wall = time.perf_counter() - t0
-    tot_b = sum(r[0] for r in res)
-    tot_k = sum(r[2] for r in res)
+    with ctx.Pool(workers, initializer=_cpu_init, initargs=(n_keys, seed)) as pool:
+        res = pool.map(_cpu_compact, range(workers), chunksize=1)
     t_max = max(r[1] for r in res)
-    return tot_b / t_max / 1e6, tot_k / t_max, wall
+    return sum(r[0] for r in res) / t_max / 1e6, 2 * n_keys * workers / t_max, t_max
 
 
 def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port) on all host
+    cores, one c3-shaped job per core built once; each step = one compaction
+    per worker, throughput = bytes of all workers / slowest worker."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cores = len(os.sched_getaffinity(0))
     n_keys = args.cpu_keys
-    # warmup: one small job per worker (imports, allocator)
-    cpu_baseline(n_keys=1024, workers=cores, reps=1)
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
     vals = []
-    for _ in range(args.steps):
-        mbps, keys_s, _ = cpu_baseline(n_keys=n_keys, workers=cores, reps=1)
-        vals.append((mbps, keys_s))
+    with ctx.Pool(cores, initializer=_cpu_init, initargs=(n_keys, 0xC3)) as pool:
+        for i in range(args.warmup + args.steps):
+            res = pool.map(_cpu_compact, range(cores), chunksize=1)
+            t_max = max(r[1] for r in res)
+            if i >= args.warmup:
+                vals.append((sum(r[0] for r in res) / t_max / 1e6, 2 * n_keys * cores / t_max))
     mbps = statistics.median(v[0] for v in vals)
     keys_s = statistics.median(v[1] for v in vals)
     sample = f"c3-shaped job of 2x{n_keys} entries (16B/128B, 20% deletes) per worker, {cores} workers"
@@ -362,7 +374,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--keys", type=int, default=1 << 25, help="distinct keys per run (c3: 2^25 → 64M entries)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-keys", type=int, default=1 << 14)
+    ap.add_argument("--cpu-keys", type=int, default=1 << 17,
+                    help="reference arm: distinct keys per run of each worker's c3-shaped job")
+    ap.add_argument("--cpu-baseline-keys", type=int, default=1 << 19,
+                    help="cpu_baseline: distinct keys per run of the single-core c3-shaped sample (~10-30 s)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -518,12 +533,22 @@ def main():
     dom = max(kern, key=lambda k: kern[k][1])
     db, dt_ = kern[dom]
     ach = db / (dt_ * 1e-3) / 1e9
+    traffic, traffic_src = None, None
+    try:  # measured DRAM bytes per launch of that kernel (one ncu --set full capture, profiles/traffic.json)
+        tj = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
+        kname = {"decode": "decode_kernel", "merge_resolve": "merge_kernel", "encode": "encode_kernel",
+                 "sst_meta": "sst_meta_kernel", "block_plan": "block_jump_kernel"}[dom]
+        if kname in tj:
+            traffic, traffic_src = tj[kname]["dram_bytes"], tj[kname]["source"]
+    except Exception:
+        pass
     cpu = None
     if not args.no_cpu and world == 1 or (not args.no_cpu and rank == 0):
-        mbps, keys_s, wall = cpu_baseline(n_keys=args.cpu_keys, workers=1)
+        mbps, keys_s, wall = cpu_baseline(n_keys=args.cpu_baseline_keys, workers=1)
         cpu = {"value": round(mbps, 4), "unit": "MB/s", "cores": 1, "kind": "port",
-               "sample": f"oracle (pure-Python restatement of the reference) on a c3-shaped job of 2x{args.cpu_keys} "
-                         f"entries, {wall:.1f}s", "keys_per_s": round(keys_s, 1)}
+               "sample": f"oracle (the reference algorithm restated in Python+zlib+numpy, pinned to the reference's "
+                         f"golden outputs) on a c3-shaped job of 2x{args.cpu_baseline_keys} entries (16B/128B, "
+                         f"20% deletes): {wall:.1f}s of compaction", "keys_per_s": round(keys_s, 1)}
     value = world * s_in / (t_step * 1e-3) / 1e6
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "MB/s", "n_gpus": world, "steps": args.steps,
@@ -540,7 +565,8 @@ def main():
                        k: (v.hex() if isinstance(v, bytes) else v) for k, v in plan.items()}},
         "keys_per_s": round(world * n_in / (t_step * 1e-3), 1),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(ach / hbm, 4), "traffic": None, "peak_kind": peak_kind,
+                     "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind,
                      "alg_bytes_per_launch": db},
         "job_roofline": {"alg_bytes": b_alg, "achieved": round(b_alg / (t_step * 1e-3) / 1e9, 1), "peak": hbm,
                          "frac": round(b_alg / (t_step * 1e-3) / 1e9 / hbm, 4),

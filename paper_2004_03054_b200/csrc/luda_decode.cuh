@@ -149,19 +149,21 @@ __device__ __forceinline__ int32_t interval_walk(const uint8_t* d, uint32_t star
 // exactly at `end`.
 template <typename Emit>
 __device__ __forceinline__ int32_t interval_positions(const uint8_t* d, uint32_t start, uint32_t end, Emit emit) {
-  uint32_t pos = start;
+  // The chain is one byte-load latency + 3 integer ops per entry: the three
+  // header bytes that decide the next position are loaded independently
+  // straight from the running pointer (no alignment arithmetic before the
+  // loads): next = p + 3 + u + b2 + (b2 >> 7) * (128 b3 - 127).
+  const uint8_t* p = d + start;
+  const uint8_t* e = d + end;
   int32_t j = 0;
-  while (pos < end) {
-    const uint32_t w = ld_u32_any(d + pos);
-    emit(j, pos);
-    const uint32_t u = prmt(w, 0u, 0x4441u);
-    const uint32_t b2 = prmt(w, 0u, 0x4442u);
-    const uint32_t b3 = __umulhi(w, 0x100u);        // w >> 24
-    const uint32_t two = __umulhi(b2, 1u << 25);    // b2 >> 7
-    pos += 3u + u + b2 + two * (b3 * 128u - 127u);  // 2-byte: 4 + u + (b2 & 0x7F) + (b3 << 7)
+  while (p < e) {
+    const uint32_t u = p[1], b2 = p[2], b3 = p[3];
+    emit(j, (uint32_t)(p - d));
+    const uint32_t two = b2 >> 7;
+    p += (3u + u + b2) + two * (b3 * 128u - 127u);
     ++j;
   }
-  return pos == end ? j : -1;
+  return p == e ? j : -1;
 }
 
 // Exact sequential decode_data_block walk (blocks.py:151-164). Returns the
@@ -215,10 +217,26 @@ struct DecState {
 };
 
 // Phase 1: structural checks + entry walk (counts; single-walk fills slots).
+#ifdef DEC_TIMING
+__device__ unsigned long long g_dec_t[16];
+#define DEC_T(i)                                                              \
+  do {                                                                        \
+    __syncwarp();                                                             \
+    const unsigned long long t_ = clock64();                                  \
+    if (lane_id() == 0) atomicAdd(&g_dec_t[i], t_ - t_last);                  \
+    t_last = t_;                                                              \
+  } while (0)
+#define DEC_T0() unsigned long long t_last = clock64()
+#else
+#define DEC_T(i) do {} while (0)
+#define DEC_T0() do {} while (0)
+#endif
+
 template <int W>
 __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t b, uint64_t addr, uint32_t blen,
                                                const uint8_t* d, DecSlot* slots) {
   const uint32_t lane = lane_id();
+  DEC_T0();
   DecState st{};
   st.len = blen;
   st.addr = addr;
@@ -242,6 +260,7 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
         st.my_en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint32_t)entries_end;
         ok = (lane != 0 || st.my_st == 0) && st.my_st < st.my_en && (int64_t)st.my_en <= entries_end;
       }
+      DEC_T(0);
       bool fast = false;
       if (single) {
         // Positions-only walk (lane per interval), then every entry header is
@@ -253,6 +272,7 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
           });
           ok = st.my_cnt >= 0 && st.my_cnt <= kDecStride;
         }
+        DEC_T(1);
         if (__all_sync(0xFFFFFFFFu, ok)) {
           __syncwarp();
           uint32_t bad = 0;
@@ -275,6 +295,7 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
           fast = !__any_sync(0xFFFFFFFFu, bad != 0);
           __syncwarp();
           if (fast) st.mode = 1;
+          DEC_T(2);
         }
       }
       if (!fast) {
@@ -295,6 +316,7 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
         st.my_pre = incl - c;
         st.n = (uint64_t)(uint32_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
       }
+      DEC_T(3);
     }
     if (st.mode == 3) {
       uint64_t nn = 0;
@@ -435,6 +457,7 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
 // Z_{-pad}, and the ~0 preset is added back as Z_n(~0) (g_zone table).
 __device__ __forceinline__ uint32_t dec_crc_staged(uint8_t* win, uint8_t* data, uint32_t n, const CrcSmem& cs) {
   const uint32_t lane = lane_id();
+  const uint32_t zone = crc_zone(n);  // global load issued first: its latency hides under the passes
   const uint32_t pre = (uint32_t)(data - win);
   if (lane < pre) win[lane] = 0;
   const uint32_t pad = (uint32_t)(0u - (uint32_t)reinterpret_cast<uintptr_t>(data + n)) & 3u;
@@ -449,7 +472,7 @@ __device__ __forceinline__ uint32_t dec_crc_staged(uint8_t* win, uint8_t* data, 
     acc = (q == (int)npass - 1) ? v : (gf2_apply(c_zgroup, acc) ^ v);
   }
   if (pad) acc = crc_unshift(acc, pad);
-  return ~(acc ^ crc_zone(n));
+  return ~(acc ^ zone);
 }
 
 template <int W>
