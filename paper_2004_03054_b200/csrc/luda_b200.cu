@@ -494,8 +494,9 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(blk_out, uint64_t, nblk, false);
   block_out_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, sch.nodes, nsst, sst_off, blk_out);
   ++g_launches;
+  const uint32_t s_edbg = getenv("LUDA_ENC_DBG") ? (uint32_t)atoi(getenv("LUDA_ENC_DBG")) : 0u;
   EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off,
-                   blk_out, res->out};
+                   blk_out, res->out, s_edbg};
   const size_t esm = sizeof(CrcSmem) + (size_t)kEncWarps * kEncWarpBytes;
   CK(cudaFuncSetAttribute(encode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
   const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncWarps - 1) / kEncWarps, (uint64_t)g_num_sms);

@@ -215,6 +215,7 @@ struct DecState {
   int32_t my_cnt, my_pre;
   uint32_t my_st, my_en;
 };
+constexpr int kDecSlotIntervals = (kDecSlots * 2) / kDecStride;  // intervals the mode-1 slot layout holds
 
 // Phase 1: structural checks + entry walk (counts; single-walk fills slots).
 #ifdef DEC_TIMING
@@ -254,7 +255,7 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
     const int64_t entries_end = st.entries_end;
     if (nres <= 32) {
       bool ok = true;
-      const bool single = nres <= (uint32_t)(kDecSlots / kDecStride);
+      const bool single = nres <= (uint32_t)kDecSlotIntervals;
       if (lane < nres) {
         st.my_st = ld_u32_le(d + entries_end + 4 * lane);
         st.my_en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint32_t)entries_end;
@@ -263,39 +264,21 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
       DEC_T(0);
       bool fast = false;
       if (single) {
-        // Positions-only walk (lane per interval), then every entry header is
-        // validated and decoded in parallel (lane per entry).
+        // Positions-only walk (lane per interval) into the slot layout
+        // [interval][<= 16 entries]; the headers are validated and decoded by
+        // lane per entry in phase 2 (mode 1), before anything is written.
+        uint32_t* pos32 = reinterpret_cast<uint32_t*>(slots);
         if (lane < nres && ok) {
-          DecSlot* mine = slots + kDecStride * lane;
+          uint32_t* mine = pos32 + kDecStride * lane;
           st.my_cnt = interval_positions(d, st.my_st, st.my_en, [&](int32_t j, uint32_t pos) {
-            if (j < kDecStride) mine[j].pos = pos;
+            if (j < kDecStride) mine[j] = pos;
           });
           ok = st.my_cnt >= 0 && st.my_cnt <= kDecStride;
         }
         DEC_T(1);
         if (__all_sync(0xFFFFFFFFu, ok)) {
-          __syncwarp();
-          uint32_t bad = 0;
-          for (uint32_t i0 = 0; i0 < kDecStride * nres; i0 += 32) {
-            const uint32_t i = i0 + lane;
-            const uint32_t k = i >> 4, j = i & (kDecStride - 1);
-            const int32_t ck = __shfl_sync(0xFFFFFFFFu, st.my_cnt, k < 32 ? k : 31);
-            if (k < nres && (int32_t)j < ck) {
-              const uint32_t pos = slots[i].pos;
-              const uint32_t w = ld_u32_any(d + pos);
-              const uint32_t sh = w & 0xFFu;
-              const uint32_t u = prmt(w, 0u, 0x4441u);
-              const uint32_t v1 = prmt(w, 0u, 0x4442u);
-              const uint32_t two = (w >> 23) & 1u;
-              const uint32_t vl = two ? ((v1 & 0x7Fu) | ((w >> 17) & 0x7F80u)) : v1;
-              bad |= (w & 0x8080u) | (two & (w >> 31)) | ((sh + u) ^ K) | (j == 0 ? sh : 0u);
-              slots[i] = DecSlot{pos + 3u + two, (vl << 8) | sh};
-            }
-          }
-          fast = !__any_sync(0xFFFFFFFFu, bad != 0);
-          __syncwarp();
-          if (fast) st.mode = 1;
-          DEC_T(2);
+          fast = true;
+          st.mode = 1;
         }
       }
       if (!fast) {
@@ -310,11 +293,13 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
         }
         if (__all_sync(0xFFFFFFFFu, ok)) st.mode = 2;
       }
-      if (st.mode != 3) {
+      if (st.mode == 2) {
         const int32_t c = lane < nres ? st.my_cnt : 0;
         const int32_t incl = warp_incl_scan<int32_t>(c);
         st.my_pre = incl - c;
         st.n = (uint64_t)(uint32_t)__shfl_sync(0xFFFFFFFFu, incl, 31);
+      } else if (st.mode == 1) {
+        st.n = __reduce_add_sync(0xFFFFFFFFu, lane < nres ? (uint32_t)st.my_cnt : 0u);
       }
       DEC_T(3);
     }
@@ -330,6 +315,104 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
     }
   }
   return st;
+}
+
+// Mode-1 records. Lane i of chunk q owns slot (interval 2q + i/16, entry
+// i%16): restart entries have shared == 0, so a lane's shared prefix always
+// comes from lanes of its own interval at or below it, and byte j of an entry
+// is written by the LAST lane <= it whose shared <= j — one ballot per
+// prefix byte, no scan, no carry between chunks (each starts at a restart).
+// Headers are validated (canonical form, shared + unshared == K) before any
+// record is written; returns false (nothing written) if one is not.
+template <int W>
+__device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const DecState& st, uint64_t base,
+                                                 const uint8_t* d, const uint32_t* pos32) {
+  constexpr int NW = 2 * W + 2;
+  const uint32_t lane = lane_id();
+  const uint32_t K = a.K, L = K - 8;
+  const uint32_t nres = st.nres;
+  const uint32_t nchunks = (nres + 1) / 2;
+  const uint32_t lt = (1u << lane) - 1u;
+  auto slot = [&](uint32_t q, uint32_t& pos, uint32_t& w, uint32_t& j) -> bool {
+    const uint32_t k = 2 * q + (lane >> 4);
+    j = lane & 15u;
+    const int32_t ck = __shfl_sync(0xFFFFFFFFu, st.my_cnt, k < 32 ? k : 31);
+    const bool act = k < nres && (int32_t)j < ck;
+    pos = act ? pos32[kDecStride * k + j] : 0u;
+    w = act ? ld_u32_any(d + pos) : 0u;
+    return act;
+  };
+  auto bad_of = [&](uint32_t w, uint32_t j) -> uint32_t {
+    const uint32_t s = w & 0xFFu, u = prmt(w, 0u, 0x4441u), two = (w >> 23) & 1u;
+    return (w & 0x8080u) | (two & (w >> 31)) | ((s + u) ^ K) | (j == 0 ? s : 0u);
+  };
+  if (nchunks > 1) {  // validate every chunk before the first record is written
+    uint32_t bad = 0;
+    for (uint32_t q = 0; q < nchunks; ++q) {
+      uint32_t pos, w, j;
+      if (slot(q, pos, w, j)) bad |= bad_of(w, j);
+    }
+    if (__any_sync(0xFFFFFFFFu, bad != 0)) return false;
+  }
+  uint64_t e0 = base;
+  for (uint32_t q = 0; q < nchunks; ++q) {
+    uint32_t pos, w, j;
+    const bool act = slot(q, pos, w, j);
+    if (nchunks == 1 && __any_sync(0xFFFFFFFFu, act && bad_of(w, j) != 0)) return false;
+    const uint32_t s = act ? (w & 0xFFu) : 0u;
+    const uint32_t two = (w >> 23) & 1u;
+    const uint32_t v1 = prmt(w, 0u, 0x4442u);
+    const uint32_t vl = two ? ((v1 & 0x7Fu) | ((w >> 17) & 0x7F80u)) : v1;
+    const uint32_t kpos = pos + 3u + two;  // key suffix
+    // key bytes [0, K) as LE words from V = key suffix - shared (prefix bytes are garbage until resolved)
+    uint32_t kw[NW];
+    {
+      const uint8_t* V = d + kpos - s;
+      const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(V) & 3u);
+      const uint32_t* wp = reinterpret_cast<const uint32_t*>(V - mis);
+      const uint32_t sh = mis * 8u;
+      uint32_t lo = act ? wp[0] : 0u;
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        const uint32_t hi = act ? wp[i + 1] : 0u;
+        kw[i] = __funnelshift_r(lo, hi, sh);
+        lo = hi;
+      }
+    }
+    const uint32_t smax = __reduce_max_sync(0xFFFFFFFFu, s);
+    uint32_t fixed[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) fixed[i] = kw[i];
+#pragma unroll
+    for (int wi = 0; wi < NW; ++wi) {
+      if ((uint32_t)(4 * wi) < smax) {  // warp-uniform; the 4 bytes of a word are independent (straight-line)
+        uint32_t src[4], sw[4];
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const uint32_t wm = __ballot_sync(0xFFFFFFFFu, act && s <= (uint32_t)(4 * wi + bb));
+          const uint32_t mine = wm & (lt | (1u << lane));
+          src[bb] = mine ? 31u - __clz(mine) : lane;
+        }
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) sw[bb] = __shfl_sync(0xFFFFFFFFu, kw[wi], src[bb]);
+        uint32_t f = fixed[wi];
+        f = s > (uint32_t)(4 * wi + 0) ? prmt(f, sw[0], 0x3214u) : f;
+        f = s > (uint32_t)(4 * wi + 1) ? prmt(f, sw[1], 0x3250u) : f;
+        f = s > (uint32_t)(4 * wi + 2) ? prmt(f, sw[2], 0x3610u) : f;
+        f = s > (uint32_t)(4 * wi + 3) ? prmt(f, sw[3], 0x7210u) : f;
+        fixed[wi] = f;
+      }
+    }
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, act);
+    if (act) {
+      Rec<W> r;
+      words_to_rec<W, NW>(fixed, L, r);
+      r.h = handle_pack(st.addr + kpos + (K - s), vl);
+      a.out[e0 + __popc(m & lt)] = r;
+    }
+    e0 += __popc(m);
+  }
+  return true;
 }
 
 // Phase 2 (parse warp): reference errors of the walk, then records at
@@ -353,15 +436,34 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   }
   if (a.dbg & 2) return;
   const uint32_t L = K - 8;
+  if (st.mode == 1) {
+    if (dec_fast_records<W>(a, st, base, d, reinterpret_cast<const uint32_t*>(slots))) return;
+    // a header outside the canonical form: the exact sequential path decides
+    uint64_t nn = 0;
+    uint32_t pc = 0, us = 0;
+    if (lane == 0)
+      pc = block_walk_exact(d, len - 4, (uint64_t)st.entries_end, K, nn, us,
+                            [](uint64_t, uint32_t, uint32_t, uint32_t) {});
+    st.n = __shfl_sync(0xFFFFFFFFu, nn, 0);
+    st.pcode = __shfl_sync(0xFFFFFFFFu, pc, 0);
+    st.unsup = __shfl_sync(0xFFFFFFFFu, us, 0);
+    st.mode = 3;
+    if (st.pcode || st.unsup || base + st.n > cap) {
+      if (lane == 0 && st.pcode) atomicMin(a.err_ref, ((unsigned long long)b << 8) | st.pcode);
+      if (lane == 0 && !st.pcode && st.unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | st.unsup);
+      return;
+    }
+  }
   const int mode = st.mode;
   const uint32_t nres = st.nres;
   uint32_t carry[NW];
 #pragma unroll
   for (int i = 0; i < NW; ++i) carry[i] = 0;
-  const uint64_t wstep = mode == 1 ? n : (uint64_t)kDecSlots;
-  for (uint64_t w0 = 0; w0 < n; w0 += wstep) {
+  const uint64_t wstep = (uint64_t)kDecSlots;
+  const uint64_t nall = st.n;
+  for (uint64_t w0 = 0; w0 < nall; w0 += wstep) {
     const uint64_t w1 = w0 + kDecSlots;
-    if (mode != 1) {
+    {
       auto put = [&](uint64_t j, uint32_t pos, uint32_t s, uint32_t vl) {
         if (j >= w0 && j < w1) slots[j - w0] = DecSlot{pos, (vl << 8) | s};
       };
@@ -380,19 +482,11 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
       }
     }
     __syncwarp();
-    const uint32_t wn = (uint32_t)((n - w0) < wstep ? (n - w0) : wstep);
+    const uint32_t wn = (uint32_t)((nall - w0) < wstep ? (nall - w0) : wstep);
     for (uint32_t c0 = 0; c0 < wn; c0 += 32) {
       const uint32_t e = c0 + lane;
       const bool act = e < wn;
-      uint32_t sidx = e;
-      if (mode == 1) {  // entry e lives in interval k with pre_k <= e < pre_{k+1}
-        uint32_t k = 0, pk = 0;
-        for (uint32_t kk = 1; kk < nres; ++kk) {
-          const uint32_t p = (uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)st.my_pre, kk);
-          if (p <= e) { k = kk; pk = p; }
-        }
-        sidx = kDecStride * k + (e - pk);
-      }
+      const uint32_t sidx = e;
       const DecSlot sl = act ? slots[sidx] : DecSlot{0, 0};
       const uint32_t s = sl.sv & 0xFFu;
       const uint32_t vl = sl.sv >> 8;

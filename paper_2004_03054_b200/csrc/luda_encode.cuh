@@ -160,6 +160,7 @@ struct EncodeArgs {
   const uint64_t* sst_off;
   const uint64_t* blk_out;   // output offset of every block
   uint8_t* out;
+  uint32_t dbg;              // experiment switches (0 in production)
 };
 
 // Output offset of every block: its SST's offset + its data offset in the SST.
@@ -300,6 +301,141 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
   __syncwarp();
 }
 
+// ---- software-pipelined fast path ------------------------------------------------
+// Blocks of <= 32 entries whose value windows fit the staging area (every
+// BASELINE shape): lane i owns entry i. While block k is finished (CRC +
+// copy-out), the records of block k+1 are already in registers and its value
+// windows are in flight (TMA into the staging area, free once block k's
+// values are realigned), so neither the record loads nor the value gather sit
+// on the per-block critical path.
+template <int W>
+struct EncLane {
+  uint64_t first, out_off;
+  uint32_t cnt, size, k;
+  bool valid;
+  Rec<W> r;            // this lane's record (lane < cnt)
+  // layout (lane's entry)
+  uint32_t s, hv, esz, off, win, wpre;
+  uint64_t voff;
+  uint32_t vl;
+  bool fast;
+};
+
+template <int W>
+__device__ __forceinline__ void enc_load(const EncodeArgs<W>& a, uint32_t k, EncLane<W>& e) {
+  e.k = k;
+  e.valid = k < a.nblk;
+  if (!e.valid) return;
+  e.first = a.blk_first[k];
+  e.cnt = a.blk_n[k];
+  e.size = a.blk_size[k];
+  e.out_off = a.blk_out[k];
+  if (lane_id() < e.cnt && e.cnt <= 32) e.r = a.rec[e.first + lane_id()];
+}
+
+// sizes, offsets and value windows of a block of <= 32 entries
+template <int W>
+__device__ __forceinline__ void enc_layout(const EncodeArgs<W>& a, EncLane<W>& e) {
+  const uint32_t lane = lane_id();
+  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage;
+  if (!e.fast) return;
+  const uint32_t K = a.K, L = K - 8;
+  const bool act = lane < e.cnt;
+  Rec<W> pr;
+#pragma unroll
+  for (int q = 0; q < W; ++q) pr.k[q] = __shfl_up_sync(0xFFFFFFFFu, e.r.k[q], 1);
+  pr.t = __shfl_up_sync(0xFFFFFFFFu, e.r.t, 1);
+  e.s = 0;
+  e.hv = e.esz = e.vl = 0;
+  e.voff = 0;
+  if (act) {
+    if (lane % a.ri != 0) e.s = ikey_lcp(pr, e.r, L);
+    e.vl = handle_len(e.r.h);
+    e.voff = handle_off(e.r.h);
+    e.hv = varint_size(e.s) + varint_size(K - e.s) + varint_size(e.vl);
+    e.esz = e.hv + (K - e.s) + e.vl;
+  }
+  const uint32_t incl = warp_incl_scan<uint32_t>(e.esz);
+  e.off = incl - e.esz;
+  const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + e.voff;
+  e.win = (act && e.vl) ? (uint32_t)(((vs + e.vl + 15) & ~uintptr_t(15)) - (vs & ~uintptr_t(15))) : 0u;
+  const uint32_t winc = warp_incl_scan<uint32_t>(e.win);
+  e.wpre = winc - e.win;
+  e.fast = __shfl_sync(0xFFFFFFFFu, winc, 31) <= (uint32_t)kEncStg;
+}
+
+template <int W>
+__device__ __forceinline__ void enc_issue(const EncodeArgs<W>& a, const EncLane<W>& e, uint8_t* stg, uint64_t* bar) {
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, e.wpre + e.win, 31);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane_id() == 0) mbar_arrive_expect_tx(bar, total);
+  __syncwarp();
+  if (e.win) {
+    const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + e.voff;
+    bulk_g2s(stg + e.wpre, reinterpret_cast<const void*>(vs & ~uintptr_t(15)), e.win, bar);
+  }
+}
+
+// headers + keys, then (after the values landed) the value realignment
+template <int W>
+__device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLane<W>& e, uint8_t* wbuf, uint8_t* stg,
+                                             uint64_t* bar, uint32_t& phase, uint32_t* pre) {
+  const uint32_t lane = lane_id();
+  const uint32_t K = a.K, L = K - 8, ri = a.ri;
+  const uint32_t nres = (e.cnt + ri - 1) / ri;
+  const uint32_t entries_end = e.size - 8 - 4 * nres;
+  uint8_t* sbase = wbuf + kEncPre;
+  uint8_t* dst = sbase + (e.out_off & 15);
+  if (lane < e.cnt) {
+    uint8_t* p = dst + e.off;
+    uint32_t h = put_varint(p, e.s);
+    h += put_varint(p + h, K - e.s);
+    h += put_varint(p + h, e.vl);
+    put_key_tail<W>(p + h, e.r, L, e.s);
+    if (lane % ri == 0) put_u32(dst + entries_end + 4 * (lane / ri), e.off);
+  }
+  if (lane == 0) put_u32(dst + entries_end + 4 * nres, nres);
+  __syncwarp();  // headers/keys written before values (edge words are read-modified-written)
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+  const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + e.voff;
+  const uint32_t soff = e.wpre + (uint32_t)(vs & 15u);
+  if (!(a.dbg & 4))
+  warp_copy_ranges16(sbase, stg, (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s), soff,
+                     lane < e.cnt ? e.vl : 0u, pre);
+  __syncwarp();
+}
+
+// CRC + 16-byte copy-out of an assembled (staged) block
+template <int W>
+__device__ __forceinline__ void enc_finish(const EncodeArgs<W>& a, const EncLane<W>& e, uint8_t* wbuf,
+                                           const CrcSmem& cs) {
+  const uint32_t lane = lane_id();
+  uint8_t* sbase = wbuf + kEncPre;
+  uint8_t* dst = sbase + (e.out_off & 15);
+  const uint32_t size = e.size;
+  const uint32_t crc = (a.dbg & 1) ? 0u : warp_crc32_smem(dst, size - 4, cs);
+  if (lane == 0) put_u32(dst + size - 4, crc);
+  __syncwarp();
+  const uintptr_t g = reinterpret_cast<uintptr_t>(a.out + e.out_off);
+  const uintptr_t g0 = g & ~uintptr_t(15), g1 = (g + size + 15) & ~uintptr_t(15);
+  const uint32_t nch = (uint32_t)((g1 - g0) >> 4);
+  const uint32_t c_first = (g0 == g) ? 0u : 1u;
+  const uint32_t c_last = ((g + size) & 15u) ? nch - 1 : nch;  // exclusive
+  if (!(a.dbg & 2))
+  for (uint32_t c = c_first + lane; c < c_last; c += 32)
+    *reinterpret_cast<uint4*>(g0 + 16ull * c) = *reinterpret_cast<const uint4*>(sbase + 16 * c);
+  {
+    const uint32_t c = lane < 16 ? 0u : nch - 1;
+    const bool partial = lane < 16 ? (c_first == 1) : (c_last == nch - 1 && !(c == 0 && c_first == 1));
+    const uint32_t bb = lane & 15u;
+    const uintptr_t A = g0 + 16ull * c + bb;
+    if (partial && A >= g && A < g + size) *reinterpret_cast<uint8_t*>(A) = sbase[16 * c + bb];
+  }
+  __syncwarp();
+}
+
 template <int W>
 __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -314,15 +450,27 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
   uint32_t phase = 0;
   const uint32_t gw = blockIdx.x * kEncWarps + (threadIdx.x >> 5);
   const uint32_t nw = gridDim.x * kEncWarps;
-  for (uint32_t k = gw; k < a.nblk; k += nw) {
-    const uint64_t first = a.blk_first[k];
-    const uint32_t cnt = a.blk_n[k];
-    const uint32_t size = a.blk_size[k];
-    const uint64_t out_off = a.blk_out[k];
-    if (size <= (uint32_t)kEncStage)
-      encode_one_block<W, true>(a, k, first, cnt, size, out_off, wbuf, stg, bar, phase, pre, cs);
-    else
-      encode_one_block<W, false>(a, k, first, cnt, size, out_off, wbuf, stg, bar, phase, pre, cs);
+  EncLane<W> cur, nxt;
+  enc_load(a, gw, cur);
+  enc_layout(a, cur);
+  if (cur.fast) enc_issue(a, cur, stg, bar);
+  while (cur.valid) {
+    enc_load(a, cur.k + nw, nxt);  // records of the next block: loads in flight
+    if (cur.fast) {
+      enc_assemble(a, cur, wbuf, stg, bar, phase, pre);
+      enc_layout(a, nxt);  // staging is free again: start the next block's value gather
+      if (nxt.fast) enc_issue(a, nxt, stg, bar);
+      enc_finish(a, cur, wbuf, cs);
+    } else {
+      const uint32_t k = cur.k;
+      if (cur.size <= (uint32_t)kEncStage)
+        encode_one_block<W, true>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, stg, bar, phase, pre, cs);
+      else
+        encode_one_block<W, false>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, stg, bar, phase, pre, cs);
+      enc_layout(a, nxt);
+      if (nxt.fast) enc_issue(a, nxt, stg, bar);
+    }
+    cur = nxt;
   }
 }
 
