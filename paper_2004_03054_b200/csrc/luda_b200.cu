@@ -364,7 +364,12 @@ int run_chain(cudaStream_t st, Scratch& scratch, const uint32_t* jmp, uint32_t n
   ++g_launches;
   chain_top_kernel<<<1, 32, 0, st>>>(c);
   ++g_launches;
-  chain_emit_kernel<<<ntiles, kChainThreads, 0, st>>>(c);
+  GET(tentry, uint32_t, ntiles, false);
+  GET(tbase, uint32_t, ntiles, false);
+  chain_tile_entry_kernel<<<(ngroups + 127) / 128, 128, 0, st>>>(c, tentry, tbase);
+  ++g_launches;
+  if (sm > 48 * 1024) CK(cudaFuncSetAttribute(chain_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  chain_emit_kernel<<<ntiles, kChainThreads, sm, st>>>(c, tentry, tbase);
   ++g_launches;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&outb.n_nodes, nn, 4, cudaMemcpyDeviceToHost, st));

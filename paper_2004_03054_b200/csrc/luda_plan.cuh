@@ -236,29 +236,44 @@ __global__ void chain_top_kernel(ChainArgs c) {
   *c.nnodes = total;
 }
 
-__global__ void __launch_bounds__(kChainThreads) chain_emit_kernel(ChainArgs c) {
-  __shared__ uint32_t s_off, s_base;
-  const uint32_t t = blockIdx.x;
-  if (threadIdx.x == 0) {
-    const uint32_t g = t / c.G;
-    uint32_t off = c.gentry[g], base = c.gbase[g];
-    for (uint32_t u = g * c.G; u < t && off != kChainEnd; ++u) {
-      const uint64_t idx = (uint64_t)u * c.D + off;
-      base += c.cnt[idx];
-      off = c.exit_[idx];
-    }
-    s_off = off;
-    s_base = base;
+// Entry offset and first node index of every tile: one thread per group walks
+// its G tiles (the tile maps compose along the true chain).
+__global__ void chain_tile_entry_kernel(ChainArgs c, uint32_t* tentry, uint32_t* tbase) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= c.ngroups) return;
+  uint32_t off = c.gentry[g], base = c.gbase[g];
+  const uint32_t tl = (g * c.G + c.G < c.ntiles) ? g * c.G + c.G : c.ntiles;
+  for (uint32_t u = g * c.G; u < tl; ++u) {
+    tentry[u] = off;
+    tbase[u] = base;
+    if (off == kChainEnd) continue;
+    const uint64_t idx = (uint64_t)u * c.D + off;
+    base += c.cnt[idx];
+    off = c.exit_[idx];
   }
-  __syncthreads();
-  if (threadIdx.x != 0 || s_off == kChainEnd) return;
+}
+
+// Walk each tile's true chain from its entry over the tile's jumps staged in
+// shared memory (one dependent LDS per node instead of a global load).
+__global__ void __launch_bounds__(kChainThreads) chain_emit_kernel(ChainArgs c, const uint32_t* tentry,
+                                                                   const uint32_t* tbase) {
+  extern __shared__ __align__(16) uint32_t sj[];
+  const uint32_t t = blockIdx.x;
+  const uint32_t off = tentry[t];
+  if (off == kChainEnd) return;
   const uint64_t t0 = (uint64_t)t * c.T;
   const uint64_t tend = t0 + c.T < c.n ? t0 + c.T : c.n;
-  uint64_t x = t0 + s_off;
-  uint32_t k = s_base;
+  const bool use_smem = c.T <= 12288;
+  if (use_smem) {
+    for (uint64_t x = t0 + threadIdx.x; x < tend; x += kChainThreads) sj[x - t0] = c.jmp[x];
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  uint64_t x = t0 + off;
+  uint32_t k = tbase[t];
   while (x < tend) {
     c.nodes[k++] = (uint32_t)x;
-    x += c.jmp[x];
+    x += use_smem ? sj[x - t0] : c.jmp[x];
   }
 }
 
