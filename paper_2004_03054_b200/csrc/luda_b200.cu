@@ -257,7 +257,7 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& s
     return LUDA_OK;
   }
   bool first_pass = true;
-  const size_t smem = sizeof(Rec<W>) * kMergeTile + 4 * kMergeTile;
+  const size_t smem = mrg_bytes<W>(kMergeTile) + 2 * kMergeTile;
   CK(cudaFuncSetAttribute(merge_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   Rec<W>* cur = X;
   Rec<W>* nxt = Y;

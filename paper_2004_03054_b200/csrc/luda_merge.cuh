@@ -160,12 +160,26 @@ struct MergeArgs {
   unsigned long long* n_out;
 };
 
+// Shared-memory tile layout: 16 bytes of padding after every 8 records. A
+// thread's heads sit ~8 records (256 B) from its neighbours'; unpadded, all
+// threads of a phase hit the same banks (ncu: 79% excess wavefronts).
+constexpr uint32_t kMergePad = 16;
+template <int W>
+__host__ __device__ constexpr uint32_t mrg_off(uint32_t i) {
+  return i * (uint32_t)sizeof(Rec<W>) + (i >> 3) * kMergePad;
+}
+template <int W>
+__host__ __device__ constexpr uint32_t mrg_bytes(uint32_t n) {
+  return mrg_off<W>(n) + kMergePad;
+}
+
 template <int W>
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  Rec<W>* S = reinterpret_cast<Rec<W>*>(smem_raw);
-  uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + sizeof(Rec<W>) * kMergeTile);
-  uint16_t* comp = perm + kMergeTile;
+  uint8_t* Sb = smem_raw;
+  auto SR = [&](uint32_t i) -> const Rec<W>& { return *reinterpret_cast<const Rec<W>*>(Sb + mrg_off<W>(i)); };
+  uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + mrg_bytes<W>(kMergeTile));
+  uint16_t* comp = perm;  // the resolve pass compacts from registers into the same array
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[kMergeThreads / 32];
   __shared__ unsigned long long s_base;
@@ -192,24 +206,29 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   if (kTma) {
     if (tid == 0) {
       mbar_init(&s_bar, 1);
-      const uint32_t bytes = nt * (uint32_t)sizeof(Rec<W>);
-      mbar_arrive_expect_tx(&s_bar, bytes);
-      m.A.pieces(a0, a1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) {
-        bulk_g2s(S + at, src, (uint32_t)cnt * (uint32_t)sizeof(Rec<W>), &s_bar);
-      });
-      m.B.pieces(b0, b1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) {
-        bulk_g2s(S + na_t + at, src, (uint32_t)cnt * (uint32_t)sizeof(Rec<W>), &s_bar);
-      });
+      mbar_arrive_expect_tx(&s_bar, nt * (uint32_t)sizeof(Rec<W>));
     }
     __syncthreads();
+    if (tid < 32) {  // one bulk copy per 8-record group (contiguous in smem) and piece
+      auto issue = [&](const Rec<W>* src, uint64_t cnt, uint64_t at) {
+        const uint32_t r0 = (uint32_t)at, r1 = (uint32_t)(at + cnt);
+        for (uint32_t gi = (r0 >> 3) + tid; gi <= ((r1 - 1) >> 3); gi += 32) {
+          const uint32_t x0 = gi * 8 > r0 ? gi * 8 : r0;
+          const uint32_t x1 = gi * 8 + 8 < r1 ? gi * 8 + 8 : r1;
+          bulk_g2s(Sb + mrg_off<W>(x0), src + (x0 - r0), (x1 - x0) * (uint32_t)sizeof(Rec<W>), &s_bar);
+        }
+      };
+      m.A.pieces(a0, a1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) { issue(src, cnt, at); });
+      m.B.pieces(b0, b1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) { issue(src, cnt, na_t + at); });
+    }
     mbar_wait(&s_bar, 0);
   } else {
     constexpr int RW = sizeof(Rec<W>) / 8;
-    uint64_t* sw = reinterpret_cast<uint64_t*>(S);
     auto copy = [&](uint32_t dst0) {
       return [&, dst0](const Rec<W>* src, uint64_t cnt, uint64_t at) {
         const uint64_t* gs = reinterpret_cast<const uint64_t*>(src);
-        for (uint32_t i = tid; i < cnt * RW; i += kMergeThreads) sw[(dst0 + at) * RW + i] = gs[i];
+        for (uint32_t i = tid; i < cnt * RW; i += kMergeThreads)
+          *reinterpret_cast<uint64_t*>(Sb + mrg_off<W>(dst0 + (uint32_t)at + i / RW) + 8 * (i % RW)) = gs[i];
       };
     };
     m.A.pieces(a0, a1, copy(0));
@@ -222,9 +241,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     const uint32_t li = inA ? i : i - na_t;
     const uint64_t gpos = inA ? a0 + li : b0 + li;
     if (gpos == 0) continue;
-    const Rec<W>& cur = S[i];
+    const Rec<W>& cur = SR(i);
     Rec<W> prev;
-    if (li > 0) prev = S[i - 1];
+    if (li > 0) prev = SR(i - 1);
     else prev = inA ? m.A[a0 - 1] : m.B[b0 - 1];
     if (rec_cmp(prev, cur) >= 0)
       atomicMin(m.err_order, (unsigned long long)((inA ? m.a_run_base : m.b_run_base) + gpos));
@@ -232,30 +251,31 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   // ---- per-thread merge of kMergeItems outputs (heads kept in registers) ----
   const uint32_t p0 = tid * kMergeItems;
   uint32_t keep_bits = 0, cnt = 0;
+  uint16_t my_perm[kMergeItems];
   if (p0 < nt) {
     uint32_t lo = p0 > nb_t ? p0 - nb_t : 0;
     uint32_t hi = p0 < na_t ? p0 : na_t;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (rec_le(S[mid], S[na_t + (p0 - 1 - mid)])) lo = mid + 1;
+      if (rec_le(SR(mid), SR(na_t + (p0 - 1 - mid)))) lo = mid + 1;
       else hi = mid;
     }
     uint32_t i = lo, j = p0 - lo;
     Rec<W> ha, hb;
-    if (i < na_t) ha = S[i];
-    if (j < nb_t) hb = S[na_t + j];
+    if (i < na_t) ha = SR(i);
+    if (j < nb_t) hb = SR(na_t + j);
     // resolve: predecessor of output p0 in merge order
     Rec<W> prev;
     bool has_prev = false;
     if (m.ra.resolve) {
       if (p0 > 0) {
-        // the element output just before p0 is the larger of S[i-1] (A) and S[na_t+j-1] (B)
+        // the element output just before p0 is the larger of SR(i-1) (A) and SR(na_t+j-1) (B)
         if (i > 0 && j > 0) {
-          const Rec<W>& pa = S[i - 1];
-          const Rec<W>& pb = S[na_t + j - 1];
+          const Rec<W>& pa = SR(i - 1);
+          const Rec<W>& pb = SR(na_t + j - 1);
           prev = rec_le(pa, pb) ? pb : pa;
         } else {
-          prev = i > 0 ? S[i - 1] : S[na_t + j - 1];
+          prev = i > 0 ? SR(i - 1) : SR(na_t + j - 1);
         }
         has_prev = true;
       } else if (d0 > 0) {
@@ -277,13 +297,14 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
         else if (j >= nb_t) takeA = true;
         else takeA = rec_le(ha, hb);
         const Rec<W> cur = takeA ? ha : hb;
-        perm[p] = (uint16_t)(takeA ? i : na_t + j);
+        my_perm[k] = (uint16_t)(takeA ? i : na_t + j);
+        if (!m.ra.resolve) perm[p] = my_perm[k];
         if (takeA) {
           ++i;
-          if (i < na_t) ha = S[i];
+          if (i < na_t) ha = SR(i);
         } else {
           ++j;
-          if (j < nb_t) hb = S[na_t + j];
+          if (j < nb_t) hb = SR(na_t + j);
         }
         if (m.ra.resolve) {
           const bool first = !has_prev || !same_user(prev, cur);
@@ -304,13 +325,13 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     constexpr int R16 = sizeof(Rec<W>) / 16;
     if (R16 * 16 == sizeof(Rec<W>)) {
       uint4* go = reinterpret_cast<uint4*>(m.out + d0);
-      const uint4* sv = reinterpret_cast<const uint4*>(S);
-      for (uint32_t i = tid; i < nt * R16; i += kMergeThreads) go[i] = sv[(uint32_t)perm[i / R16] * R16 + i % R16];
+      for (uint32_t i = tid; i < nt * R16; i += kMergeThreads)
+        go[i] = *reinterpret_cast<const uint4*>(Sb + mrg_off<W>(perm[i / R16]) + 16 * (i % R16));
     } else {
       constexpr int RW = sizeof(Rec<W>) / 8;
       uint64_t* go = reinterpret_cast<uint64_t*>(m.out + d0);
-      const uint64_t* sv = reinterpret_cast<const uint64_t*>(S);
-      for (uint32_t i = tid; i < nt * RW; i += kMergeThreads) go[i] = sv[(uint32_t)perm[i / RW] * RW + i % RW];
+      for (uint32_t i = tid; i < nt * RW; i += kMergeThreads)
+        go[i] = *reinterpret_cast<const uint64_t*>(Sb + mrg_off<W>(perm[i / RW]) + 8 * (i % RW));
     }
     return;
   }
@@ -337,20 +358,20 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   uint32_t w = s_warp[wid] + incl - cnt;
 #pragma unroll
   for (int k = 0; k < kMergeItems; ++k)
-    if (keep_bits & (1u << k)) comp[w++] = perm[p0 + k];
+    if (keep_bits & (1u << k)) comp[w++] = my_perm[k];
   __syncthreads();
   {
     const uint32_t tot = s_total;
     constexpr int R16 = sizeof(Rec<W>) / 16;
     if (R16 * 16 == sizeof(Rec<W>) && (s_base * sizeof(Rec<W>)) % 16 == 0) {
       uint4* go = reinterpret_cast<uint4*>(m.out + s_base);
-      const uint4* sv = reinterpret_cast<const uint4*>(S);
-      for (uint32_t i = tid; i < tot * R16; i += kMergeThreads) go[i] = sv[(uint32_t)comp[i / R16] * R16 + i % R16];
+      for (uint32_t i = tid; i < tot * R16; i += kMergeThreads)
+        go[i] = *reinterpret_cast<const uint4*>(Sb + mrg_off<W>(comp[i / R16]) + 16 * (i % R16));
     } else {
       constexpr int RW = sizeof(Rec<W>) / 8;
       uint64_t* go = reinterpret_cast<uint64_t*>(m.out + s_base);
-      const uint64_t* sv = reinterpret_cast<const uint64_t*>(S);
-      for (uint32_t i = tid; i < tot * RW; i += kMergeThreads) go[i] = sv[(uint32_t)comp[i / RW] * RW + i % RW];
+      for (uint32_t i = tid; i < tot * RW; i += kMergeThreads)
+        go[i] = *reinterpret_cast<const uint64_t*>(Sb + mrg_off<W>(comp[i / RW]) + 8 * (i % RW));
     }
   }
 }
