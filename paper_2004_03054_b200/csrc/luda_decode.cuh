@@ -53,9 +53,9 @@ enum BlockCode : uint32_t {
 // Paired warps: a PARSE warp (producer + walk + records) and a CRC warp share
 // a pair of staging slots; both consume every block of the pair's contiguous
 // block range concurrently (the CRC never modifies bytes the parse warp reads).
-constexpr int kDecPairs = 10;
+constexpr int kDecPairs = 14;
 constexpr int kDecWarps = 2 * kDecPairs;
-constexpr int kDecNSlot = 3;                     // staging slots per pair (2 blocks in flight)
+constexpr int kDecNSlot = 2;                     // staging slots per pair (1 block in flight)
 constexpr int kDecLead = 48;                     // zero lead before the TMA window (never written by TMA)
 constexpr int kDecStage = 4352;                  // TMA window capacity
 constexpr int kDecSlot = kDecLead + kDecStage;   // bytes per staging slot
@@ -333,6 +333,7 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
   const uint32_t nres = st.nres;
   const uint32_t nchunks = (nres + 1) / 2;
   const uint32_t lt = (1u << lane) - 1u;
+  DEC_T0();
   auto slot = [&](uint32_t q, uint32_t& pos, uint32_t& w, uint32_t& j) -> bool {
     const uint32_t k = 2 * q + (lane >> 4);
     j = lane & 15u;
@@ -358,7 +359,9 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
   for (uint32_t q = 0; q < nchunks; ++q) {
     uint32_t pos, w, j;
     const bool act = slot(q, pos, w, j);
+    DEC_T(4);
     if (nchunks == 1 && __any_sync(0xFFFFFFFFu, act && bad_of(w, j) != 0)) return false;
+    DEC_T(5);
     const uint32_t s = act ? (w & 0xFFu) : 0u;
     const uint32_t two = (w >> 23) & 1u;
     const uint32_t v1 = prmt(w, 0u, 0x4442u);
@@ -379,6 +382,7 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
         lo = hi;
       }
     }
+    DEC_T(6);
     const uint32_t smax = __reduce_max_sync(0xFFFFFFFFu, s);
     uint32_t fixed[NW];
 #pragma unroll
@@ -403,6 +407,7 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
         fixed[wi] = f;
       }
     }
+    DEC_T(7);
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, act);
     if (act) {
       Rec<W> r;
@@ -411,6 +416,7 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
       a.out[e0 + __popc(m & lt)] = r;
     }
     e0 += __popc(m);
+    DEC_T(8);
   }
   return true;
 }

@@ -78,7 +78,7 @@ int main() {
     unsigned long long tt[16];
     cudaMemcpyFromSymbol(tt, g_dec_t, sizeof(tt));
     double nb = 148.0 * warps * iters;
-    printf("   p1 sections: restarts %.0f walk %.0f validate %.0f scan %.0f\n", tt[0] / nb, tt[1] / nb, tt[2] / nb, tt[3] / nb);
+    printf("   p1 sections: restarts %.0f walk %.0f validate %.0f scan %.0f | p2: slot+hdr %.0f validate %.0f keyload %.0f resolve %.0f write %.0f\n", tt[0] / nb, tt[1] / nb, tt[2] / nb, tt[3] / nb, tt[4] / nb, tt[5] / nb, tt[6] / nb, tt[7] / nb, tt[8] / nb);
     { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_dec_t, z, sizeof(z)); }
     unsigned long long e[2]; cudaMemcpy(e, d_err, 16, cudaMemcpyDeviceToHost);
     double cpb = (double)h[0] / iters;
