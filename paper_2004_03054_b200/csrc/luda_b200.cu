@@ -502,9 +502,9 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   const uint32_t s_edbg = getenv("LUDA_ENC_DBG") ? (uint32_t)atoi(getenv("LUDA_ENC_DBG")) : 0u;
   EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off,
                    blk_out, res->out, s_edbg};
-  const size_t esm = sizeof(CrcSmem) + (size_t)kEncWarps * kEncWarpBytes;
+  const size_t esm = sizeof(CrcSmem) + (size_t)kEncPairs * sizeof(EncPairSmem);
   CK(cudaFuncSetAttribute(encode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
-  const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncWarps - 1) / kEncWarps, (uint64_t)g_num_sms);
+  const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncPairs - 1) / kEncPairs, (uint64_t)g_num_sms);
   KT_START(3, st);
   encode_kernel<W><<<std::max(1u, egrid), kEncWarps * 32, esm, st>>>(ea);
   ++g_launches;

@@ -25,14 +25,30 @@
 
 namespace luda {
 
-constexpr int kEncWarps = 13;
+// Pairs: a BUILDER warp (records, layout, value TMA, assembly) and a CRC warp
+// (CRC + copy-out) hand assembled blocks over through two buffers.
+constexpr int kEncPairs = 9;
+constexpr int kEncWarps = 2 * kEncPairs;
 constexpr int kEncStage = 4608;                        // blocks up to this size are assembled in smem
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
-constexpr int kEncStg = 5120;                          // per-warp TMA staging for value windows
-constexpr int kEncWarpBytes = kEncBuf + kEncStg + 16 + 512 + kCopyMap;  // + mbarrier + copy scratch
+constexpr int kEncStg = 4608;                          // per-pair TMA staging for value windows
+struct EncMeta {
+  uint64_t out_off;
+  uint32_t size;
+  uint32_t skip;  // the builder finished the block itself (generic path)
+};
+struct alignas(16) EncPairSmem {
+  uint8_t buf[2][kEncBuf];
+  uint8_t stg[kEncStg];
+  uint64_t bar;                 // value TMA
+  uint32_t pre[128 + kCopyMap / 4];  // copy scratch (512 B + map)
+  uint64_t full[2], empty[2];
+  EncMeta meta[2];
+};
 static_assert(kEncStg / 16 <= kCopyMap, "copy map smaller than the staging chunk count");
-static_assert(sizeof(CrcSmem) + kEncWarps * kEncWarpBytes <= 232448, "encode smem over the 227 KB limit");
+static_assert(sizeof(CrcSmem) + kEncPairs * sizeof(EncPairSmem) <= 232448, "encode smem over the 227 KB limit");
+static_assert(sizeof(EncPairSmem) % 16 == 0 && kEncBuf % 16 == 0, "TMA / vector alignment");
 
 // Copy n bytes src → dst (any alignment; dst generic: smem or global) with
 // `nl` cooperating threads (rank `r`). Destination-aligned 32-bit words are
@@ -440,37 +456,70 @@ template <int W>
 __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
-  uint8_t* wbuf = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * kEncWarpBytes;
-  uint8_t* stg = wbuf + kEncBuf;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kEncStg);
-  uint32_t* pre = reinterpret_cast<uint32_t*>(stg + kEncStg + 16);
+  EncPairSmem* pairs = reinterpret_cast<EncPairSmem*>(smem_raw + sizeof(CrcSmem));
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const bool builder = warp < kEncPairs;
+  const uint32_t p = warp % kEncPairs;
+  EncPairSmem& ps = pairs[p];
   crc_smem_init(cs);
-  if (lane_id() == 0) mbar_init(bar, 1);
-  __syncthreads();
-  uint32_t phase = 0;
-  const uint32_t gw = blockIdx.x * kEncWarps + (threadIdx.x >> 5);
-  const uint32_t nw = gridDim.x * kEncWarps;
-  EncLane<W> cur, nxt;
-  enc_load(a, gw, cur);
-  enc_layout(a, cur);
-  if (cur.fast) enc_issue(a, cur, stg, bar);
-  while (cur.valid) {
-    enc_load(a, cur.k + nw, nxt);  // records of the next block: loads in flight
-    if (cur.fast) {
-      enc_assemble(a, cur, wbuf, stg, bar, phase, pre);
-      enc_layout(a, nxt);  // staging is free again: start the next block's value gather
-      if (nxt.fast) enc_issue(a, nxt, stg, bar);
-      enc_finish(a, cur, wbuf, cs);
-    } else {
-      const uint32_t k = cur.k;
-      if (cur.size <= (uint32_t)kEncStage)
-        encode_one_block<W, true>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, stg, bar, phase, pre, cs);
-      else
-        encode_one_block<W, false>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, stg, bar, phase, pre, cs);
-      enc_layout(a, nxt);
-      if (nxt.fast) enc_issue(a, nxt, stg, bar);
+  if (builder && lane == 0) {
+    mbar_init(&ps.bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ps.full[b], 1);
+      mbar_init(&ps.empty[b], 1);
     }
-    cur = nxt;
+  }
+  __syncthreads();
+  const uint32_t gw = blockIdx.x * kEncPairs + p;
+  const uint32_t nw = gridDim.x * kEncPairs;
+  if (builder) {
+    uint32_t phase = 0;
+    EncLane<W> cur, nxt;
+    enc_load(a, gw, cur);
+    enc_layout(a, cur);
+    if (cur.fast) enc_issue(a, cur, ps.stg, &ps.bar);
+    for (uint32_t i = 0; cur.valid; ++i) {
+      const uint32_t b = i & 1u;
+      uint8_t* wbuf = ps.buf[b];
+      if (i >= 2) mbar_wait(&ps.empty[b], ((i - 2) >> 1) & 1u);  // the CRC warp is done with block i-2
+      enc_load(a, cur.k + nw, nxt);  // records of the next block: loads in flight
+      EncMeta mt{cur.out_off, cur.size, 0u};
+      if (cur.fast) {
+        enc_assemble(a, cur, wbuf, ps.stg, &ps.bar, phase, ps.pre);
+        enc_layout(a, nxt);  // staging is free again: start the next block's value gather
+        if (nxt.fast) enc_issue(a, nxt, ps.stg, &ps.bar);
+      } else {
+        const uint32_t k = cur.k;
+        if (cur.size <= (uint32_t)kEncStage)
+          encode_one_block<W, true>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, ps.stg, &ps.bar, phase,
+                                    ps.pre, cs);
+        else
+          encode_one_block<W, false>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, ps.stg, &ps.bar, phase,
+                                     ps.pre, cs);
+        mt.skip = 1;
+        enc_layout(a, nxt);
+        if (nxt.fast) enc_issue(a, nxt, ps.stg, &ps.bar);
+      }
+      if (lane == 0) ps.meta[b] = mt;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps.full[b]);  // release: the assembled block and its meta
+      cur = nxt;
+    }
+  } else {
+    // CRC warp: CRC + copy-out of the blocks the builder assembled, in order
+    for (uint32_t i = 0, k = gw; k < a.nblk; ++i, k += nw) {
+      const uint32_t b = i & 1u;
+      mbar_wait(&ps.full[b], (i >> 1) & 1u);
+      const EncMeta mt = ps.meta[b];
+      if (!mt.skip) {
+        EncLane<W> e;
+        e.out_off = mt.out_off;
+        e.size = mt.size;
+        enc_finish(a, e, ps.buf[b], cs);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps.empty[b]);
+    }
   }
 }
 
