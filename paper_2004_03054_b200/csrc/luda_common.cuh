@@ -447,6 +447,38 @@ __device__ __forceinline__ void copy_chunk16(uint8_t* base_dst, const uint8_t* b
   v3 = __funnelshift_r(y[3], y[4], sh);
 }
 
+// Per-lane copy of one range src → dst (both in smem; 16-aligned bases, any
+// offsets): every destination 16-byte chunk the range touches is realigned
+// from two aligned LDS.128; interior chunks are one STS.128, the <= 2 partial
+// edge chunks are written per word (partial words read-modify-written — the
+// caller guarantees no other lane writes those words concurrently). Source
+// windows must be readable 16 bytes beyond the range.
+__device__ __forceinline__ void lane_copy16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
+                                            uint32_t src_off, uint32_t n) {
+  if (n == 0) return;
+  const uint32_t c_lo = dst_off & ~15u, c_hi = (dst_off + n + 15) & ~15u;
+  for (uint32_t dchunk = c_lo; dchunk < c_hi; dchunk += 16) {
+    const int32_t sstart = (int32_t)(src_off + dchunk) - (int32_t)dst_off;
+    uint32_t v[4];
+    copy_chunk16(base_dst, base_src, dchunk, sstart, v[0], v[1], v[2], v[3]);
+    const uint32_t lo = dchunk < dst_off ? dst_off - dchunk : 0u;
+    const uint32_t hi = (dchunk + 16 > dst_off + n) ? dst_off + n - dchunk : 16u;
+    if (lo == 0 && hi == 16) {
+      *reinterpret_cast<uint4*>(base_dst + dchunk) = make_uint4(v[0], v[1], v[2], v[3]);
+    } else {
+      uint32_t* dw = reinterpret_cast<uint32_t*>(base_dst + dchunk);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t a = (int32_t)lo - 4 * k, b = (int32_t)hi - 4 * k;  // valid bytes [a, b) of word k
+        if (b <= 0 || a >= 4) continue;
+        const uint32_t m =
+            (b >= 4 ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u)) & (a <= 0 ? 0xFFFFFFFFu : ~((1u << (8 * a)) - 1u));
+        dw[k] = m == 0xFFFFFFFFu ? v[k] : ((dw[k] & ~m) | (v[k] & m));
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void warp_copy_ranges16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
                                                    uint32_t src_off, uint32_t n, uint32_t* scratch) {
   const uint32_t lane = lane_id();

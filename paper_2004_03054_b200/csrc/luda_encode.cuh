@@ -417,9 +417,10 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   phase ^= 1u;
   const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + e.voff;
   const uint32_t soff = e.wpre + (uint32_t)(vs & 15u);
-  if (!(a.dbg & 4))
-  warp_copy_ranges16(sbase, stg, (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s), soff,
-                     lane < e.cnt ? e.vl : 0u, pre);
+  // each lane realigns its own value (no chunk map; edge words of neighbouring
+  // entries are >= 12 bytes apart, so the per-word read-modify-writes never race)
+  if (!(a.dbg & 4) && lane < e.cnt)
+    lane_copy16(sbase, stg, (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s), soff, e.vl);
   __syncwarp();
 }
 
