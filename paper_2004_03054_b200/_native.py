@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libluda_b200.so")
+LIB_PATH = os.environ.get("LUDA_LIB") or os.path.join(HERE, "libluda_b200.so")
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)
 c_u32p = ctypes.POINTER(ctypes.c_uint32)

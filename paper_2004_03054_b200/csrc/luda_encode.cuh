@@ -104,6 +104,79 @@ __device__ __forceinline__ void put_key_tail(uint8_t* p, const Rec<W>& r, uint32
   }
 }
 
+// Entry prefix (varint shared ∥ varint unshared ∥ varint value_len ∥
+// key[shared:]) written to smem as aligned 32-bit words instead of byte
+// stores. Phase 1 (this function) writes every word except the first when the
+// entry does not start on a word boundary; those bytes may belong to the
+// previous entry, whose lane is writing in the same phase. The bytes past the
+// prefix in its last word are placeholders: the entry's own value (written
+// later with masked edges) or, for an empty value, the next entry's first
+// word (written in phase 2). Returns the first word for phase 2. Requires the
+// header to fit 8 bytes (shared, unshared < 128 — every key length <= 120).
+template <int W>
+__device__ __forceinline__ uint32_t put_prefix_words(uint8_t* D, const Rec<W>& r, uint32_t L, uint32_t s,
+                                                     uint32_t vl, uint32_t hv) {
+  constexpr int NK = 2 * W + 2;             // internal-key words (K <= 8W + 8)
+  constexpr int NO = (8 * W + 8 + 7 + 3 + 3) / 4;  // output words: a + hv + u <= 3 + 7 + K
+  constexpr int QM = (8 * W + 8 + 12) / 4;  // max word shift
+  constexpr int NB = NO + 1 + QM;
+  const uint32_t K = L + 8, u = K - s;
+  const uint32_t a = (uint32_t)reinterpret_cast<uintptr_t>(D) & 3u;
+  uint32_t kw[NK];
+  rec_to_words<W, NK>(r, L, kw);
+  // Z = 3 zero words ∥ key words; output word w = Z bytes [4w + c, 4w + c + 4), c = s - a - hv + 12
+  const uint32_t c = s + 12u - a - hv;
+  const uint32_t q = c >> 2, sh = 8u * (c & 3u);
+  uint32_t B[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) B[i] = (i >= 3 && i - 3 < NK) ? kw[i - 3] : 0u;
+#pragma unroll
+  for (int k = 0; (1 << k) <= QM; ++k) {
+    const bool take = (q >> k) & 1u;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) B[i] = take ? (i + (1 << k) < NB ? B[i + (1 << k)] : 0u) : B[i];
+  }
+  // header bytes at output positions [a, a + hv)
+  uint64_t H = 0;
+  {
+    uint32_t n = 0;
+    H = (uint64_t)s | ((uint64_t)u << 8);
+    n = 2;
+    uint32_t v = vl;
+    while (v >= 0x80u) { H |= (uint64_t)((v & 0x7Fu) | 0x80u) << (8 * n); ++n; v >>= 7; }
+    H |= (uint64_t)v << (8 * n);
+  }
+  const uint64_t Mv = (hv >= 8) ? ~0ull : ((1ull << (8 * hv)) - 1ull);
+  const uint32_t ab = 8u * a;
+  const uint32_t h0 = (uint32_t)H << ab, m0 = (uint32_t)Mv << ab;
+  const uint32_t h1 = ab ? (uint32_t)(H >> (32 - ab)) : (uint32_t)(H >> 32);
+  const uint32_t m1 = ab ? (uint32_t)(Mv >> (32 - ab)) : (uint32_t)(Mv >> 32);
+  const uint32_t h2 = ab ? (uint32_t)(H >> (64 - ab)) : 0u;
+  const uint32_t m2 = ab ? (uint32_t)(Mv >> (64 - ab)) : 0u;
+  const uint32_t nout = (a + hv + u + 3) >> 2;
+  uint32_t* A0 = reinterpret_cast<uint32_t*>(D - a);
+  uint32_t first = 0;
+#pragma unroll
+  for (int w = 0; w < NO; ++w) {
+    uint32_t v = __funnelshift_r(B[w], B[w + 1], sh);
+    if (w == 0) v = (v & ~m0) | (h0 & m0);
+    if (w == 1) v = (v & ~m1) | (h1 & m1);
+    if (w == 2) v = (v & ~m2) | (h2 & m2);
+    if (w == 0) first = v;
+    if ((uint32_t)w < nout && (w > 0 || a == 0)) A0[w] = v;
+  }
+  return first;
+}
+
+// Phase 2 of put_prefix_words: the shared first word, bytes [a, 4) ours.
+__device__ __forceinline__ void put_prefix_first(uint8_t* D, uint32_t first) {
+  const uint32_t a = (uint32_t)reinterpret_cast<uintptr_t>(D) & 3u;
+  if (a == 0) return;
+  uint32_t* A0 = reinterpret_cast<uint32_t*>(D - a);
+  const uint32_t m = 0xFFFFFFFFu << (8 * a);
+  *A0 = (*A0 & ~m) | (first & m);
+}
+
 // CTA-wide CRC-32 of smem data (passes spread over warps). All threads call;
 // returns the CRC in every thread. The data needs kCrcLead writable bytes
 // before it (prepared and restored here). `red` = smem scratch of >= 32 words.
@@ -353,7 +426,7 @@ __device__ __forceinline__ void enc_load(const EncodeArgs<W>& a, uint32_t k, Enc
 template <int W>
 __device__ __forceinline__ void enc_layout(const EncodeArgs<W>& a, EncLane<W>& e) {
   const uint32_t lane = lane_id();
-  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage;
+  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage && a.K < 128;
   if (!e.fast) return;
   const uint32_t K = a.K, L = K - 8;
   const bool act = lane < e.cnt;
@@ -403,12 +476,11 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   const uint32_t entries_end = e.size - 8 - 4 * nres;
   uint8_t* sbase = wbuf + kEncPre;
   uint8_t* dst = sbase + (e.out_off & 15);
+  uint32_t first = 0;
+  if (lane < e.cnt) first = put_prefix_words<W>(dst + e.off, e.r, L, e.s, e.vl, e.hv);
+  __syncwarp();
   if (lane < e.cnt) {
-    uint8_t* p = dst + e.off;
-    uint32_t h = put_varint(p, e.s);
-    h += put_varint(p + h, K - e.s);
-    h += put_varint(p + h, e.vl);
-    put_key_tail<W>(p + h, e.r, L, e.s);
+    put_prefix_first(dst + e.off, first);
     if (lane % ri == 0) put_u32(dst + entries_end + 4 * (lane / ri), e.off);
   }
   if (lane == 0) put_u32(dst + entries_end + 4 * nres, nres);
