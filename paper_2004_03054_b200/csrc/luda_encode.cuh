@@ -33,6 +33,7 @@ constexpr int kEncStage = 4608;                        // blocks up to this size
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
 constexpr int kEncStg = 4608;                          // per-pair TMA staging for value windows
+constexpr int kEncGap = 64;                            // arena gap bridged by one value window
 struct EncMeta {
   uint64_t out_off;
   uint32_t size;
@@ -404,7 +405,7 @@ struct EncLane {
   bool valid;
   Rec<W> r;            // this lane's record (lane < cnt)
   // layout (lane's entry)
-  uint32_t s, hv, esz, off, win, wpre;
+  uint32_t s, hv, esz, off, win, wpre, soff;
   uint64_t voff;
   uint32_t vl;
   bool fast;
@@ -446,11 +447,34 @@ __device__ __forceinline__ void enc_layout(const EncodeArgs<W>& a, EncLane<W>& e
   }
   const uint32_t incl = warp_incl_scan<uint32_t>(e.esz);
   e.off = incl - e.esz;
+  // value windows: 16-byte-aligned source spans. Consecutive entries whose
+  // values sit close together in the arena (same input block) share one
+  // window — one bulk copy instead of one per entry; the gap bytes are staged
+  // too. If merged windows overflow the staging area, entries get their own.
   const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + e.voff;
-  e.win = (act && e.vl) ? (uint32_t)(((vs + e.vl + 15) & ~uintptr_t(15)) - (vs & ~uintptr_t(15))) : 0u;
-  const uint32_t winc = warp_incl_scan<uint32_t>(e.win);
-  e.wpre = winc - e.win;
-  e.fast = __shfl_sync(0xFFFFFFFFu, winc, 31) <= (uint32_t)kEncStg;
+  const bool has = act && e.vl;
+  const uintptr_t ws = vs & ~uintptr_t(15), we = (vs + e.vl + 15) & ~uintptr_t(15);
+  const uintptr_t pve = __shfl_up_sync(0xFFFFFFFFu, vs + e.vl, 1);  // previous value's end
+  const bool phas = __shfl_up_sync(0xFFFFFFFFu, (uint32_t)has, 1) && lane > 0;
+  const bool cont = has && phas && vs >= pve && vs <= pve + (uintptr_t)kEncGap;  // windows stay monotone
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool join = attempt == 0 && cont;
+    const uint32_t heads = __ballot_sync(0xFFFFFFFFu, has && !join);
+    const uint32_t joins = __ballot_sync(0xFFFFFFFFu, join);
+    // last lane of my group: first lane after me that does not join, minus one
+    const uint32_t after = ~joins & ~((2u << lane) - 1u);
+    const uint32_t last = after ? (uint32_t)(__ffs(after) - 2) : 31u;
+    const uint32_t head = has ? 31u - __clz(heads & ((2u << lane) - 1u)) : lane;
+    const uintptr_t gws = __shfl_sync(0xFFFFFFFFu, ws, head);
+    const uintptr_t gwe = __shfl_sync(0xFFFFFFFFu, we, last);
+    e.win = (has && !join) ? (uint32_t)(gwe - ws) : 0u;  // group window, at the head lane
+    const uint32_t winc = warp_incl_scan<uint32_t>(e.win);
+    e.wpre = winc - e.win;
+    const uint32_t gpre = __shfl_sync(0xFFFFFFFFu, e.wpre, head);
+    e.soff = gpre + (uint32_t)(vs - gws);
+    e.fast = __shfl_sync(0xFFFFFFFFu, winc, 31) <= (uint32_t)kEncStg;
+    if (e.fast || !__any_sync(0xFFFFFFFFu, cont)) break;
+  }
 }
 
 template <int W>
@@ -462,7 +486,7 @@ __device__ __forceinline__ void enc_issue(const EncodeArgs<W>& a, const EncLane<
   __syncwarp();
   if (e.win) {
     const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + e.voff;
-    bulk_g2s(stg + e.wpre, reinterpret_cast<const void*>(vs & ~uintptr_t(15)), e.win, bar);
+    bulk_g2s(stg + e.wpre, reinterpret_cast<const void*>(vs & ~uintptr_t(15)), e.win, bar);  // group head
   }
 }
 
@@ -487,8 +511,7 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   __syncwarp();  // headers/keys written before values (edge words are read-modified-written)
   mbar_wait(bar, phase);
   phase ^= 1u;
-  const uintptr_t vs = reinterpret_cast<uintptr_t>(a.arena) + e.voff;
-  const uint32_t soff = e.wpre + (uint32_t)(vs & 15u);
+  const uint32_t soff = e.soff;
   // each lane realigns its own value (no chunk map; edge words of neighbouring
   // entries are >= 12 bytes apart, so the per-word read-modify-writes never race)
   if (!(a.dbg & 4) && lane < e.cnt)
