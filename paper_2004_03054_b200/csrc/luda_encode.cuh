@@ -33,7 +33,7 @@ constexpr int kEncStage = 4608;                        // blocks up to this size
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
 constexpr int kEncStg = 4608;                          // per-pair TMA staging for value windows
-constexpr int kEncGap = 64;                            // arena gap bridged by one value window
+constexpr int kEncGap = 128;                            // arena gap bridged by one value window
 struct EncMeta {
   uint64_t out_off;
   uint32_t size;
