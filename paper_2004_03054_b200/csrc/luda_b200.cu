@@ -767,7 +767,10 @@ int luda_shutdown(void) {
 int luda_region_alloc(uint64_t nbytes, void** dev_ptr) {
   // regions start zero-filled like the reference's shared-memory regions
   CK(cudaMalloc(dev_ptr, std::max<uint64_t>(nbytes, 1) + 512));
-  CK(cudaMemset(*dev_ptr, 0, std::max<uint64_t>(nbytes, 1) + 512));
+  // (cudaMemset may return before the fill lands, and the staging streams are
+  // non-blocking: finish it before any stream can copy into the region)
+  CK(cudaMemsetAsync(*dev_ptr, 0, std::max<uint64_t>(nbytes, 1) + 512, 0));
+  CK(cudaStreamSynchronize(0));
   return LUDA_OK;
 }
 int luda_region_free(void* p) {

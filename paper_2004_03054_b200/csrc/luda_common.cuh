@@ -479,6 +479,89 @@ __device__ __forceinline__ void lane_copy16(uint8_t* base_dst, const uint8_t* ba
   }
 }
 
+// lane_copy16 for an entry's value inside an assembled block: the source
+// chunk is carried between iterations (one LDS.128 per destination chunk),
+// and the two edge words are completed from registers instead of being
+// read-modified-written: bytes below the value in its first word are the
+// entry's own prefix (`head`, when use_head), bytes above the value in its last
+// word are the next entry's first prefix word (`tail`, when use_tail). The
+// edge words are composed once, outside the chunk loop; other partial words
+// are read-modified-written.
+__device__ __forceinline__ void value_copy16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
+                                             uint32_t src_off, uint32_t n, uint32_t head, bool use_head,
+                                             uint32_t tail, bool use_tail) {
+  if (n == 0) return;
+  const uint32_t end = dst_off + n;
+  const uint32_t hw = dst_off & ~3u, tw = (end - 1) & ~3u;
+  const uint32_t ha = dst_off & 3u, ta = end & 3u;
+  const bool do_head = use_head && ha != 0;
+  const bool do_tail = use_tail && ta != 0;
+  const bool one = hw == tw;  // the value sits inside one word
+  // chunk loop over [lo_all, hi_all)
+  const uint32_t lo_all = do_head ? hw + 4 : dst_off;
+  const uint32_t hi_all = do_tail ? tw : end;
+  if (lo_all < hi_all) {
+    const uint32_t c_lo = lo_all & ~15u, c_hi = (hi_all + 15) & ~15u;
+    const int32_t s0 = (int32_t)src_off + (int32_t)c_lo - (int32_t)dst_off;  // source of byte c_lo
+    const uint32_t o = (uint32_t)s0 & 15u;
+    const uint4* sp = reinterpret_cast<const uint4*>(base_src + (s0 - (int32_t)o));
+    const uint32_t q = o >> 2, sh = (o & 3u) * 8u;
+    uint4 A = sp[0];
+    uint32_t i = 1;
+    for (uint32_t dchunk = c_lo; dchunk < c_hi; dchunk += 16, ++i) {
+      const uint4 B = sp[i];
+      const uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+      A = B;
+      uint32_t x[6], y[5], v[4];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) x[k] = (q & 2u) ? w[k + 2] : w[k];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) y[k] = (q & 1u) ? x[k + 1] : x[k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __funnelshift_r(y[k], y[k + 1], sh);
+      const uint32_t lo = dchunk < lo_all ? lo_all - dchunk : 0u;
+      const uint32_t hi = (dchunk + 16 > hi_all) ? hi_all - dchunk : 16u;
+      if (lo == 0 && hi == 16) {
+        *reinterpret_cast<uint4*>(base_dst + dchunk) = make_uint4(v[0], v[1], v[2], v[3]);
+      } else {
+        uint32_t* dw = reinterpret_cast<uint32_t*>(base_dst + dchunk);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int32_t a = (int32_t)lo - 4 * k, b = (int32_t)hi - 4 * k;  // bytes [a, b) of word k
+          if (b <= 0 || a >= 4) continue;
+          const uint32_t m =
+              (b >= 4 ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u)) & (a <= 0 ? 0xFFFFFFFFu : ~((1u << (8 * a)) - 1u));
+          dw[k] = m == 0xFFFFFFFFu ? v[k] : ((dw[k] & ~m) | (v[k] & m));
+        }
+      }
+    }
+  }
+  // edge words
+  const uint32_t tmask = ta ? (1u << (8 * ta)) - 1u : 0xFFFFFFFFu;  // bytes below the value end (tail word)
+  if (do_head) {
+    const uint32_t hmask = 0xFFFFFFFFu << (8 * ha);  // value bytes and above
+    uint32_t v = (head & ~hmask) | ((ld_u32_any(base_src + src_off) << (8 * ha)) & hmask);
+    uint32_t* p = reinterpret_cast<uint32_t*>(base_dst + hw);
+    if (one && ta) {
+      if (do_tail) *p = (v & tmask) | (tail & ~tmask);
+      else *p = (v & tmask) | (*p & ~tmask);
+    } else {
+      *p = v;
+    }
+  }
+  if (do_tail && !(do_head && one)) {
+    uint32_t v = ld_u32_any(base_src + src_off + (tw - dst_off));
+    uint32_t* p = reinterpret_cast<uint32_t*>(base_dst + tw);
+    if (one && ha) {  // value starts inside this word too, below it is not ours
+      v = ld_u32_any(base_src + src_off) << (8 * ha);
+      const uint32_t m = 0xFFFFFFFFu << (8 * ha);
+      *p = (*p & ~m) | (((v & tmask) | (tail & ~tmask)) & m);
+    } else {
+      *p = (v & tmask) | (tail & ~tmask);
+    }
+  }
+}
+
 __device__ __forceinline__ void warp_copy_ranges16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
                                                    uint32_t src_off, uint32_t n, uint32_t* scratch) {
   const uint32_t lane = lane_id();

@@ -515,7 +515,8 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   // each lane realigns its own value (no chunk map; edge words of neighbouring
   // entries are >= 12 bytes apart, so the per-word read-modify-writes never race)
   if (!(a.dbg & 4) && lane < e.cnt)
-    lane_copy16(sbase, stg, (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s), soff, e.vl);
+    value_copy16(sbase, stg, (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s), soff, e.vl, 0u, false, 0u,
+                 false);
   __syncwarp();
 }
 
