@@ -184,8 +184,6 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   __shared__ uint32_t s_warp[kMergeThreads / 32];
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_total;
-  __shared__ __align__(8) uint64_t s_bar;
-  constexpr bool kTma = (sizeof(Rec<W>) % 16) == 0;
   const uint32_t tid = threadIdx.x;
   uint64_t tile;
   if (m.ra.resolve) {
@@ -202,37 +200,27 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   const uint64_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t na_t = (uint32_t)(a1 - a0), nb_t = (uint32_t)(b1 - b0);
   const uint32_t nt = na_t + nb_t;
-  // ---- load the A and B slices: TMA bulk copies (or vector loads) ----
-  if (kTma) {
-    if (tid == 0) {
-      mbar_init(&s_bar, 1);
-      mbar_arrive_expect_tx(&s_bar, nt * (uint32_t)sizeof(Rec<W>));
-    }
-    __syncthreads();
-    if (tid < 32) {  // one bulk copy per 8-record group (contiguous in smem) and piece
-      auto issue = [&](const Rec<W>* src, uint64_t cnt, uint64_t at) {
-        const uint32_t r0 = (uint32_t)at, r1 = (uint32_t)(at + cnt);
-        for (uint32_t gi = (r0 >> 3) + tid; gi <= ((r1 - 1) >> 3); gi += 32) {
-          const uint32_t x0 = gi * 8 > r0 ? gi * 8 : r0;
-          const uint32_t x1 = gi * 8 + 8 < r1 ? gi * 8 + 8 : r1;
-          bulk_g2s(Sb + mrg_off<W>(x0), src + (x0 - r0), (x1 - x0) * (uint32_t)sizeof(Rec<W>), &s_bar);
-        }
-      };
-      m.A.pieces(a0, a1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) { issue(src, cnt, at); });
-      m.B.pieces(b0, b1, [&](const Rec<W>* src, uint64_t cnt, uint64_t at) { issue(src, cnt, na_t + at); });
-    }
-    mbar_wait(&s_bar, 0);
-  } else {
-    constexpr int RW = sizeof(Rec<W>) / 8;
+  // ---- load the A and B slices into the padded layout: per-thread async
+  // 16-byte (8-byte) copies. (One bulk copy per 8-record group serialised on
+  // the SM's TMA unit: ~256 copies per tile.)
+  {
+    constexpr uint32_t RS = (uint32_t)sizeof(Rec<W>);
+    constexpr uint32_t CH = (RS % 16 == 0) ? 16u : 8u;
+    constexpr uint32_t NC = RS / CH;  // chunks per record
     auto copy = [&](uint32_t dst0) {
       return [&, dst0](const Rec<W>* src, uint64_t cnt, uint64_t at) {
-        const uint64_t* gs = reinterpret_cast<const uint64_t*>(src);
-        for (uint32_t i = tid; i < cnt * RW; i += kMergeThreads)
-          *reinterpret_cast<uint64_t*>(Sb + mrg_off<W>(dst0 + (uint32_t)at + i / RW) + 8 * (i % RW)) = gs[i];
+        const uint8_t* gs = reinterpret_cast<const uint8_t*>(src);
+        const uint32_t r0 = dst0 + (uint32_t)at;
+        for (uint32_t c = tid; c < (uint32_t)cnt * NC; c += kMergeThreads) {
+          uint8_t* d = Sb + mrg_off<W>(r0 + c / NC) + CH * (c % NC);
+          if (CH == 16) cp_async16(d, gs + 16ull * c);
+          else cp_async8(d, gs + 8ull * c);
+        }
       };
     };
     m.A.pieces(a0, a1, copy(0));
     m.B.pieces(b0, b1, copy(na_t));
+    cp_async_wait_all();
     __syncthreads();
   }
   // strict-order check of both slices (including the seam to the previous tile)
