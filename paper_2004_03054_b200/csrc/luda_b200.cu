@@ -270,7 +270,7 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& s
   auto launch = [&](const RunView<W>& A, uint64_t na, const RunView<W>& B, uint64_t nb, Rec<W>* out, uint64_t abase,
                     uint64_t bbase, bool resolve) -> int {
     const uint64_t ntiles = (na + nb + kMergeTile - 1) / kMergeTile;
-    GET(split, uint64_t, ntiles + 1, false);
+    GET(split, uint64_t, 3 * (ntiles + 1), false);
     merge_partition_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, st>>>(A, na, B, nb, ntiles, split);
     ++g_launches;
     MergeArgs<W> m{};

@@ -22,7 +22,7 @@
 namespace luda {
 
 constexpr int kMergeThreads = 256;
-constexpr int kMergeItems = 8;
+constexpr int kMergeItems = 6;
 constexpr int kMergeTile = kMergeThreads * kMergeItems;
 
 struct KeyBound {
@@ -87,6 +87,20 @@ struct RunView {
     }
     return l;
   }
+  // segment of logical g starting from a nearby segment (the merge partition
+  // stores each tile's starting segments, so CTAs never binary-search)
+  __device__ __forceinline__ uint32_t seg_near(uint64_t g, uint32_t s) const {
+    if (s >= nseg) s = nseg - 1;
+    while (s > 0 && lo[s] > g) --s;
+    while (s + 1 < nseg && lo[s + 1] <= g) ++s;
+    return s;
+  }
+  __device__ __forceinline__ const Rec<W>& at_near(uint64_t i, uint32_t s) const {
+    if (!lo) return base[off + i];
+    const uint64_t g = off + i;
+    s = seg_near(g, s);
+    return base[(uint64_t)s * cap + (g - lo[s])];
+  }
   __device__ __forceinline__ uint64_t phys(uint64_t i) const {
     if (!lo) return off + i;
     const uint64_t g = off + i;
@@ -96,7 +110,7 @@ struct RunView {
   __device__ __forceinline__ const Rec<W>& operator[](uint64_t i) const { return base[phys(i)]; }
   // f(physical pointer, count, destination offset) over the contiguous pieces of [i0, i1)
   template <typename F>
-  __device__ __forceinline__ void pieces(uint64_t i0, uint64_t i1, F f) const {
+  __device__ __forceinline__ void pieces(uint64_t i0, uint64_t i1, F f, uint32_t hint = ~0u) const {
     if (i0 >= i1) return;
     if (!lo) {
       f(base + off + i0, i1 - i0, 0ull);
@@ -104,7 +118,7 @@ struct RunView {
     }
     uint64_t g = off + i0;
     const uint64_t g1 = off + i1;
-    uint32_t s = seg(g);
+    uint32_t s = hint == ~0u ? seg(g) : seg_near(g, hint);
     uint64_t done = 0;
     while (g < g1) {
       const uint64_t e = lo[s + 1] < g1 ? lo[s + 1] : g1;
@@ -139,7 +153,11 @@ __global__ void merge_partition_kernel(RunView<W> A, uint64_t na, RunView<W> B, 
   if (t > ntiles) return;
   uint64_t diag = t * (uint64_t)kMergeTile;
   if (diag > na + nb) diag = na + nb;
-  split[t] = merge_split(A, na, B, nb, diag);
+  const uint64_t a = merge_split(A, na, B, nb, diag);
+  split[t] = a;
+  // starting segments of the tile's A / B slices (segmented views)
+  split[(ntiles + 1) + t] = A.lo ? A.seg(A.off + a) : 0u;
+  split[2 * (ntiles + 1) + t] = B.lo ? B.seg(B.off + (diag - a)) : 0u;
 }
 
 template <int W>
@@ -148,7 +166,7 @@ struct MergeArgs {
   uint64_t na;
   RunView<W> B;
   uint64_t nb;
-  const uint64_t* split;  // [ntiles+1]
+  const uint64_t* split;  // [3][ntiles+1]: A elements before each tile, then A / B starting segments
   uint64_t ntiles;
   Rec<W>* out;            // plain pass: out[0 .. na+nb); resolve pass: survivors
   uint64_t a_run_base, b_run_base;  // record index of A[0] / B[0] in the decoded array
@@ -200,6 +218,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   const uint64_t b0 = d0 - a0, b1 = d1 - a1;
   const uint32_t na_t = (uint32_t)(a1 - a0), nb_t = (uint32_t)(b1 - b0);
   const uint32_t nt = na_t + nb_t;
+  const uint32_t sa = (uint32_t)m.split[(m.ntiles + 1) + tile], sb = (uint32_t)m.split[2 * (m.ntiles + 1) + tile];
   // ---- load the A and B slices into the padded layout: per-thread async
   // 16-byte (8-byte) copies. (One bulk copy per 8-record group serialised on
   // the SM's TMA unit: ~256 copies per tile.)
@@ -218,8 +237,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
         }
       };
     };
-    m.A.pieces(a0, a1, copy(0));
-    m.B.pieces(b0, b1, copy(na_t));
+    m.A.pieces(a0, a1, copy(0), sa);
+    m.B.pieces(b0, b1, copy(na_t), sb);
     cp_async_wait_all();
     __syncthreads();
   }
@@ -232,7 +251,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     const Rec<W>& cur = SR(i);
     Rec<W> prev;
     if (li > 0) prev = SR(i - 1);
-    else prev = inA ? m.A[a0 - 1] : m.B[b0 - 1];
+    else prev = inA ? m.A.at_near(a0 - 1, sa) : m.B.at_near(b0 - 1, sb);
     if (rec_cmp(prev, cur) >= 0)
       atomicMin(m.err_order, (unsigned long long)((inA ? m.a_run_base : m.b_run_base) + gpos));
   }
@@ -268,10 +287,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
         has_prev = true;
       } else if (d0 > 0) {
         if (a0 > 0 && b0 > 0) {
-          const Rec<W> pa = m.A[a0 - 1], pb = m.B[b0 - 1];
+          const Rec<W> pa = m.A.at_near(a0 - 1, sa), pb = m.B.at_near(b0 - 1, sb);
           prev = rec_le(pa, pb) ? pb : pa;
         } else {
-          prev = a0 > 0 ? m.A[a0 - 1] : m.B[b0 - 1];
+          prev = a0 > 0 ? m.A.at_near(a0 - 1, sa) : m.B.at_near(b0 - 1, sb);
         }
         has_prev = true;
       }
