@@ -848,12 +848,19 @@ int luda_stream_wait_event(void* s, void* e) {
 int luda_crc32_batch(const void* data, const uint64_t* off, const uint32_t* len, uint32_t n, uint32_t* out,
                      void* stream) {
   if (n == 0) return LUDA_OK;
-  const size_t sm = sizeof(CrcSmem) + kCrcWarps * (kGroup + 192);
-  CK(cudaFuncSetAttribute(crc_ranges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  const unsigned grid = std::min<unsigned>((n + kCrcWarps - 1) / kCrcWarps, 4 * g_num_sms);
-  crc_ranges_kernel<<<grid, kCrcWarps * 32, sm, (cudaStream_t)stream>>>((const uint8_t*)data, off, len, n, out);
-  ++g_launches;
+  // (range, pass) items: prefix of per-range pass counts, then warps over items
+  // (stream-ordered scratch: concurrent callers on other streams never share it)
+  uint32_t* s_pstart = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&s_pstart), ((uint64_t)n + 1) * sizeof(uint32_t),
+                     (cudaStream_t)stream));
+  crc_plan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(len, n, s_pstart, out);
+  const size_t sm = sizeof(CrcSmem) + kCrcFlatWarps * (kGroup + 192);
+  CK(cudaFuncSetAttribute(crc_flat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  crc_flat_kernel<<<g_num_sms, kCrcFlatWarps * 32, sm, (cudaStream_t)stream>>>((const uint8_t*)data, off, len, n,
+                                                                              s_pstart, out);
+  g_launches += 2;
   CK(cudaGetLastError());
+  CK(cudaFreeAsync(s_pstart, (cudaStream_t)stream));
   return LUDA_OK;
 }
 

@@ -202,9 +202,12 @@ __device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint6
   }
   __syncwarp();
   uint8_t* base = stage + ((uintptr_t)((int64_t)gA + lo) - w0);  // smem addr of data index lo
-  if (lo < 0) {  // prepare: zero data indices [lo-8, 0), complement [0, 4)
+  if (lo0 < 4) {
+    // prepare: zero data indices [lo-8, 0); complement the bytes of [0, 4)
+    // (the preset) that THIS pass reads, [max(0, hi - kGroup), hi) — a pass
+    // boundary may fall inside the first word
     for (int64_t i = lo - 8 + lane; i < 0; i += 32) base[i - lo] = 0;
-    if (lane < 4 && (uint64_t)lane < n) base[lane - lo] ^= 0xFFu;
+    if (lane < 4 && (uint64_t)lane < n && (int64_t)lane >= lo0 && (int64_t)lane < hi) base[lane - lo] ^= 0xFFu;
     __syncwarp();
   }
   const uint32_t v = warp_xor(pass_lane_value(base - lo, n, (uint32_t)q, cs, base));
@@ -238,6 +241,78 @@ __global__ void __launch_bounds__(kCrcWarps * 32) crc_ranges_kernel(const uint8_
       acc = ~raw;
     }
     if (lane == 0) out[r] = acc;
+  }
+}
+
+// Many ranges, flattened: work item = (range, pass). pstart[r] = first item of
+// range r (exclusive prefix of max(1, ceil(len/kGroup))), pstart[n] = total.
+// Each warp takes a contiguous run of items (one binary search, then a forward
+// walk) and XORs its pass values into out[r] (pre-set to 0xFFFFFFFF by
+// crc_plan_kernel), so every pass's loads are in flight on their own warp
+// instead of queueing behind the range's earlier passes.
+constexpr int kCrcFlatWarps = 16;
+__global__ void __launch_bounds__(1024) crc_plan_kernel(const uint32_t* len, uint32_t n, uint32_t* pstart,
+                                                        uint32_t* out) {
+  __shared__ uint32_t s_sum[1024];
+  const uint32_t t = threadIdx.x;
+  const uint32_t per = (n + 1023) / 1024;
+  const uint32_t r0 = t * per, r1 = min(n, r0 + per);
+  uint32_t sum = 0;
+  for (uint32_t r = r0; r < r1; ++r) {
+    const uint32_t L = len[r];
+    sum += L < 4 ? 1u : (L + kGroup - 1) / kGroup;
+    out[r] = 0xFFFFFFFFu;
+  }
+  s_sum[t] = sum;
+  __syncthreads();
+  for (uint32_t o = 1; o < 1024; o <<= 1) {
+    const uint32_t v = t >= o ? s_sum[t - o] : 0u;
+    __syncthreads();
+    s_sum[t] += v;
+    __syncthreads();
+  }
+  uint32_t acc = s_sum[t] - sum;
+  for (uint32_t r = r0; r < r1; ++r) {
+    pstart[r] = acc;
+    const uint32_t L = len[r];
+    acc += L < 4 ? 1u : (L + kGroup - 1) / kGroup;
+  }
+  if (t == 1023) pstart[n] = s_sum[1023];
+}
+
+__global__ void __launch_bounds__(kCrcFlatWarps * 32) crc_flat_kernel(const uint8_t* arena, const uint64_t* addr,
+                                                                      const uint32_t* len, uint32_t nranges,
+                                                                      const uint32_t* pstart, uint32_t* out) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
+  uint8_t* stage = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * (kGroup + 192);
+  crc_smem_init(cs);
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint32_t total = pstart[nranges];
+  const uint32_t nw = gridDim.x * kCrcFlatWarps, gw = blockIdx.x * kCrcFlatWarps + (threadIdx.x >> 5);
+  const uint32_t chunk = (total + nw - 1) / nw;
+  const uint32_t i0 = gw * chunk, i1 = min(total, i0 + chunk);
+  if (i0 >= i1) return;
+  uint32_t l = 0, h = nranges;  // largest r with pstart[r] <= i0
+  while (h - l > 1) {
+    const uint32_t mid = (l + h) >> 1;
+    if (pstart[mid] <= i0) l = mid;
+    else h = mid;
+  }
+  uint32_t r = l, rend = pstart[r + 1];
+  for (uint32_t i = i0; i < i1; ++i) {
+    while (i >= rend) rend = pstart[++r + 1];
+    const uint8_t* g = arena + addr[r];
+    const uint32_t n = len[r];
+    uint32_t v;
+    if (n < 4) {
+      v = 0;
+      if (lane == 0) v = crc32_bytes(g, n, crc_lane(cs, 0)) ^ 0xFFFFFFFFu;
+    } else {
+      v = warp_crc_pass_global(g, n, i - pstart[r], stage, cs);
+    }
+    if (lane == 0 && v) atomicXor(out + r, v);
   }
 }
 

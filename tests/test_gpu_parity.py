@@ -57,10 +57,46 @@ def test_crc32_kat_and_random(native):
     assert gpu_crc(native, b"") == 0
     rng = random.Random(7)
     for n in (1, 2, 3, 4, 5, 7, 8, 131, 132, 133, 263, 264, 265, 1000, 4095, 4096, 4223, 4224, 4225, 8448,
+              4607, 4608, 4609, 9216, 13824,
               10025, 65537, 1 << 20, (1 << 22) + 3):
         for pad in (0, 1, 3, 13):
             b = rng.randbytes(n)
             assert gpu_crc(native, b, pad) == zlib.crc32(b), (n, pad)
+
+
+def test_crc32_batch_many_ranges(native):
+    """luda_crc32_batch ((range, pass) work items over all warps) vs zlib on
+    ranges of every size class, unaligned offsets, empty and 1-3 byte ranges."""
+    import numpy as np
+    rng = random.Random(11)
+    lens = [0, 1, 2, 3, 4, 5, 9, 4607, 4608, 4609, 9216, 33000, 34011, 100003] + \
+        [rng.randrange(0, 70000) for _ in range(300)]
+    blob = bytearray()
+    offs = []
+    for n in lens:
+        blob += bytes(rng.randrange(0, 16))  # misalign the next range
+        offs.append(len(blob))
+        blob += rng.randbytes(n)
+    p = ctypes.c_void_p()
+    assert native.luda_region_alloc(len(blob) + 64, ctypes.byref(p)) == 0
+    try:
+        buf = ctypes.create_string_buffer(bytes(blob), len(blob))
+        assert native.luda_stage_in_async(p.value, buf, len(blob), None) == 0
+        import torch
+        d_off = torch.tensor(offs, dtype=torch.int64, device="cuda")
+        d_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+        d_out = torch.zeros(len(lens), dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        c_u64p, c_u32p = ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)
+        assert native.luda_crc32_batch(p.value, ctypes.cast(d_off.data_ptr(), c_u64p),
+                                       ctypes.cast(d_len.data_ptr(), c_u32p), len(lens),
+                                       ctypes.cast(d_out.data_ptr(), c_u32p), None) == 0
+        torch.cuda.synchronize()
+        got = d_out.cpu().numpy().astype(np.uint32).tolist()
+        want = [zlib.crc32(bytes(blob[o:o + n])) for o, n in zip(offs, lens)]
+        assert got == want
+    finally:
+        native.luda_region_free(p.value)
 
 
 def build(name):
