@@ -2,20 +2,22 @@
 //
 // CRC-32/IEEE (reflected 0xEDB88320, init/xorout 0xFFFFFFFF; the zlib flavour
 // of checksum.py:12-13) is computed warp-parallel: a byte range is cut into
-// END-ALIGNED 36-byte segments (9 words). In one pass a warp covers 128
-// segments (4608 B): lane d owns the segments at distance d, d+32, d+64, d+96
-// from the pass end and runs their four table chains interleaved (4-way ILP:
-// the chains are latency-bound, two dependent LDS per word). Segment
+// END-ALIGNED 44-byte segments (11 words). In one pass a warp covers 96
+// segments (4224 B — a whole 4 KiB block plus the alignment pad, so a typical
+// block is one pass with ~4% idle segments): lane d owns the segments at
+// distance d, d+32, d+64 from the pass end and runs their three table chains
+// interleaved (3-way ILP: the chains are latency-bound, two dependent LDS per
+// word). Segment
 // registers are combined with the GF(2) "advance over n zero bytes" operator
 // Z_n (the crc32_combine algebra: raw(A∥B) = Z_|B|(raw(A)) ^ raw(B)), by
-// Horner over the lane's chains with H = Z_1152:
-//   lane value = Z_{36d}( r_d ^ H(r_{d+32} ^ H(r_{d+64} ^ H(r_{d+96}))) ), XOR over lanes.
+// Horner over the lane's chains with H = Z_1408:
+//   lane value = Z_{44d}( r_d ^ H(r_{d+32} ^ H(r_{d+64})) ), XOR over lanes.
 // Words go through SLICING-BY-2 tables (two 16-bit steps per word). The two
 // byte tables T1 (byte then a zero byte) and T0 are replicated once per lane
 // and interleaved so that one PRMT forms the whole shared-memory offset:
 //   offset = idx << 8 | table << 7 | lane << 2      (64 KB, bank = lane)
 // i.e. per 2 bytes: 2 PRMT + 2 LDS + SHF + LOP3, no bank conflicts.
-// 9 words (odd) per segment makes the 32 lanes' LDS.32 data streams hit 32
+// 11 words (odd) per segment makes the 32 lanes' LDS.32 data streams hit 32
 // distinct banks. The ~0 preset is folded into the data: callers run
 // crc_prep() on the smem copy (zero the 72 bytes before it, complement the
 // first 4 bytes: F(~0, D) = F(0, D') and leading zeros leave a zero register
@@ -27,20 +29,20 @@
 namespace luda {
 
 constexpr uint32_t kCrcPoly = 0xEDB88320u;
-constexpr int kSeg = 36;             // bytes per CRC segment
-constexpr int kSegWords = kSeg / 4;  // 9 (odd: the lanes' word streams hit distinct banks)
-constexpr int kChains = 4;           // segments (independent table chains) per lane per pass
-constexpr int kHalf = 32 * kSeg;     // 1152: distance between a lane's consecutive segments
-constexpr int kGroup = 32 * kChains * kSeg;  // 4608: bytes one warp covers per pass
+constexpr int kSeg = 44;             // bytes per CRC segment
+constexpr int kSegWords = kSeg / 4;  // 11 (odd: the lanes' word streams hit distinct banks)
+constexpr int kChains = 3;           // segments (independent table chains) per lane per pass
+constexpr int kHalf = 32 * kSeg;     // 1408: distance between a lane's consecutive segments
+constexpr int kGroup = 32 * kChains * kSeg;  // 4224: bytes one warp covers per pass (>= a 4 KiB block + pad)
 constexpr int kCrcLead = 72;         // zeroed bytes required before the data
 
 // ---- tables (device globals; initialised by luda_init) ---------------------
 // g_crc_tab[b]          : byte table T0[b]
 // g_crc_tab1[b]         : T1[b] = T0 advanced over one more (zero) byte
-// g_seg_nib[n][v][d]    : Z_{36*d}(v << 4n)    (8 x 16 x 32 words)
-// g_half_tab[k][b]      : Z_1152(b << 8k)     (4 x 256 words)
+// g_seg_nib[n][v][d]    : Z_{44*d}(v << 4n)    (8 x 16 x 32 words)
+// g_half_tab[k][b]      : Z_1408(b << 8k)     (4 x 256 words)
 // c_zpow[i][j]          : Z_{2^i}(1 << j)      (48 x 32 words) for arbitrary shifts
-// c_zgroup[j]           : Z_4608(1 << j)       (one warp pass)
+// c_zgroup[j]           : Z_4224(1 << j)       (one warp pass)
 // (single translation unit: luda_b200.cu includes every stage header)
 __device__ uint32_t g_crc_tab[256];
 __device__ uint32_t g_crc_tab1[256];
@@ -105,7 +107,7 @@ __device__ __forceinline__ uint32_t crc_byte(uint32_t c, uint32_t b, const CrcLa
   return crc_lut(t, prmt(c ^ b, t.a0, 0x7604u)) ^ (c >> 8);  // T0[(c ^ b) & 0xFF] ^ (c >> 8)
 }
 
-// Z_{36*lane}(c) via the lane's nibble tables. `nl` = s.nib + lane.
+// Z_{44*lane}(c) via the lane's nibble tables. `nl` = s.nib + lane.
 __device__ __forceinline__ uint32_t seg_shift(uint32_t c, const uint32_t* __restrict__ nl) {
   uint32_t r = 0;
 #pragma unroll
@@ -113,7 +115,7 @@ __device__ __forceinline__ uint32_t seg_shift(uint32_t c, const uint32_t* __rest
   return r;
 }
 
-// Z_1152(c) (byte tables).
+// Z_1408(c) (byte tables).
 __device__ __forceinline__ uint32_t half_shift(uint32_t c, const uint32_t* __restrict__ ht) {
   return ht[c & 0xFFu] ^ ht[256 + ((c >> 8) & 0xFFu)] ^ ht[512 + ((c >> 16) & 0xFFu)] ^ ht[768 + (c >> 24)];
 }
@@ -171,7 +173,7 @@ __device__ __forceinline__ uint32_t lane_combine(const uint32_t (&r)[kChains], c
 
 // Warp: un-combined pass value of pass q over prepared smem data of length n:
 // this lane's combined chains before the cross-lane XOR, with segment
-// distances d = lane + 32c + 128q (pass q covers distances [128q, 128q+128)).
+// distances d = lane + 32c + 96q (pass q covers distances [96q, 96q+96)).
 __device__ __forceinline__ uint32_t pass_lane_value(const uint8_t* data, uint64_t n, uint32_t q, const CrcSmem& cs,
                                                     const uint8_t* safe) {
   const uint32_t lane = lane_id();
@@ -181,7 +183,7 @@ __device__ __forceinline__ uint32_t pass_lane_value(const uint8_t* data, uint64_
   bool val[kChains];
 #pragma unroll
   for (int c = 0; c < kChains; ++c) {
-    const int64_t dd = (int64_t)lane + 32 * c + 128 * (int64_t)q;
+    const int64_t dd = (int64_t)lane + 32 * c + 32 * kChains * (int64_t)q;
     val[c] = dd < nseg;
     sp[c] = seg_ptr(val[c] ? data + ((int64_t)n - (int64_t)kSeg * (dd + 1)) : safe);  // `safe`: any readable smem
   }
@@ -234,7 +236,7 @@ __device__ __forceinline__ uint32_t pass_lane_value_al(const uint8_t* end, uint3
   bool val[kChains];
 #pragma unroll
   for (int c = 0; c < kChains; ++c) {
-    const int32_t dd = (int32_t)lane + 32 * c + 128 * (int32_t)q;
+    const int32_t dd = (int32_t)lane + 32 * c + 32 * kChains * (int32_t)q;
     val[c] = dd < nseg;
     p[c] = reinterpret_cast<const uint32_t*>(end - kSeg * (val[c] ? dd + 1 : 1));
   }

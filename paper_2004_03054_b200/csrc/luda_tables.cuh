@@ -3,8 +3,8 @@
 // Host code computes, once per process (luda_init):
 //   g_crc_tab   byte table of the reflected polynomial 0xEDB88320
 //   g_crc_tab1  slicing-by-2 partner table (byte, then a zero byte)
-//   g_seg_nib   nibble tables of Z_{36*d}, d = 0..31 (segment combine)
-//   g_half_tab  byte tables of Z_1152 (between a lane's segments)
+//   g_seg_nib   nibble tables of Z_{kSeg*d}, d = 0..31 (segment combine)
+//   g_half_tab  byte tables of Z_kHalf (between a lane's segments)
 //   c_zpow      columns of Z_{2^i}, i = 0..47 (arbitrary shifts)
 //   c_zgroup    columns of Z_4352 (one warp pass)
 // where Z_n advances a raw CRC register over n zero bytes (the operator
