@@ -502,7 +502,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   const uint32_t s_edbg = getenv("LUDA_ENC_DBG") ? (uint32_t)atoi(getenv("LUDA_ENC_DBG")) : 0u;
   EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off,
                    blk_out, res->out, s_edbg};
-  const size_t esm = sizeof(CrcSmem) + (size_t)kEncPairs * sizeof(EncPairSmem);
+  const size_t esm = sizeof(CrcSmem) + (size_t)kEncPairs * sizeof(EncPairSmem) + sizeof(EncCtaSmem);
   CK(cudaFuncSetAttribute(encode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
   const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncPairs - 1) / kEncPairs, (uint64_t)g_num_sms);
   KT_START(3, st);
@@ -1110,4 +1110,15 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   return LUDA_OK;
 }
 
+#ifdef ENC_TIMING
+// instrumentation build only: accumulated encode builder/CRC warp section cycles
+int luda_dbg_enc_timing(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, luda::g_enc_t, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(luda::g_enc_t, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 }  // extern "C"

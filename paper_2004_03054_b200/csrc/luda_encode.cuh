@@ -27,7 +27,7 @@ namespace luda {
 
 // Pairs: a BUILDER warp (records, layout, value TMA, assembly) and a CRC warp
 // (CRC + copy-out) hand assembled blocks over through two buffers.
-constexpr int kEncPairs = 9;
+constexpr int kEncPairs = 10;
 constexpr int kEncWarps = 2 * kEncPairs;
 constexpr int kEncStage = 4608;                        // blocks up to this size are assembled in smem
 constexpr int kEncPre = 160;
@@ -43,12 +43,18 @@ struct alignas(16) EncPairSmem {
   uint8_t buf[2][kEncBuf];
   uint8_t stg[kEncStg];
   uint64_t bar;                 // value TMA
-  uint32_t pre[128 + kCopyMap / 4];  // copy scratch (512 B + map)
   uint64_t full[2], empty[2];
   EncMeta meta[2];
 };
+// Per-CTA copy scratch of the generic (rare) block path, taken under a lock
+// so the pairs need not each carry 1 KB.
+struct alignas(16) EncCtaSmem {
+  uint32_t pre[128 + kCopyMap / 4];  // 512 B + chunk map
+  int lock;
+};
 static_assert(kEncStg / 16 <= kCopyMap, "copy map smaller than the staging chunk count");
-static_assert(sizeof(CrcSmem) + kEncPairs * sizeof(EncPairSmem) <= 232448, "encode smem over the 227 KB limit");
+static_assert(sizeof(CrcSmem) + kEncPairs * sizeof(EncPairSmem) + sizeof(EncCtaSmem) <= 232448,
+              "encode smem over the 227 KB limit");
 static_assert(sizeof(EncPairSmem) % 16 == 0 && kEncBuf % 16 == 0, "TMA / vector alignment");
 
 // Copy n bytes src → dst (any alignment; dst generic: smem or global) with
@@ -391,6 +397,25 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
   __syncwarp();
 }
 
+// Section timing (instrumentation builds only: -DENC_TIMING, read with
+// luda_dbg_enc_timing / profiles/encode_timing.py): per-warp clock64 deltas
+// accumulated in shared memory, flushed once per warp.
+#ifdef ENC_TIMING
+__device__ unsigned long long g_enc_t[16];
+__shared__ unsigned long long s_enc_t[kEncWarps][16];
+#define ENC_T(i)                                                              \
+  do {                                                                        \
+    __syncwarp();                                                             \
+    const unsigned long long t_ = clock64();                                  \
+    if (lane_id() == 0) s_enc_t[threadIdx.x >> 5][i] += t_ - t_last;         \
+    t_last = t_;                                                              \
+  } while (0)
+#define ENC_T0() unsigned long long t_last = clock64()
+#else
+#define ENC_T(i) do {} while (0)
+#define ENC_T0() do {} while (0)
+#endif
+
 // ---- software-pipelined fast path ------------------------------------------------
 // Blocks of <= 32 entries whose value windows fit the staging area (every
 // BASELINE shape): lane i owns entry i. While block k is finished (CRC +
@@ -509,8 +534,10 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   }
   if (lane == 0) put_u32(dst + entries_end + 4 * nres, nres);
   __syncwarp();  // headers/keys written before values (edge words are read-modified-written)
+  ENC_T0();
   mbar_wait(bar, phase);
   phase ^= 1u;
+  ENC_T(4);
   const uint32_t soff = e.soff;
   // each lane realigns its own value (no chunk map; edge words of neighbouring
   // entries are >= 12 bytes apart, so the per-word read-modify-writes never race)
@@ -518,6 +545,7 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
     value_copy16(sbase, stg, (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s), soff, e.vl, 0u, false, 0u,
                  false);
   __syncwarp();
+  ENC_T(5);
 }
 
 // CRC + 16-byte copy-out of an assembled (staged) block
@@ -558,7 +586,12 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
   const bool builder = warp < kEncPairs;
   const uint32_t p = warp % kEncPairs;
   EncPairSmem& ps = pairs[p];
+  EncCtaSmem& cta = *reinterpret_cast<EncCtaSmem*>(smem_raw + sizeof(CrcSmem) + kEncPairs * sizeof(EncPairSmem));
+  if (threadIdx.x == 0) cta.lock = 0;
   crc_smem_init(cs);
+#ifdef ENC_TIMING
+  if (lane < 16) s_enc_t[warp][lane] = 0;
+#endif
   if (builder && lane == 0) {
     mbar_init(&ps.bar, 1);
     for (int b = 0; b < 2; ++b) {
@@ -578,21 +611,32 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
     for (uint32_t i = 0; cur.valid; ++i) {
       const uint32_t b = i & 1u;
       uint8_t* wbuf = ps.buf[b];
+      ENC_T0();
       if (i >= 2) mbar_wait(&ps.empty[b], ((i - 2) >> 1) & 1u);  // the CRC warp is done with block i-2
+      ENC_T(0);
       enc_load(a, cur.k + nw, nxt);  // records of the next block: loads in flight
+      ENC_T(1);
       EncMeta mt{cur.out_off, cur.size, 0u};
       if (cur.fast) {
-        enc_assemble(a, cur, wbuf, ps.stg, &ps.bar, phase, ps.pre);
+        enc_assemble(a, cur, wbuf, ps.stg, &ps.bar, phase, nullptr);
+        ENC_T(2);
         enc_layout(a, nxt);  // staging is free again: start the next block's value gather
+        ENC_T(3);
         if (nxt.fast) enc_issue(a, nxt, ps.stg, &ps.bar);
+        ENC_T(6);
       } else {
         const uint32_t k = cur.k;
+        if (lane == 0)
+          while (atomicCAS(&cta.lock, 0, 1) != 0) __nanosleep(64);
+        __syncwarp();
         if (cur.size <= (uint32_t)kEncStage)
           encode_one_block<W, true>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, ps.stg, &ps.bar, phase,
-                                    ps.pre, cs);
+                                    cta.pre, cs);
         else
           encode_one_block<W, false>(a, k, cur.first, cur.cnt, cur.size, cur.out_off, wbuf, ps.stg, &ps.bar, phase,
-                                     ps.pre, cs);
+                                     cta.pre, cs);
+        __syncwarp();
+        if (lane == 0) atomicExch(&cta.lock, 0);
         mt.skip = 1;
         enc_layout(a, nxt);
         if (nxt.fast) enc_issue(a, nxt, ps.stg, &ps.bar);
@@ -601,12 +645,15 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps.full[b]);  // release: the assembled block and its meta
       cur = nxt;
+      ENC_T(7);
     }
   } else {
     // CRC warp: CRC + copy-out of the blocks the builder assembled, in order
     for (uint32_t i = 0, k = gw; k < a.nblk; ++i, k += nw) {
       const uint32_t b = i & 1u;
+      ENC_T0();
       mbar_wait(&ps.full[b], (i >> 1) & 1u);
+      ENC_T(8);
       const EncMeta mt = ps.meta[b];
       if (!mt.skip) {
         EncLane<W> e;
@@ -614,10 +661,15 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
         e.size = mt.size;
         enc_finish(a, e, ps.buf[b], cs);
       }
+      ENC_T(9);
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps.empty[b]);
     }
   }
+#ifdef ENC_TIMING
+  __syncwarp();
+  if (lane < 16) atomicAdd(&g_enc_t[lane], s_enc_t[warp][lane]);
+#endif
 }
 
 // ---- per-SST filter + index + footer -----------------------------------------------------
