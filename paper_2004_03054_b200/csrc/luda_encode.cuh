@@ -564,9 +564,14 @@ __device__ __forceinline__ void enc_finish(const EncodeArgs<W>& a, const EncLane
   const uint32_t nch = (uint32_t)((g1 - g0) >> 4);
   const uint32_t c_first = (g0 == g) ? 0u : 1u;
   const uint32_t c_last = ((g + size) & 15u) ? nch - 1 : nch;  // exclusive
-  if (!(a.dbg & 2))
-  for (uint32_t c = c_first + lane; c < c_last; c += 32)
-    *reinterpret_cast<uint4*>(g0 + 16ull * c) = *reinterpret_cast<const uint4*>(sbase + 16 * c);
+  // interior 16-byte chunks: one TMA bulk store (the smem reads leave the LSU
+  // pipe); the caller waits for its smem reads before releasing the buffer
+  fence_proxy_async_smem();  // every lane's smem writes (CRC prep/unprep, CRC word) → async proxy
+  __syncwarp();
+  if (!(a.dbg & 2) && lane == 0 && c_last > c_first) {
+    bulk_s2g(reinterpret_cast<void*>(g0 + 16ull * c_first), sbase + 16 * c_first, 16u * (c_last - c_first));
+    bulk_commit();
+  }
   {
     const uint32_t c = lane < 16 ? 0u : nch - 1;
     const bool partial = lane < 16 ? (c_first == 1) : (c_last == nch - 1 && !(c == 0 && c_first == 1));
@@ -642,6 +647,7 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
         if (nxt.fast) enc_issue(a, nxt, ps.stg, &ps.bar);
       }
       if (lane == 0) ps.meta[b] = mt;
+      fence_proxy_async_smem();  // the assembled bytes are read by the CRC warp's bulk store
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps.full[b]);  // release: the assembled block and its meta
       cur = nxt;
@@ -660,11 +666,13 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
         e.out_off = mt.out_off;
         e.size = mt.size;
         enc_finish(a, e, ps.buf[b], cs);
+        if (lane == 0) bulk_wait_read0();  // the bulk store has read the buffer
       }
       ENC_T(9);
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps.empty[b]);
     }
+    if (lane == 0) bulk_wait0();
   }
 #ifdef ENC_TIMING
   __syncwarp();
