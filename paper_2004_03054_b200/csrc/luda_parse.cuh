@@ -176,11 +176,12 @@ __global__ void parse_files_a(ParseArgs a) {
 // Warp CRC contribution of pass q (segments at distances [64q, 64q+64) from
 // the end) of the n-byte range at global address g, staged through the
 // warp's smem buffer `stage` (>= kGroup + 160 bytes, 16-aligned). Returns
-// Z_{4352 q}(pass raw); the XOR over all passes of a range is its raw
+// the pass's raw register (not yet advanced over the kGroup·q bytes after
+// the pass); Z_{kGroup q} of it XORed over all passes is the range's raw
 // register with the ~0 preset folded in (the staged copy is prepared:
 // bytes before the range are zeroed, its first 4 bytes complemented).
 template <bool kCg = false>
-__device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint64_t n, uint64_t q,
+__device__ __forceinline__ uint32_t warp_crc_pass_global_raw(const uint8_t* g, uint64_t n, uint64_t q,
                                                          uint8_t* stage, const CrcSmem& cs) {
   const uint32_t lane = lane_id();
   const int64_t hi = (int64_t)n - (int64_t)kGroup * (int64_t)q;          // pass end (data index)
@@ -212,7 +213,14 @@ __device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint6
   }
   const uint32_t v = warp_xor(pass_lane_value(base - lo, n, (uint32_t)q, cs, base));
   __syncwarp();
-  return crc_shift(v, (uint64_t)kGroup * q);
+  return v;
+}
+
+// Pass q's contribution, already advanced over the kGroup·q bytes after it.
+template <bool kCg = false>
+__device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint64_t n, uint64_t q,
+                                                         uint8_t* stage, const CrcSmem& cs) {
+  return crc_shift(warp_crc_pass_global_raw<kCg>(g, n, q, stage, cs), (uint64_t)kGroup * q);
 }
 
 // Stage B: CRC of many ranges; warp per range, looping passes. out[i] = crc.
@@ -300,19 +308,27 @@ __global__ void __launch_bounds__(kCrcFlatWarps * 32) crc_flat_kernel(const uint
     if (pstart[mid] <= i0) l = mid;
     else h = mid;
   }
-  uint32_t r = l, rend = pstart[r + 1];
-  for (uint32_t i = i0; i < i1; ++i) {
-    while (i >= rend) rend = pstart[++r + 1];
+  // per range: this warp's passes q_hi..q_lo by Horner (Z_kGroup between
+  // passes), one arbitrary shift by kGroup·q_lo at the end
+  uint32_t r = l;
+  for (uint32_t i = i0; i < i1;) {
+    while (i >= pstart[r + 1]) ++r;
+    const uint32_t ge = min(i1, pstart[r + 1]);
     const uint8_t* g = arena + addr[r];
     const uint32_t n = len[r];
-    uint32_t v;
+    uint32_t v = 0;
     if (n < 4) {
-      v = 0;
       if (lane == 0) v = crc32_bytes(g, n, crc_lane(cs, 0)) ^ 0xFFFFFFFFu;
     } else {
-      v = warp_crc_pass_global(g, n, i - pstart[r], stage, cs);
+      const uint32_t q_lo = i - pstart[r], q_hi = ge - 1 - pstart[r];
+      for (int q = (int)q_hi; q >= (int)q_lo; --q) {
+        const uint32_t x = warp_crc_pass_global_raw<false>(g, n, (uint64_t)q, stage, cs);
+        v = (q == (int)q_hi) ? x : (gf2_apply(c_zgroup, v) ^ x);
+      }
+      v = crc_shift(v, (uint64_t)kGroup * q_lo);
     }
     if (lane == 0 && v) atomicXor(out + r, v);
+    i = ge;
   }
 }
 
