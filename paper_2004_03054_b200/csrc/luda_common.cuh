@@ -346,8 +346,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Order this thread's earlier generic-proxy smem accesses before later
-// async-proxy (TMA) writes to the same smem.
 // smem → global bulk copy (TMA store; 16-byte aligned addresses and size),
 // tracked by the issuing thread's bulk async-group.
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
@@ -361,6 +359,8 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 // every committed bulk store is complete (its global writes performed)
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Order this thread's earlier generic-proxy smem accesses before later
+// async-proxy (TMA) accesses to the same smem.
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
