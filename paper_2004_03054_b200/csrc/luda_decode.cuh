@@ -166,6 +166,23 @@ __device__ __forceinline__ int32_t interval_positions(const uint8_t* d, uint32_t
   return p == e ? j : -1;
 }
 
+// interval_positions into a lane's 16 slots: slot j & 15 (an interval with
+// more than 16 entries overwrites its own slots, but then the block leaves
+// the slot fast path), no predicate or running position in the loop.
+__device__ __forceinline__ int32_t interval_positions_slots(const uint8_t* d, uint32_t start, uint32_t end,
+                                                            uint32_t* mine) {
+  uint32_t pos = start;
+  uint32_t j = 0;
+  while (pos < end) {
+    const uint8_t* h = d + pos;
+    const uint32_t u = h[1], b2 = h[2], b3 = h[3];
+    mine[j & (kDecStride - 1)] = pos;
+    pos += (3u + u + b2) + (b2 >> 7) * (b3 * 128u - 127u);
+    ++j;
+  }
+  return pos == end ? (int32_t)j : -1;
+}
+
 // Exact sequential decode_data_block walk (blocks.py:151-164). Returns the
 // reference error code (0 ok) and sets `unsup` for envelope violations.
 template <typename Emit>
@@ -270,9 +287,7 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
         uint32_t* pos32 = reinterpret_cast<uint32_t*>(slots);
         if (lane < nres && ok) {
           uint32_t* mine = pos32 + kDecStride * lane;
-          st.my_cnt = interval_positions(d, st.my_st, st.my_en, [&](int32_t j, uint32_t pos) {
-            if (j < kDecStride) mine[j] = pos;
-          });
+          st.my_cnt = interval_positions_slots(d, st.my_st, st.my_en, mine);
           ok = st.my_cnt >= 0 && st.my_cnt <= kDecStride;
         }
         DEC_T(1);
