@@ -250,7 +250,16 @@ __device__ unsigned long long g_dec_t[16];
 #define DEC_T0() do {} while (0)
 #endif
 
-template <int W>
+// u32le at p: staged blocks (smem with slack after the window) use two
+// aligned word loads + PRMT; blocks read from global keep byte loads (never
+// past the block's end).
+template <bool kStaged>
+__device__ __forceinline__ uint32_t dec_ld32(const uint8_t* p) {
+  if (kStaged) return ld_u32_any(p);
+  return ld_u32_le(p);
+}
+
+template <int W, bool kStaged>
 __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t b, uint64_t addr, uint32_t blen,
                                                const uint8_t* d, DecSlot* slots) {
   const uint32_t lane = lane_id();
@@ -262,7 +271,7 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
   const uint32_t len = st.len;
   st.code = len < 12 ? (uint32_t)B_SHORT : 0u;
   if (!st.code) {
-    st.nres = ld_u32_le(d + len - 8);
+    st.nres = dec_ld32<kStaged>(d + len - 8);
     st.entries_end = (int64_t)len - 8 - 4 * (int64_t)st.nres;
     st.restart_bad = st.nres < 1 || st.entries_end < 0;
   }
@@ -274,8 +283,8 @@ __device__ __forceinline__ DecState dec_phase1(const DecodeArgs<W>& a, uint32_t 
       bool ok = true;
       const bool single = nres <= (uint32_t)kDecSlotIntervals;
       if (lane < nres) {
-        st.my_st = ld_u32_le(d + entries_end + 4 * lane);
-        st.my_en = (lane + 1 < nres) ? ld_u32_le(d + entries_end + 4 * (lane + 1)) : (uint32_t)entries_end;
+        st.my_st = dec_ld32<kStaged>(d + entries_end + 4 * lane);
+        st.my_en = (lane + 1 < nres) ? dec_ld32<kStaged>(d + entries_end + 4 * (lane + 1)) : (uint32_t)entries_end;
         ok = (lane != 0 || st.my_st == 0) && st.my_st < st.my_en && (int64_t)st.my_en <= entries_end;
       }
       DEC_T(0);
@@ -667,11 +676,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       if (!(a.dbg & 4)) {
         if (mt.staged) {
           const uint8_t* d = ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15);
-          DecState stt = dec_phase1(a, b, mt.addr, mt.len, d, slots);
+          DecState stt = dec_phase1<W, true>(a, b, mt.addr, mt.len, d, slots);
           dec_phase2<W, true>(a, b, stt, seg0 + cnt, seg1, d, slots);
           n = stt.n;
         } else {
-          DecState stt = dec_phase1(a, b, mt.addr, mt.len, gp, slots);
+          DecState stt = dec_phase1<W, false>(a, b, mt.addr, mt.len, gp, slots);
           dec_phase2<W, false>(a, b, stt, seg0 + cnt, seg1, gp, slots);
           n = stt.n;
         }
@@ -697,7 +706,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
         if (st_ok) {
           uint8_t* wstart = ps.slot[s] + kDecLead;
           uint8_t* d = wstart + (reinterpret_cast<uintptr_t>(gp) & 15);
-          stored = ld_u32_le(d + len - 4);
+          stored = ld_u32_any(d + len - 4);
           __syncwarp();
           crc = dec_crc_staged(wstart, d, len - 4, cs);
         } else {
