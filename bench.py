@@ -38,6 +38,17 @@ CONFIGS = {
 }
 
 METRIC = "compaction input MB/s"
+
+
+def workload_text(keys, world):
+    """The c3 description with the actual job size (--keys other than 2^25 is a smaller c3-shaped job)."""
+    t = CONFIGS["c3"]
+    if keys != 1 << 25:
+        t = t.replace("64M KV pairs", f"{2 * keys / 2**20:g}M KV pairs (c3-shaped, reduced from 64M)")
+    if world > 1:
+        t = t.replace(", 1 B200", "") + (f" per GPU; global job = {world} key-range shards "
+                                         "(5th BASELINE config's subcompaction scheme)")
+    return t
 MIB4 = 4 * 2**20
 
 
@@ -582,9 +593,7 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "MB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": CONFIGS["c3"] if world == 1 else
-                   CONFIGS["c3"].replace(", 1 B200", "") + f" per GPU; global job = {world} key-range shards "
-                   f"(5th BASELINE config's subcompaction scheme)", "keys_per_run": args.keys, "n_in": n_in, "n_out": n_out,
+        "config": {"workload": workload_text(args.keys, world), "keys_per_run": args.keys, "n_in": n_in, "n_out": n_out,
                    "input_bytes": s_in, "output_bytes": int(s_out), "input_ssts": len(w.file_off),
                    "output_ssts": int(n_sst), "block_size": 4096, "sst_size_target": MIB4,
                    "l2": "inputs (%.1f GB) larger than L2; no flush" % (s_in / 1e9),
