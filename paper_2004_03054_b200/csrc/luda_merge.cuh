@@ -242,18 +242,14 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     cp_async_wait_all();
     __syncthreads();
   }
-  // strict-order check of both slices (including the seam to the previous tile)
-  for (uint32_t i = tid; i < nt; i += kMergeThreads) {
-    const bool inA = i < na_t;
-    const uint32_t li = inA ? i : i - na_t;
-    const uint64_t gpos = inA ? a0 + li : b0 + li;
-    if (gpos == 0) continue;
-    const Rec<W>& cur = SR(i);
-    Rec<W> prev;
-    if (li > 0) prev = SR(i - 1);
-    else prev = inA ? m.A.at_near(a0 - 1, sa) : m.B.at_near(b0 - 1, sb);
-    if (rec_cmp(prev, cur) >= 0)
-      atomicMin(m.err_order, (unsigned long long)((inA ? m.a_run_base : m.b_run_base) + gpos));
+  // Strict-order check of both slices: inside the tile, the merge loop below
+  // compares every consumed element with the next one of its run (both in
+  // registers); here only the seams to the previous tile.
+  if (tid == 0) {
+    if (na_t > 0 && a0 > 0 && rec_cmp(m.A.at_near(a0 - 1, sa), SR(0)) >= 0)
+      atomicMin(m.err_order, (unsigned long long)(m.a_run_base + a0));
+    if (nb_t > 0 && b0 > 0 && rec_cmp(m.B.at_near(b0 - 1, sb), SR(na_t)) >= 0)
+      atomicMin(m.err_order, (unsigned long long)(m.b_run_base + b0));
   }
   // ---- per-thread merge of kMergeItems outputs (heads kept in registers) ----
   const uint32_t p0 = tid * kMergeItems;
@@ -308,10 +304,16 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
         if (!m.ra.resolve) perm[p] = my_perm[k];
         if (takeA) {
           ++i;
-          if (i < na_t) ha = SR(i);
+          if (i < na_t) {
+            ha = SR(i);
+            if (rec_cmp(cur, ha) >= 0) atomicMin(m.err_order, (unsigned long long)(m.a_run_base + a0 + i));
+          }
         } else {
           ++j;
-          if (j < nb_t) hb = SR(na_t + j);
+          if (j < nb_t) {
+            hb = SR(na_t + j);
+            if (rec_cmp(cur, hb) >= 0) atomicMin(m.err_order, (unsigned long long)(m.b_run_base + b0 + j));
+          }
         }
         if (m.ra.resolve) {
           const bool first = !has_prev || !same_user(prev, cur);
