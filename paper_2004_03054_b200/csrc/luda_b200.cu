@@ -4,7 +4,7 @@
 // globals (CRC tables) need no relocatable device code.
 //
 // luda_compact(job) runs the fused compaction pipeline on one stream:
-//   parse_files_a + crc_ranges   footer/filter/index checks   (sst.py:284-310)
+//   parse_files_a + crc_flat     footer/filter/index checks   (sst.py:284-310)
 //   parse_files_c                data-block table
 //   decode_kernel<W>             CRC verify + parse → records (blocks.py:130-165)
 //   merge passes <W>             merge path + resolve + compaction (SPEC D12/D20)

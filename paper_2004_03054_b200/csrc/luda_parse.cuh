@@ -223,34 +223,8 @@ __device__ __forceinline__ uint32_t warp_crc_pass_global(const uint8_t* g, uint6
   return crc_shift(warp_crc_pass_global_raw<kCg>(g, n, q, stage, cs), (uint64_t)kGroup * q);
 }
 
-// Stage B: CRC of many ranges; warp per range, looping passes. out[i] = crc.
-// Ranges with length < 4 are done by lane 0 bytewise.
+// CTA width of crc_big_kernel.
 constexpr int kCrcWarps = 8;
-__global__ void __launch_bounds__(kCrcWarps * 32) crc_ranges_kernel(const uint8_t* arena, const uint64_t* addr,
-                                                                   const uint32_t* len, uint32_t nranges,
-                                                                   uint32_t* out) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
-  uint8_t* stage = smem_raw + sizeof(CrcSmem) + (threadIdx.x >> 5) * (kGroup + 192);
-  crc_smem_init(cs);
-  __syncthreads();
-  const uint32_t lane = lane_id();
-  const uint32_t nw = gridDim.x * kCrcWarps;
-  for (uint32_t r = blockIdx.x * kCrcWarps + (threadIdx.x >> 5); r < nranges; r += nw) {
-    const uint8_t* g = arena + addr[r];
-    const uint64_t n = len[r];
-    uint32_t acc = 0;
-    if (n < 4) {
-      if (lane == 0) acc = crc32_bytes(g, (uint32_t)n, crc_lane(cs, lane_id()));
-    } else {
-      const uint64_t npass = (n + kGroup - 1) / kGroup;
-      uint32_t raw = 0;
-      for (uint64_t q = 0; q < npass; ++q) raw ^= warp_crc_pass_global(g, n, q, stage, cs);
-      acc = ~raw;
-    }
-    if (lane == 0) out[r] = acc;
-  }
-}
 
 // Many ranges, flattened: work item = (range, pass). pstart[r] = first item of
 // range r (exclusive prefix of max(1, ceil(len/kGroup))), pstart[n] = total.
