@@ -1079,9 +1079,10 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
     GET(f_, uint32_t, nblk, false);
     bt = BlockTable{a_, l_, o_, f_};
   }
-  GET(bound, unsigned long long, 1, true);
-  parse_files_c<<<(nf * 32 + 255) / 256, 256, 0, st>>>(pa, d_fbb, bt, std::max<uint32_t>(jd->restart_interval, 16),
-                                                       bound);
+  uint32_t max_nb = 0;
+  for (uint32_t f = 0; f < nf; ++f) max_nb = std::max(max_nb, hinfo[f].nblocks);
+  parse_files_c<<<dim3(nf, std::max(1u, (max_nb + kParseChunk - 1) / kParseChunk)), kParseThreads, 0, st>>>(
+      pa, d_fbb, bt);
   ++g_launches;
   CK(cudaGetLastError());
   const unsigned long long hbound = 0;  // (entry counts now come from the count pre-pass)
