@@ -590,6 +590,49 @@ __device__ __forceinline__ void value_copy16(uint8_t* base_dst, const uint8_t* b
   }
 }
 
+// value_copy16 for a value shared by G lanes (few, large values per block —
+// BASELINE c4 256-byte values, c2 1 KiB values): this lane writes destination
+// chunks sub, sub+G, sub+2G, ... of [dst_off, dst_off+n), each realigned
+// from two aligned LDS.128; partial words are read-modified-written (a value's
+// edge words never share a word with another value's).
+__device__ __forceinline__ void value_copy16_strided(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
+                                                     uint32_t src_off, uint32_t n, uint32_t sub, uint32_t G) {
+  if (n == 0) return;
+  const uint32_t end = dst_off + n;
+  const uint32_t c_lo = dst_off & ~15u, c_hi = (end + 15) & ~15u;
+  const int32_t s0 = (int32_t)src_off - (int32_t)(dst_off - c_lo);  // source of byte c_lo
+  const uint32_t o = (uint32_t)s0 & 15u;
+  const uint8_t* sbase = base_src + (s0 - (int32_t)o);
+  const uint32_t q = o >> 2, sh = (o & 3u) * 8u;
+  for (uint32_t dchunk = c_lo + 16 * sub; dchunk < c_hi; dchunk += 16 * G) {
+    const uint4* sp = reinterpret_cast<const uint4*>(sbase + (dchunk - c_lo));
+    const uint4 A = sp[0], B = sp[1];
+    const uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+    uint32_t x[6], y[5], v[4];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) x[k] = (q & 2u) ? w[k + 2] : w[k];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) y[k] = (q & 1u) ? x[k + 1] : x[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __funnelshift_r(y[k], y[k + 1], sh);
+    const uint32_t lo = dchunk < dst_off ? dst_off - dchunk : 0u;
+    const uint32_t hi = (dchunk + 16 > end) ? end - dchunk : 16u;
+    if (lo == 0 && hi == 16) {
+      *reinterpret_cast<uint4*>(base_dst + dchunk) = make_uint4(v[0], v[1], v[2], v[3]);
+    } else {
+      uint32_t* dw = reinterpret_cast<uint32_t*>(base_dst + dchunk);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t a = (int32_t)lo - 4 * k, b = (int32_t)hi - 4 * k;  // bytes [a, b) of word k
+        if (b <= 0 || a >= 4) continue;
+        const uint32_t m =
+            (b >= 4 ? 0xFFFFFFFFu : ((1u << (8 * b)) - 1u)) & (a <= 0 ? 0xFFFFFFFFu : ~((1u << (8 * a)) - 1u));
+        dw[k] = m == 0xFFFFFFFFu ? v[k] : ((dw[k] & ~m) | (v[k] & m));
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void warp_copy_ranges16(uint8_t* base_dst, const uint8_t* base_src, uint32_t dst_off,
                                                    uint32_t src_off, uint32_t n, uint32_t* scratch) {
   const uint32_t lane = lane_id();

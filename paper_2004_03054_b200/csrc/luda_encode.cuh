@@ -541,9 +541,18 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   const uint32_t soff = e.soff;
   // each lane realigns its own value (no chunk map; edge words of neighbouring
   // entries are >= 12 bytes apart, so the per-word read-modify-writes never race)
-  if (!(a.dbg & 4) && lane < e.cnt)
-    value_copy16(sbase, stg, (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s), soff, e.vl, 0u, false, 0u,
-                 false);
+  // Blocks of few, large values (cnt <= 16) share each value among G = 32/2^ceil(log2 cnt) lanes.
+  const uint32_t lgc = e.cnt <= 1 ? 0u : 32u - __clz(e.cnt - 1u);
+  const uint32_t G = 32u >> lgc;
+  const uint32_t vdst = (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s);
+  if (G == 1) {
+    if (!(a.dbg & 4) && lane < e.cnt) value_copy16(sbase, stg, vdst, soff, e.vl, 0u, false, 0u, false);
+  } else {
+    const uint32_t v = lane / G;
+    const uint32_t gd = __shfl_sync(0xFFFFFFFFu, vdst, v), gs = __shfl_sync(0xFFFFFFFFu, soff, v);
+    const uint32_t gn = __shfl_sync(0xFFFFFFFFu, e.vl, v);
+    if (!(a.dbg & 4) && v < e.cnt) value_copy16_strided(sbase, stg, gd, gs, gn, lane % G, G);
+  }
   __syncwarp();
   ENC_T(5);
 }
