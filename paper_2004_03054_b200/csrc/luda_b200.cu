@@ -360,13 +360,13 @@ int run_chain(cudaStream_t st, Scratch& scratch, const uint32_t* jmp, uint32_t n
   if (sm > 48 * 1024) CK(cudaFuncSetAttribute(chain_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   chain_map_kernel<<<ntiles, kChainThreads, sm, st>>>(c);
   ++g_launches;
-  chain_group_kernel<<<ngroups, kChainThreads, 0, st>>>(c);
+  chain_group_kernel<<<ngroups, kChainThreads, kChainStage, st>>>(c);
   ++g_launches;
-  chain_top_kernel<<<1, 32, 0, st>>>(c);
+  chain_top_kernel<<<1, 1024, kChainStage, st>>>(c);
   ++g_launches;
   GET(tentry, uint32_t, ntiles, false);
   GET(tbase, uint32_t, ntiles, false);
-  chain_tile_entry_kernel<<<(ngroups + 127) / 128, 128, 0, st>>>(c, tentry, tbase);
+  chain_tile_entry_kernel<<<ngroups, kChainThreads, kChainStage, st>>>(c, tentry, tbase);
   ++g_launches;
   if (sm > 48 * 1024) CK(cudaFuncSetAttribute(chain_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   chain_emit_kernel<<<ntiles, kChainThreads, sm, st>>>(c, tentry, tbase);

@@ -206,50 +206,100 @@ __global__ void __launch_bounds__(kChainThreads) chain_map_kernel(ChainArgs c) {
   }
 }
 
+// The composition walks below follow dependent (tile, offset) lookups; each
+// CTA first stages the rows it walks into shared memory (kChainStage bytes
+// max) so a step is one LDS instead of an L2 round trip.
+constexpr uint32_t kChainStage = 40 * 1024;
+
 __global__ void __launch_bounds__(kChainThreads) chain_group_kernel(ChainArgs c) {
+  extern __shared__ __align__(16) uint32_t sg[];
   const uint32_t g = blockIdx.x;
   const uint32_t tf = g * c.G;
   const uint32_t tl = (tf + c.G < c.ntiles) ? tf + c.G : c.ntiles;
+  const uint64_t rows = (uint64_t)(tl - tf) * c.D;
+  const bool staged = rows * 8 <= kChainStage;
+  const uint32_t* cnt = c.cnt + (uint64_t)tf * c.D;
+  const uint32_t* ex = c.exit_ + (uint64_t)tf * c.D;
+  if (staged) {
+    for (uint32_t i = threadIdx.x; i < rows; i += kChainThreads) {
+      sg[i] = cnt[i];
+      sg[rows + i] = ex[i];
+    }
+    __syncthreads();
+    cnt = sg;
+    ex = sg + rows;
+  }
   for (uint32_t o = threadIdx.x; o < c.D; o += kChainThreads) {
     uint32_t off = o, total = 0;
-    for (uint32_t t = tf; t < tl && off != kChainEnd; ++t) {
+    for (uint32_t t = 0; t < tl - tf && off != kChainEnd; ++t) {
       const uint64_t idx = (uint64_t)t * c.D + off;
-      total += c.cnt[idx];
-      off = c.exit_[idx];
+      total += cnt[idx];
+      off = ex[idx];
     }
     c.gexit[(uint64_t)g * c.D + o] = off;
     c.gcnt[(uint64_t)g * c.D + o] = total;
   }
 }
 
-__global__ void chain_top_kernel(ChainArgs c) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(1024) chain_top_kernel(ChainArgs c) {
+  extern __shared__ __align__(16) uint32_t sg[];
+  const uint64_t rows = (uint64_t)c.ngroups * c.D;
+  const bool staged = rows * 8 <= kChainStage;
+  const uint32_t* gcnt = c.gcnt;
+  const uint32_t* gex = c.gexit;
+  if (staged) {
+    for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) {
+      sg[i] = c.gcnt[i];
+      sg[rows + i] = c.gexit[i];
+    }
+    __syncthreads();
+    gcnt = sg;
+    gex = sg + rows;
+  }
+  if (threadIdx.x != 0) return;
   uint32_t off = 0, total = 0;
   for (uint32_t g = 0; g < c.ngroups; ++g) {
     c.gentry[g] = off;
     c.gbase[g] = total;
     if (off == kChainEnd) continue;
     const uint64_t idx = (uint64_t)g * c.D + off;
-    total += c.gcnt[idx];
-    off = c.gexit[idx];
+    total += gcnt[idx];
+    off = gex[idx];
   }
   *c.nnodes = total;
 }
 
-// Entry offset and first node index of every tile: one thread per group walks
-// its G tiles (the tile maps compose along the true chain).
-__global__ void chain_tile_entry_kernel(ChainArgs c, uint32_t* tentry, uint32_t* tbase) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= c.ngroups) return;
+// Entry offset and first node index of every tile: CTA per group, its G
+// tile rows staged in shared memory, one thread walks them (the tile maps
+// compose along the true chain).
+__global__ void __launch_bounds__(kChainThreads) chain_tile_entry_kernel(ChainArgs c, uint32_t* tentry,
+                                                                          uint32_t* tbase) {
+  extern __shared__ __align__(16) uint32_t sg[];
+  const uint32_t g = blockIdx.x;
+  const uint32_t tf = g * c.G;
+  const uint32_t tl = (tf + c.G < c.ntiles) ? tf + c.G : c.ntiles;
+  const uint64_t rows = (uint64_t)(tl - tf) * c.D;
+  const bool staged = rows * 8 <= kChainStage;
+  const uint32_t* cnt = c.cnt + (uint64_t)tf * c.D;
+  const uint32_t* ex = c.exit_ + (uint64_t)tf * c.D;
+  if (staged) {
+    for (uint32_t i = threadIdx.x; i < rows; i += kChainThreads) {
+      sg[i] = cnt[i];
+      sg[rows + i] = ex[i];
+    }
+    __syncthreads();
+    cnt = sg;
+    ex = sg + rows;
+  }
+  if (threadIdx.x != 0) return;
   uint32_t off = c.gentry[g], base = c.gbase[g];
-  const uint32_t tl = (g * c.G + c.G < c.ntiles) ? g * c.G + c.G : c.ntiles;
-  for (uint32_t u = g * c.G; u < tl; ++u) {
-    tentry[u] = off;
-    tbase[u] = base;
+  for (uint32_t u = 0; u < tl - tf; ++u) {
+    tentry[tf + u] = off;
+    tbase[tf + u] = base;
     if (off == kChainEnd) continue;
     const uint64_t idx = (uint64_t)u * c.D + off;
-    base += c.cnt[idx];
-    off = c.exit_[idx];
+    base += cnt[idx];
+    off = ex[idx];
   }
 }
 
