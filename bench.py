@@ -119,7 +119,8 @@ class Workload:
     pass
 
 
-def synth_c3(n_keys, seed, device_index, del_frac=0.2, vlen=128, klen=16, sst_target=MIB4, shard=0, nshards=1):
+def synth_c3(n_keys, seed, device_index, del_frac=0.2, vlen=128, klen=16, sst_target=MIB4, shard=0, nshards=1,
+             keep_truth=False):
     import torch
 
     from paper_2004_03054_b200 import _native
@@ -200,6 +201,8 @@ def synth_c3(n_keys, seed, device_index, del_frac=0.2, vlen=128, klen=16, sst_ta
     w.stream = s.value
     L.luda_job_release(ctypes.byref(r_lo))
     L.luda_job_release(ctypes.byref(r_up))
+    # generator truth for the tests (user keys, value bytes, value offsets of the Li run, delete flags)
+    w.truth = (keys, values, voff_lo, is_del) if keep_truth else None
     del values, keys, words, hi, lo, tr_up, tr_lo, voff_up, voff_lo, vlen_up, vlen_lo, is_del, idx
     torch.cuda.empty_cache()
     return w

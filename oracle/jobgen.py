@@ -160,3 +160,85 @@ def materialize(job: JobSpec, builder=O.build_tables_split, **cfg):
     lower = [f for r in job.lower for f in files_of(r)]
     upper = [f for r in job.upper for f in files_of(r)]
     return lower, upper
+
+
+def values_job(n=400, seed=0xB16, klen=16, vmin=4096, vmax=12288, del_frac=0.1, sst_target=2**31):
+    """Two overlapping runs (Li newer than Li+1) with value lengths uniform in
+    [vmin, vmax]: values of 4-12 KiB make single-entry blocks larger than the
+    4 KiB block size (sst.py:153-177 lets one entry overflow a block)."""
+    rng = random.Random(seed)
+    keys = _distinct_keys(rng, n, klen)
+    upper = [(k, 1 + i, O.KIND_PUT) for i, k in enumerate(keys)]
+    sub = sorted(rng.sample(keys, n // 2))
+    lower = [(k, n + 1 + i, O.KIND_DELETE if rng.random() < del_frac else O.KIND_PUT) for i, k in enumerate(sub)]
+
+    def run(trip):
+        pairs = []
+        for uk, seq, kind in trip:
+            v = b"" if kind == O.KIND_DELETE else rng.randbytes(rng.randint(vmin, vmax))
+            pairs.append((O.make_ikey(uk, seq, kind), v))
+        return pairs
+    return JobSpec("values", lower=[RunSpec(run(lower), 1, sst_target)],
+                   upper=[RunSpec(run(upper), 2, sst_target)], source_level=1, target_level=2)
+
+
+def spec_a1(seed):
+    """SPEC A1 random job: 1-6 L0 SSTs over a shared key space,
+    value sizes 64 B - 4 KiB, 0-20% tombstones, overwrites across files."""
+    rng = random.Random(0xA1000 + seed)
+    n_files = rng.randint(1, 6)
+    del_frac = rng.uniform(0.0, 0.2)
+    space = _distinct_keys(rng, rng.randint(50, 400), 16)
+    seq = 1
+    runs = []
+    for _ in range(n_files):
+        ks = sorted(rng.sample(space, rng.randint(1, min(200, len(space)))))
+        pairs = []
+        for k in ks:
+            kind = O.KIND_DELETE if rng.random() < del_frac else O.KIND_PUT
+            v = b"" if kind == O.KIND_DELETE else rng.randbytes(rng.randint(64, 4096))
+            pairs.append((O.make_ikey(k, seq, kind), v))
+            seq += 1
+        runs.append(RunSpec(pairs, 0, 2**31))
+    runs.reverse()  # newest file first, like L0 in a Version
+    return JobSpec(f"spec_a1_{seed}", lower=runs, upper=[], source_level=0, target_level=1)
+
+
+def _varkeys(rng, n, max_len):
+    """Distinct user keys of mixed lengths 0..max_len, rich in prefix pairs
+    (k and k + suffix) and in bytes that collide with trailer bytes, so shared
+    prefixes run into the 8-byte trailer (blocks.py:33-58, keys.py:60-63)."""
+    out = set()
+    alphabet = bytes([0, 1, 2, 0x7F, 0x80, 0xFE, 0xFF]) + b"abc"
+    while len(out) < n:
+        r = rng.random()
+        if out and r < 0.35:
+            base = rng.choice(sorted(out))
+            if rng.random() < 0.5 and len(base) < max_len:   # extend: base is a prefix of the new key
+                k = base + bytes(rng.choice(alphabet) for _ in range(rng.randint(1, min(8, max_len - len(base)))))
+            else:                                             # truncate: new key is a prefix of base
+                k = base[:rng.randint(0, len(base))]
+        elif r < 0.6:
+            k = bytes(rng.choice(alphabet) for _ in range(rng.randint(0, max_len)))
+        else:
+            k = rng.randbytes(rng.randint(0, max_len))
+        out.add(k)
+    return sorted(out)
+
+
+def varkey(seed, max_len=64, n_space=500, n_files=None):
+    """Mixed user-key lengths 0..max_len in one job (L0 files over one key space)."""
+    rng = random.Random(0x7A4000 + seed)
+    space = _varkeys(rng, n_space, max_len)
+    n_files = n_files or rng.randint(2, 5)
+    seq = 1
+    runs = []
+    for _ in range(n_files):
+        ks = sorted(rng.sample(space, rng.randint(1, len(space))))
+        trip = []
+        for k in ks:
+            trip.append((k, seq, O.KIND_DELETE if rng.random() < 0.1 else O.KIND_PUT))
+            seq += 1
+        runs.append(RunSpec(_run(trip, rng, 40, vlen_jitter=40), 0, 2**31))
+    runs.reverse()
+    return JobSpec(f"varkey{seed}", lower=runs, upper=[], source_level=0, target_level=1)

@@ -72,6 +72,7 @@ _SIGS = {
     "luda_last_error": (ctypes.c_char_p, []),
     "luda_last_error_offset": (ctypes.c_int64, []),
     "luda_abi_version": (ctypes.c_int, []),
+    "luda_set_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64]),
     "luda_region_alloc": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
     "luda_region_free": (ctypes.c_int, [ctypes.c_void_p]),
     "luda_host_alloc": (ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
@@ -134,6 +135,9 @@ def lib(device_ordinal: int = 0):
             check(L.luda_init(device_ordinal))
             _inited[device_ordinal] = True
     return L
+
+
+OPT_PLANNER_TILE = 1  # include/luda_b200.h enum luda_option
 
 
 def check(status: int):

@@ -159,7 +159,7 @@ class JobRunner:
         for s in (s_lo, s_up):
             e = dev._event_on(s)
             _native.check(self.L.luda_stream_wait_event(s_cmp, e))
-            self._keep.append(e)
+            _native.check(self.L.luda_event_destroy(e))  # released once the wait is satisfied
         return arena, offs, total
 
     def describe(self, pj: PreparedJob, arena, offs, total):
@@ -207,6 +207,7 @@ class JobRunner:
         s_cmp = self.device.stream("compute")
         e = self.device._event_on(s_cmp)
         _native.check(self.L.luda_stream_wait_event(s_out, e))
+        _native.check(self.L.luda_event_destroy(e))
         self.pin_out.ensure(n)
         _native.check(self.L.luda_stage_out_async(self.pin_out.ptr, res.out, n, s_out))
         _native.check(self.L.luda_stream_sync(s_out))
@@ -247,14 +248,37 @@ def runner_for(device) -> JobRunner:
     return r
 
 
+def file_id_allocator(job, new_file_id=None, *, stride: int = 1, offset: int = 0):
+    """Callable handing out output file ids.
+
+    ``new_file_id`` may be a callable, or an object with a ``new_file_id()``
+    method (the reference's ``VersionSet``, version.py:299). Without one, ids
+    count up from above EVERY file id of ``job.version`` and the job's inputs
+    (files flushed meanwhile belong to the caller's VersionSet, which should
+    then be passed). ``stride``/``offset`` interleave the ids of several
+    ranks of one subcompacted job (rank r of G: stride G, offset r)."""
+    if new_file_id is not None:
+        return getattr(new_file_id, "new_file_id", new_file_id)
+    ids = [m.file_id for m in list(job.lower) + list(job.upper)]
+    for level in getattr(getattr(job, "version", None), "levels", None) or []:
+        ids += [m.file_id for m in level]
+    nxt = [max(ids + [0]) + 1 + offset]
+
+    def alloc():
+        v = nxt[0]
+        nxt[0] += stride
+        return v
+    return alloc
+
+
 def run_compaction(job, device, *, inputs=None, directory=None, config: StoreConfig | None = None,
                    new_file_id=None, key_range=None, job_id: int = 0):
     """Compact ``job`` on ``device``; returns ``(outputs, stats)`` where
     outputs is ``[(sst_bytes, SstMeta)]`` in key order.
 
     ``inputs`` maps file_id → bytes (else ``{directory}/{file_id}.sst`` is read).
-    ``new_file_id`` is a callable producing output file ids (default: counting
-    up from the largest input id). ``key_range=(lo, hi)`` restricts the job to
+    ``new_file_id`` is a callable (or a ``VersionSet``) producing output file
+    ids (default: :func:`file_id_allocator`). ``key_range=(lo, hi)`` restricts the job to
     user keys in [lo, hi) (one subcompaction).
     """
     if not isinstance(device, B200Device):
@@ -262,12 +286,7 @@ def run_compaction(job, device, *, inputs=None, directory=None, config: StoreCon
     pj = prepare(job, inputs=inputs, directory=directory, config=config, key_range=key_range)
     n_lower = len(job.lower)
     outs, info, (t0, t1, t2, t3) = runner_for(device).run(pj, n_lower)
-    if new_file_id is None:
-        nxt = [max([m.file_id for m in job.lower + job.upper] + [0])]
-
-        def new_file_id():
-            nxt[0] += 1
-            return nxt[0]
+    new_file_id = file_id_allocator(job, new_file_id)
     results = []
     for data, smallest, largest in outs:
         results.append((data, SstMeta(file_id=new_file_id(), file_size=len(data), smallest=smallest,

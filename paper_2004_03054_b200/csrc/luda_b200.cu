@@ -44,6 +44,7 @@ thread_local std::string g_err;
 thread_local int64_t g_err_off = -1;
 int g_device = -1;
 int g_num_sms = 148;
+uint32_t g_planner_tile = 8192;  // LUDA_OPT_PLANNER_TILE
 
 int fail(int status, const std::string& msg, int64_t off = -1) {
   g_err = msg;
@@ -421,7 +422,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   if (rc) return rc;
   if (hctl[1]) return fail(LUDA_DEVICE, "block planner halo overflow");
   ChainBufs bch{};
-  rc = run_chain(st, scratch, jmp, (uint32_t)n, hctl[0], 8192, bch);
+  rc = run_chain(st, scratch, jmp, (uint32_t)n, hctl[0], g_planner_tile, bch);
   if (rc) return rc;
   const uint32_t nblk = bch.n_nodes;
   res->blocks_out = nblk;
@@ -447,7 +448,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   rc = sync(st);
   if (rc) return rc;
   ChainBufs sch{};
-  rc = run_chain(st, scratch, sjmp, nblk, hctl[2], 8192, sch);
+  rc = run_chain(st, scratch, sjmp, nblk, hctl[2], g_planner_tile, sch);
   if (rc) return rc;
   const uint32_t nsst = sch.n_nodes;
   GET(sst_size, uint64_t, nsst, false);
@@ -473,6 +474,9 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   CK(cudaMemcpyAsync(nent.data(), sst_nent, 8ull * nsst, cudaMemcpyDeviceToHost, st));
   rc = sync(st);
   if (rc) return rc;
+  for (uint32_t s = 0; s < nsst; ++s)  // footer / index offsets are u32 (sst.py:199-208 struct.pack '<IIIIQ')
+    if (priv->len[s] > 0xFFFFFFFFull)
+      return fail(LUDA_FORMAT, "output SST larger than 4 GiB: u32 footer/index offsets cannot address it");
   if (ev) CK(cudaEventRecord(ev[0], st));
   const uint64_t total = priv->off[nsst];
   // big-filter scratch
@@ -499,7 +503,11 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(blk_out, uint64_t, nblk, false);
   block_out_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, sch.nodes, nsst, sst_off, blk_out);
   ++g_launches;
+#ifdef LUDA_ABLATION
   const uint32_t s_edbg = getenv("LUDA_ENC_DBG") ? (uint32_t)atoi(getenv("LUDA_ENC_DBG")) : 0u;
+#else
+  const uint32_t s_edbg = 0;
+#endif
   EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off,
                    blk_out, res->out, s_edbg};
   const size_t esm = sizeof(CrcSmem) + (size_t)kEncPairs * sizeof(EncPairSmem) + sizeof(EncCtaSmem);
@@ -535,11 +543,10 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
 template <int W>
 int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_job_result* res, uint32_t K,
               uint32_t nblk, const BlockTable& bt, const uint32_t* d_file_blk_base,
-              const std::vector<uint32_t>& file_blk_base, uint64_t bound, cudaEvent_t* ev) {
+              cudaEvent_t* ev) {
   const uint32_t L = K - 8;
   res->blocks_in = nblk;
   // ---- decode ----
-  (void)bound;
   GET(errs, unsigned long long, 2, false);
   const size_t dsm = sizeof(CrcSmem) + (size_t)kDecPairs * sizeof(DecPairSmem) + sizeof(DecCtaSmem);
   CK(cudaFuncSetAttribute(decode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
@@ -564,7 +571,11 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
     CK(cudaMemsetAsync(errs, 0xFF, 16, st));
     CK(cudaMemsetAsync(d_max, 0, 8, st));
+#ifdef LUDA_ABLATION
     static const uint32_t s_dbg = getenv("LUDA_DEC_DBG") ? (uint32_t)atoi(getenv("LUDA_DEC_DBG")) : 0u;
+#else
+    const uint32_t s_dbg = 0;
+#endif
     DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, errs, errs + 1, s_dbg};
     KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
@@ -600,13 +611,23 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_local, d_lo, nblk, nw, d_file_blk_base,
                                                                           jd->n_files, d_fbase);
   ++g_launches;
+  const RunView<W> segview{X, d_lo, seg_cap, nw, 0};
+  // file seams of every multi-file run, checked before any merge pass
+  std::vector<uint32_t> run_first(jd->run_first_file, jd->run_first_file + jd->n_runs + 1);
+  std::vector<uint32_t> first_of_run(jd->n_files, 0), seam_bad(jd->n_files, 0);
+  for (uint32_t r = 0; r + 1 < run_first.size(); ++r)
+    for (uint32_t f = run_first[r]; f < run_first[r + 1] && f < jd->n_files; ++f) first_of_run[f] = run_first[r];
+  GET(d_for, uint32_t, jd->n_files, false);
+  GET(d_bad, uint32_t, jd->n_files, false);
+  CK(cudaMemcpyAsync(d_for, first_of_run.data(), 4ull * jd->n_files, cudaMemcpyHostToDevice, st));
+  seam_check_kernel<W><<<(jd->n_files + 255) / 256, 256, 0, st>>>(segview, d_fbase, d_for, jd->n_files, d_bad);
+  ++g_launches;
   CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(seam_bad.data(), d_bad, 4ull * jd->n_files, cudaMemcpyDeviceToHost, st));
   {
     int rc = sync(st);
     if (rc) return rc;
   }
-  const RunView<W> segview{X, d_lo, seg_cap, nw, 0};
-  if (getenv("LUDA_DEC_DBG")) return LUDA_OK;  // decode ablation experiments stop here
   res->n_in = n_in;
   if (ev) CK(cudaEventRecord(ev[2], st));
   // ---- merge + resolve ----
@@ -633,17 +654,22 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   if (jd->range_lo) ra.range_lo = make_bound(jd->range_lo, jd->range_lo_len, L, true, true);
   if (jd->range_hi) ra.range_hi = make_bound(jd->range_hi, jd->range_hi_len, L, false, false);
   ra.resolve = true;
-  std::vector<uint32_t> run_first(jd->run_first_file, jd->run_first_file + jd->n_runs + 1);
+  // runs in merge-priority order; a run with a violated file seam is split into per-file runs
+  std::vector<RunSeg> runs;
+  for (uint32_t r = 0; r + 1 < run_first.size(); ++r) {
+    bool split = false;
+    for (uint32_t f = run_first[r]; f < run_first[r + 1]; ++f) split |= seam_bad[f] != 0;
+    if (split) {
+      for (uint32_t f = run_first[r]; f < run_first[r + 1]; ++f) runs.push_back({fbase[f], fbase[f + 1] - fbase[f]});
+    } else {
+      runs.push_back({fbase[run_first[r]], fbase[run_first[r + 1]] - fbase[run_first[r]]});
+    }
+  }
   GET(Y, Rec<W>, n_in, false);
   GET(S, Rec<W>, n_in, false);
   GET(merr, unsigned long long, 2, false);
   uint64_t n_out = 0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    std::vector<RunSeg> runs;
-    for (uint32_t r = 0; r + 1 < run_first.size(); ++r) {
-      const uint64_t a = fbase[run_first[r]], b = fbase[run_first[r + 1]];
-      runs.push_back({a, b - a});
-    }
+  {
     CK(cudaMemsetAsync(merr, 0xFF, 8, st));
     CK(cudaMemsetAsync(merr + 1, 0, 8, st));
     int rc = merge_runs<W>(st, scratch, X, segview, Y, S, runs, ra, merr, merr + 1);
@@ -652,24 +678,8 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     CK(cudaMemcpyAsync(hm, merr, 16, cudaMemcpyDeviceToHost, st));
     rc = sync(st);
     if (rc) return rc;
-    if (hm[0] == ~0ull) {
-      n_out = hm[1];
-      break;
-    }
-    // violation at decoded position p: a seam between files of one run → split runs per file and retry
-    const uint64_t p = hm[0];
-    bool seam = false;
-    for (uint32_t f = 0; f < jd->n_files; ++f)
-      if (fbase[f] == p && fbase[f + 1] >= p) {
-        // file f starts at p; seam only if f is not the first file of its run
-        bool run_start = false;
-        for (uint32_t r : run_first) run_start |= (r == f);
-        seam = !run_start;
-      }
-    if (!seam || attempt == 1) return fail(LUDA_ORDERING, "input run not strictly ascending");
-    std::vector<uint32_t> per_file;
-    for (uint32_t f = 0; f <= jd->n_files; ++f) per_file.push_back(f);
-    run_first = per_file;
+    if (hm[0] != ~0ull) return fail(LUDA_ORDERING, "input run not strictly ascending");
+    n_out = hm[1];
   }
   if (ev) CK(cudaEventRecord(ev[3], st));
   // survivors have distinct user keys → LCP < L → unshared >= 9 → entry >= 12 B
@@ -732,7 +742,18 @@ int build_w(cudaStream_t st, Scratch& scratch, const uint8_t* keys, uint32_t L, 
 
 extern "C" {
 
-int luda_abi_version(void) { return 1; }
+int luda_abi_version(void) { return 2; }
+
+int luda_set_option(int option, int64_t value) {
+  switch (option) {
+    case LUDA_OPT_PLANNER_TILE:
+      if (value < 32 || value > (1 << 20)) return fail(LUDA_DEVICE, "planner tile must be in [32, 2^20]");
+      g_planner_tile = (uint32_t)value;
+      return LUDA_OK;
+    default:
+      return fail(LUDA_DEVICE, "unknown option");
+  }
+}
 
 const char* luda_last_error(void) { return g_err.c_str(); }
 int64_t luda_last_error_offset(void) { return g_err_off; }
@@ -1085,15 +1106,14 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
       pa, d_fbb, bt);
   ++g_launches;
   CK(cudaGetLastError());
-  const unsigned long long hbound = 0;  // (entry counts now come from the count pre-pass)
   const uint32_t W = std::max<uint32_t>(1, (L + 7) / 8);
   CK(cudaEventRecord(ev[1], st));
   cudaEvent_t* pev = ev;
   switch (W) {
-    case 1: rc = compact_w<1>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
-    case 2: rc = compact_w<2>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
-    case 3: rc = compact_w<3>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
-    default: rc = compact_w<4>(st, scratch, jd, res, K, nblk, bt, d_fbb, fbb, hbound, pev); break;
+    case 1: rc = compact_w<1>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
+    case 2: rc = compact_w<2>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
+    case 3: rc = compact_w<3>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
+    default: rc = compact_w<4>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
   }
   if (rc) {
     luda_job_release(res);

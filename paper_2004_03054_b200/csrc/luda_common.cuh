@@ -26,6 +26,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Ablation experiments (profiles/*_ablation.py) switch pipeline stages off in
+// a separate -DLUDA_ABLATION build; production builds compile them out.
+#ifdef LUDA_ABLATION
+#define LUDA_ABLATE(args, bit) (((args).dbg & (bit)) != 0)
+#else
+#define LUDA_ABLATE(args, bit) false
+#endif
+
 namespace luda {
 
 constexpr uint32_t kCrcPoly = 0xEDB88320u;

@@ -99,7 +99,7 @@ struct DecodeArgs {
   uint64_t* seg_count;      // out [nwarps]: records of each warp segment (may exceed seg_cap → rerun)
   unsigned long long* err_ref;
   unsigned long long* err_unsup;
-  uint32_t dbg;             // experiment switches (0 in production)
+  uint32_t dbg;             // ablation switches (LUDA_ABLATION builds only)
 };
 
 // Block range of warp segment w of nw: [w*nblk/nw, (w+1)*nblk/nw).
@@ -464,7 +464,7 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
     if (lane == 0 && !code && st.unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | st.unsup);
     return;
   }
-  if (a.dbg & 2) return;
+  if (LUDA_ABLATE(a, 2)) return;
   const uint32_t L = K - 8;
   if (st.mode == 1) {
     if (dec_fast_records<W>(a, st, base, d, reinterpret_cast<const uint32_t*>(slots))) return;
@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       const uint8_t* gp = a.arena + mt.addr;
       if (lane == 0) a.blk_local[b] = (uint32_t)cnt;
       uint64_t n = 0;
-      if (!(a.dbg & 4)) {
+      if (!LUDA_ABLATE(a, 4)) {
         if (mt.staged) {
           const uint8_t* d = ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15);
           DecState stt = dec_phase1<W, true>(a, b, mt.addr, mt.len, d, slots);
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       const DecSlotMeta mt = ps.meta[s];
       const bool st_ok = mt.staged != 0;
       const uint32_t len = mt.len;
-      if (len >= 12 && !(a.dbg & 1)) {
+      if (len >= 12 && !LUDA_ABLATE(a, 1)) {
         const uint8_t* gp = a.arena + mt.addr;
         uint32_t crc, stored;
         if (st_ok) {

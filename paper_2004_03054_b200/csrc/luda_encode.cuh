@@ -256,7 +256,7 @@ struct EncodeArgs {
   const uint64_t* sst_off;
   const uint64_t* blk_out;   // output offset of every block
   uint8_t* out;
-  uint32_t dbg;              // experiment switches (0 in production)
+  uint32_t dbg;              // ablation switches (LUDA_ABLATION builds only)
 };
 
 // Output offset of every block: its SST's offset + its data offset in the SST.
@@ -546,12 +546,12 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   const uint32_t G = 32u >> lgc;
   const uint32_t vdst = (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s);
   if (G == 1) {
-    if (!(a.dbg & 4) && lane < e.cnt) value_copy16(sbase, stg, vdst, soff, e.vl, 0u, false, 0u, false);
+    if (!LUDA_ABLATE(a, 4) && lane < e.cnt) value_copy16(sbase, stg, vdst, soff, e.vl, 0u, false, 0u, false);
   } else {
     const uint32_t v = lane / G;
     const uint32_t gd = __shfl_sync(0xFFFFFFFFu, vdst, v), gs = __shfl_sync(0xFFFFFFFFu, soff, v);
     const uint32_t gn = __shfl_sync(0xFFFFFFFFu, e.vl, v);
-    if (!(a.dbg & 4) && v < e.cnt) value_copy16_strided(sbase, stg, gd, gs, gn, lane % G, G);
+    if (!LUDA_ABLATE(a, 4) && v < e.cnt) value_copy16_strided(sbase, stg, gd, gs, gn, lane % G, G);
   }
   __syncwarp();
   ENC_T(5);
@@ -565,7 +565,7 @@ __device__ __forceinline__ void enc_finish(const EncodeArgs<W>& a, const EncLane
   uint8_t* sbase = wbuf + kEncPre;
   uint8_t* dst = sbase + (e.out_off & 15);
   const uint32_t size = e.size;
-  const uint32_t crc = (a.dbg & 1) ? 0u : warp_crc32_smem(dst, size - 4, cs);
+  const uint32_t crc = LUDA_ABLATE(a, 1) ? 0u : warp_crc32_smem(dst, size - 4, cs);
   if (lane == 0) put_u32(dst + size - 4, crc);
   __syncwarp();
   const uintptr_t g = reinterpret_cast<uintptr_t>(a.out + e.out_off);
@@ -577,7 +577,7 @@ __device__ __forceinline__ void enc_finish(const EncodeArgs<W>& a, const EncLane
   // pipe); the caller waits for its smem reads before releasing the buffer
   fence_proxy_async_smem();  // every lane's smem writes (CRC prep/unprep, CRC word) → async proxy
   __syncwarp();
-  if (!(a.dbg & 2) && lane == 0 && c_last > c_first) {
+  if (!LUDA_ABLATE(a, 2) && lane == 0 && c_last > c_first) {
     bulk_s2g(reinterpret_cast<void*>(g0 + 16ull * c_first), sbase + 16 * c_first, 16u * (c_last - c_first));
     bulk_commit();
   }

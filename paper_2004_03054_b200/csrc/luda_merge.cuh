@@ -160,6 +160,23 @@ __global__ void merge_partition_kernel(RunView<W> A, uint64_t na, RunView<W> B, 
   split[2 * (ntiles + 1) + t] = B.lo ? B.seg(B.off + (diag - a)) : 0u;
 }
 
+// Level-run file seams, checked before any merge pass: the last record of
+// file f-1 against the first record of file f, for every file f that is not
+// the first of its run. A violated seam makes that run per-file runs (the
+// reference merges per-file runs); order violations inside
+// a file are OrderingErrors raised by the merge.
+//   first_of_run[f]: index of the first file of f's run
+template <int W>
+__global__ void seam_check_kernel(RunView<W> v, const uint64_t* fbase, const uint32_t* first_of_run, uint32_t nfiles,
+                                  uint32_t* bad) {
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nfiles) return;
+  uint32_t b = 0;
+  const uint64_t g = fbase[f];
+  if (first_of_run[f] != f && g < fbase[f + 1] && g > fbase[first_of_run[f]]) b = rec_cmp(v[g - 1], v[g]) >= 0;
+  bad[f] = b;
+}
+
 template <int W>
 struct MergeArgs {
   RunView<W> A;
@@ -214,8 +231,16 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   if (tile >= m.ntiles) return;
   const uint64_t d0 = tile * kMergeTile;
   const uint64_t d1 = (d0 + kMergeTile < m.na + m.nb) ? d0 + kMergeTile : m.na + m.nb;
-  const uint64_t a0 = m.split[tile], a1 = m.split[tile + 1];
-  const uint64_t b0 = d0 - a0, b1 = d1 - a1;
+  uint64_t a0 = m.split[tile], a1 = m.split[tile + 1];
+  uint64_t b0 = d0 - a0, b1 = d1 - a1;
+  if (a1 < a0 || b1 < b0) {
+    // Split points are monotone only over sorted runs: an unsorted run is an
+    // OrderingError, never an out-of-bounds tile load. The tile is emptied (the
+    // resolve pass still publishes its look-back entry so later tiles proceed).
+    if (tid == 0) atomicMin(m.err_order, (unsigned long long)(m.a_run_base + a0));
+    a1 = a0;
+    b1 = b0;
+  }
   const uint32_t na_t = (uint32_t)(a1 - a0), nb_t = (uint32_t)(b1 - b0);
   const uint32_t nt = na_t + nb_t;
   const uint32_t sa = (uint32_t)m.split[(m.ntiles + 1) + tile], sb = (uint32_t)m.split[2 * (m.ntiles + 1) + tile];

@@ -193,14 +193,19 @@ def plan_ranges(job: CompactionJob, inputs, *, nranges: int = 64, per_file: int 
 
 
 def run_subcompactions(job: CompactionJob, device, *, inputs, config=None, nranges: int = 64, per_file: int = 64,
-                       world: int = 1, rank: int = 0, group=None, compact=None):
+                       world: int = 1, rank: int = 0, group=None, compact=None, new_file_id=None):
     """Plan the ranges (one all-gather) and compact this rank's ranges.
 
     Returns (plan, [(range_index, outputs, stats)]). ``compact`` defaults to
     ``run_compaction``; it receives (sub_job, device, inputs=, config=,
-    key_range=)."""
+    key_range=, new_file_id=). One file-id allocator is shared by all ranges
+    of this rank; without ``new_file_id`` the ranks draw interleaved ids
+    above every file of the job's Version (rank r of G: r, r + G, ...), so
+    no two outputs of the job share an id."""
+    from .compaction import file_id_allocator
     if compact is None:
         from .compaction import run_compaction as compact
+    new_file_id = file_id_allocator(job, new_file_id, stride=max(1, world), offset=rank)
     plan = plan_ranges(job, inputs, nranges=nranges, per_file=per_file, world=world, rank=rank, group=group)
     results = []
     for r in plan.mine:
@@ -209,6 +214,6 @@ def run_subcompactions(job: CompactionJob, device, *, inputs, config=None, nrang
         if not sub.lower and not sub.upper:
             results.append((r, [], None))
             continue
-        outs, stats = compact(sub, device, inputs=inputs, config=config, key_range=(lo, hi))
+        outs, stats = compact(sub, device, inputs=inputs, config=config, key_range=(lo, hi), new_file_id=new_file_id)
         results.append((r, outs, stats))
     return plan, results

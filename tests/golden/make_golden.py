@@ -52,7 +52,7 @@ def sha(b: bytes) -> str:
     return hashlib.sha256(bytes(b)).hexdigest()
 
 
-def ref_build_split(pairs, sst_size_target, block_size=4096, restart_interval=16, bits_per_key=10):
+def ref_build_split(pairs, sst_size_target=4 * 2**20, block_size=4096, restart_interval=16, bits_per_key=10):
     outs = []
 
     def new():
@@ -102,7 +102,7 @@ def ref_compact(files, deeper, out_cfg):
     return ref_build_split(survivors(), **out_cfg)
 
 
-from tests.golden.cases import CASES  # noqa: E402
+from tests.golden.cases import ALL_CASES as CASES  # noqa: E402
 
 
 def make_compaction_goldens():

@@ -29,4 +29,4 @@ def test_binding_declares_every_header_symbol():
 
 def test_load_without_gpu():
     L = _native.load()
-    assert L.luda_abi_version() == 1
+    assert L.luda_abi_version() == 2

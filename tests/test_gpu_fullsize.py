@@ -17,6 +17,8 @@ import os
 import numpy as np
 import pytest
 
+from oracle import luda_oracle as O
+
 pytestmark = pytest.mark.gpu
 
 
@@ -32,6 +34,44 @@ def _host(L, ptr, n, stream):
     return out
 
 
+TARGET = 4 * 2**20
+
+
+def _index_last(sst: bytes):
+    """(data bytes, last block length) of one SST from its footer + index (sst.py:67-76)."""
+    foff, flen, ioff, ilen, _ = O.FOOTER.unpack_from(sst, len(sst) - O.FOOTER_SIZE)
+    idx = O.parse_index(sst[ioff:ioff + ilen])
+    return foff, idx[-1][2]
+
+
+def check_sst_cuts(out: np.ndarray, offs, lens, target=TARGET):
+    """The SST cut rule (sst.py:161-162) over EVERY output:
+    a non-last SST closes right after the first block whose flush makes its
+    data bytes >= target."""
+    for i, (o, ln) in enumerate(zip(offs, lens)):
+        data, last = _index_last(out[o:o + ln].tobytes())
+        if i + 1 < len(offs):
+            assert data >= target and data - last < target, (i, data, last)
+        else:
+            assert data - last < target or data < target, (i, data, last)
+
+
+def check_rebuild(out: np.ndarray, offs, lens, picks, target=TARGET):
+    """Each sampled SST, decoded and rebuilt by the oracle's SstBuilder at the
+    same target, comes back as exactly one byte-identical SST: its block cuts,
+    restarts, shared prefixes, CRCs, filter, index and footer are the
+    reference's. Returns the decoded entries per pick."""
+    got = {}
+    for i in picks:
+        sst = out[offs[i]:offs[i] + lens[i]].tobytes()
+        _, index = O.open_table(sst)
+        pairs = list(O.scan_table(sst, index))
+        rebuilt = O.build_tables_split(pairs, sst_size_target=target)
+        assert len(rebuilt) == 1 and rebuilt[0][0] == sst, i
+        got[i] = pairs
+    return got
+
+
 def test_c3_full_size_accounting_and_recompaction_identity():
     import bench
     from paper_2004_03054_b200 import _native
@@ -39,7 +79,7 @@ def test_c3_full_size_accounting_and_recompaction_identity():
     torch.cuda.set_device(0)
     L = _native.lib(0)
     keys = int(os.environ.get("LUDA_FULL_KEYS", 1 << 25))
-    w = bench.synth_c3(keys, seed=0xC3, device_index=0)
+    w = bench.synth_c3(keys, seed=0xC3, device_index=0, keep_truth=True)
     desc, keep = bench.job_desc(w, w.arena.data_ptr())
     res = _native.JobResult()
     _native.check(L.luda_compact(ctypes.byref(desc), ctypes.byref(res), w.stream))
@@ -74,10 +114,41 @@ def test_c3_full_size_accounting_and_recompaction_identity():
             a = _host(L, res.out, res.out_bytes, w.stream)
             b = _host(L, res2.out, res2.out_bytes, w.stream)
             assert a.size == b.size and np.array_equal(a, b)
+            check_sst_cuts(a, offs, lens)
+            picks = sorted({0, 1, n // 3, n // 2, n - 2, n - 1})
+            decoded = check_rebuild(a, offs, lens, picks)
+            check_against_generator(w, keys, decoded)
         finally:
             L.luda_job_release(ctypes.byref(res2))
     finally:
         L.luda_job_release(ctypes.byref(res))
+
+
+def check_against_generator(w, n, decoded):
+    """Survivors of the sampled SSTs vs the generator (bench.synth_c3): every
+    entry is the Li (newest) version of its key — seq n + 1 + index, a Put
+    whose value is the generator's bytes — and its key was not deleted; the
+    SSTs' entries are consecutive surviving keys."""
+    import torch
+    keys_d, values_d, voff_lo, is_del = w.truth
+    kh = keys_d.view(-1, 16)[:, :8].cpu().numpy().copy().view(">u8").reshape(-1).astype(np.uint64)
+    alive = (~is_del).cpu().numpy()
+    for i, pairs in decoded.items():
+        uk = np.frombuffer(b"".join(k[:8] for k, _ in pairs), dtype=">u8").astype(np.uint64)
+        idx = np.searchsorted(kh, uk)
+        assert (idx < n).all() and (kh[idx] == uk).all(), i
+        full = keys_d.view(-1, 16)[torch.from_numpy(idx).to(keys_d.device)].cpu().numpy()
+        assert [bytes(r) for r in full] == [k[:16] for k, _ in pairs], i
+        tr = [int.from_bytes(k[16:], "little") for k, _ in pairs]
+        assert [t >> 8 for t in tr] == (idx + n + 1).tolist(), i
+        assert all(t & 0xFF == O.KIND_PUT for t in tr) and alive[idx].all(), i
+        # consecutive survivors: no live key between two neighbours of one SST
+        live_rank = np.cumsum(alive) - 1
+        assert (np.diff(live_rank[idx]) == 1).all(), i
+        offs = voff_lo[torch.from_numpy(idx).to(voff_lo.device)]
+        cols = torch.arange(128, device=offs.device)
+        vals = values_d[(offs[:, None] + cols[None, :]).reshape(-1)].view(-1, 128).cpu().numpy()
+        assert [bytes(r) for r in vals] == [v for _, v in pairs], i
 
 
 def _synth_c4_runs(L, runs, n, seed, stream):
@@ -173,6 +244,8 @@ def test_c4_scaled_eight_runs_accounting_and_recompaction_identity():
             a = _host(L, res.out, res.out_bytes, s.value)
             b = _host(L, res2.out, res2.out_bytes, s.value)
             assert np.array_equal(a, b)
+            check_sst_cuts(a, o1, l1)
+            check_rebuild(a, o1, l1, sorted({0, m // 2, m - 1}))
         finally:
             L.luda_job_release(ctypes.byref(res2))
     finally:

@@ -13,7 +13,7 @@ import pytest
 
 from oracle import jobgen
 from oracle import luda_oracle as O
-from tests.golden.cases import CASES
+from tests.golden.cases import ALL_CASES, CASES, EDGE_CASES, FULL_CASES, SPEC_A1_CASES, VARKEY_CASES
 
 pytestmark = pytest.mark.gpu
 
@@ -100,7 +100,7 @@ def test_crc32_batch_many_ranges(native):
 
 
 def build(name):
-    mk, out_cfg = {n: (m, c) for n, m, c in CASES}[name]
+    mk, out_cfg = {n: (m, c) for n, m, c in ALL_CASES}[name]
     job = mk()
     blk = {k: out_cfg[k] for k in ("block_size", "restart_interval") if k in out_cfg}
     lower, upper = jobgen.materialize(job, **blk)
@@ -115,8 +115,7 @@ def gpu_compact(dev, job, lower, upper, out_cfg, **kw):
     return compact_files(dev, lower, upper, source_level=job.source_level, deeper=job.deeper, config=cfg, **kw)
 
 
-@pytest.mark.parametrize("name", [n for n, _, _ in CASES])
-def test_compaction_matches_oracle_and_golden(dev, name):
+def check_case(dev, name):
     job, lower, upper, out_cfg = build(name)
     want = O.reference_compact(lower + upper, deeper=job.deeper, **out_cfg)
     got = gpu_compact(dev, job, lower, upper, out_cfg)
@@ -125,6 +124,29 @@ def test_compaction_matches_oracle_and_golden(dev, name):
         assert gs == ws and gl == wl
         assert gb == wb
     assert [sha(b) for b, _, _ in got] == [o["sha256"] for o in GOLD[name]["outputs"]]
+
+
+FIXED_KEY_CASES = CASES + FULL_CASES + EDGE_CASES + SPEC_A1_CASES
+
+
+@pytest.mark.parametrize("name", [n for n, _, _ in FIXED_KEY_CASES])
+def test_compaction_matches_oracle_and_golden(dev, name):
+    check_case(dev, name)
+
+
+@pytest.fixture
+def small_planner_tiles(native):
+    """Greedy-chain planner tiles of 32 items (LUDA_OPT_PLANNER_TILE): every
+    job's block cut and SST cut then compose over many tiles and groups."""
+    from paper_2004_03054_b200 import _native
+    _native.check(native.luda_set_option(_native.OPT_PLANNER_TILE, 32))
+    yield
+    _native.check(native.luda_set_option(_native.OPT_PLANNER_TILE, 8192))
+
+
+@pytest.mark.parametrize("name", [n for n, _, _ in CASES + FULL_CASES + EDGE_CASES[2:] + SPEC_A1_CASES[:40]])
+def test_compaction_multitile_planner(dev, small_planner_tiles, name):
+    check_case(dev, name)
 
 
 def test_flush_builder_matches_oracle(native):
@@ -199,3 +221,136 @@ def test_subcompactions_match_per_range_oracle(dev):
         want = O.reference_compact([inputs[m.file_id] for m in sub.lower + sub.upper],
                                    sst_size_target=64 * 1024, key_range=(lo, hi))
         assert [o[0] for o in outs] == [w[0] for w in want], r
+
+
+def _unchecked_table(pairs, **cfg):
+    """An SST whose entries are NOT in order: the oracle builder with its
+    ascending check bypassed (the reference's SstBuilder would refuse)."""
+    b = O.TableBuilder(**cfg)
+    for k, v in pairs:
+        b.last_order = None
+        b.add(k, v)
+    return b.finish()
+
+
+def test_level_run_with_overlapping_files_merges_per_file(dev):
+    """A level >= 1 run whose files overlap (every file seam out of order),
+    each file spanning many merge tiles: the seams are found before merging
+    and the run is merged per file, like the reference's per-file heap merge."""
+    rng = random.Random(0x5EA)
+    files = []
+    seq = 1
+    for f in range(3):
+        keys = sorted({rng.randbytes(16) for _ in range(6000)})
+        pairs = []
+        for k in keys:
+            pairs.append((O.make_ikey(k, seq, O.KIND_PUT), rng.randbytes(rng.randint(0, 64))))
+            seq += 1
+        files.append(O.build_table(pairs, sst_size_target=2**31))
+    files.reverse()  # newest first
+    want = O.reference_compact(files, sst_size_target=256 * 1024)
+    from paper_2004_03054_b200.compaction import compact_files
+    from paper_2004_03054_b200.config import StoreConfig
+    got = compact_files(dev, files, [], source_level=1, config=StoreConfig(sst_size_target=256 * 1024))
+    assert [g[0] for g in got] == [w[0] for w in want]
+
+
+@pytest.mark.parametrize("where", ["start", "middle", "end"])
+def test_unsorted_file_raises_ordering_error(dev, where):
+    """Order violations inside a file (many merge tiles) are OrderingErrors,
+    never out-of-bounds tile loads (merge-path splits are monotone only over
+    sorted runs)."""
+    from paper_2004_03054_b200 import OrderingError
+    from paper_2004_03054_b200.compaction import compact_files
+    rng = random.Random({"start": 1, "middle": 2, "end": 3}[where])
+    keys = sorted({rng.randbytes(16) for _ in range(20000)})
+    pairs = [(O.make_ikey(k, i + 1, O.KIND_PUT), rng.randbytes(20)) for i, k in enumerate(keys)]
+    i = {"start": 10, "middle": 9000, "end": len(pairs) - 30}[where]
+    pairs[i:i + 20] = pairs[i:i + 20][::-1]
+    bad = _unchecked_table(pairs, sst_size_target=2**31)
+    other = O.build_table(sorted(((O.make_ikey(rng.randbytes(16), 10**6 + j, O.KIND_PUT), b"x")
+                                  for j in range(5000)), key=lambda kv: O.order_key(kv[0])), sst_size_target=2**31)
+    with pytest.raises(O.OrderingError):
+        O.reference_compact([bad, other])
+    with pytest.raises(OrderingError):
+        compact_files(dev, [bad], [other], source_level=1)
+    with pytest.raises(OrderingError):
+        compact_files(dev, [other, bad], [], source_level=0)
+    # the device stays usable afterwards
+    job, lower, upper, out_cfg = build("c3_small")
+    got = gpu_compact(dev, job, lower, upper, out_cfg)
+    assert [sha(b) for b, _, _ in got] == [o["sha256"] for o in GOLD["c3_small"]["outputs"]]
+
+
+def _reseal_block(f: bytes, block_index: int, mutate) -> bytes:
+    """Mutate one data block's payload and recompute its CRC (blocks.py:99-103),
+    so the block passes verification and reaches the entry parser."""
+    import struct
+    _, index = O.open_table(f)
+    _, off, ln = index[block_index]
+    body = bytearray(f[off:off + ln - 4])
+    mutate(body)
+    out = bytearray(f)
+    out[off:off + ln - 4] = body
+    struct.pack_into("<I", out, off + ln - 4, zlib.crc32(bytes(body)))
+    return bytes(out)
+
+
+@pytest.mark.parametrize("kind", ["filter", "index"])
+def test_filter_and_index_crc_corruption(dev, kind):
+    """Table.__init__ checks (sst.py:293-306): a flipped bit in the filter or
+    the index block is a CorruptionError at that block's offset."""
+    from paper_2004_03054_b200 import CorruptionError
+    job, lower, upper = _corrupt_case()
+    f = bytearray(upper[2])
+    foff, flen, ioff, ilen, _ = O.FOOTER.unpack_from(f, len(f) - O.FOOTER_SIZE)
+    pos = foff + 5 if kind == "filter" else ioff + 3
+    f[pos] ^= 0x10
+    upper = list(upper)
+    upper[2] = bytes(f)
+    with pytest.raises(O.CorruptionError) as want:
+        O.reference_compact(lower + upper)
+    with pytest.raises(CorruptionError) as got:
+        gpu_compact(dev, job, lower, upper, {})
+    assert got.value.offset == want.value.offset == (foff if kind == "filter" else ioff)
+
+
+def _damage_block(body, damage):
+    import struct
+    n = len(body)
+    n_restarts = struct.unpack_from("<I", body, n - 4)[0]
+    entries_end = n - 4 - 4 * n_restarts
+    shared, p = O.varint_read(body, 0)
+    unshared, p = O.varint_read(body, p)
+    vstart = p
+    vlen, p = O.varint_read(body, p)
+    first_end = p + unshared + vlen
+    if damage == "varint_long":        # an 11-byte varint: shift > 63 (varint.py:42-43)
+        body[0:11] = b"\x80" * 10 + b"\x01"
+    elif damage == "entry_trunc":      # value runs past the entries region
+        body[vstart:vstart + 2] = O.varint_bytes(16000)
+    elif damage == "shared_too_long":  # second entry shares more than the previous key's length
+        body[first_end] = 60
+    elif damage == "restarts_zero":    # n_restarts must be >= 1
+        struct.pack_into("<I", body, n - 4, 0)
+    else:                              # restart array larger than the block
+        struct.pack_into("<I", body, n - 4, n)
+
+
+@pytest.mark.parametrize("damage", ["varint_long", "entry_trunc", "shared_too_long", "restarts_zero", "restarts_huge"])
+def test_block_entry_format_errors(dev, damage):
+    """Structural errors inside a CRC-valid data block (blocks.py:137-164,
+    varint.py:28-43) are FormatErrors with the reference's message. (The
+    'truncated varint' and 'trailing garbage' branches of decode_data_block
+    cannot fire on a block whose restart count is valid: the count's high
+    byte would have to be >= 0x80.)"""
+    import paper_2004_03054_b200 as P
+    job, lower, upper = _corrupt_case()
+    upper = list(upper)
+    upper[1] = _reseal_block(upper[1], 2, lambda body: _damage_block(body, damage))
+    with pytest.raises((O.FormatError, O.CorruptionError)) as want:
+        O.reference_compact(lower + upper)
+    with pytest.raises((P.FormatError, P.CorruptionError)) as got:
+        gpu_compact(dev, job, lower, upper, {})
+    assert type(got.value).__name__ == type(want.value).__name__, (got.value, want.value)
+    assert str(want.value) in str(got.value)

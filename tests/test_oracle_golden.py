@@ -11,7 +11,7 @@ import pytest
 
 from oracle import jobgen
 from oracle import luda_oracle as O
-from tests.golden.cases import CASES
+from tests.golden.cases import ALL_CASES as CASES
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = json.load(open(os.path.join(HERE, "golden", "compaction.json")))

@@ -31,7 +31,7 @@ def job_with_inputs(n=4000, seed=0xE5, sst_target=48 * 1024):
     return job, inputs
 
 
-def oracle_compact(sub, device, *, inputs, config=None, key_range=None):
+def oracle_compact(sub, device, *, inputs, config=None, key_range=None, new_file_id=None):
     files = [inputs[m.file_id] for m in sub.lower + sub.upper]
     return O.reference_compact(files, sst_size_target=64 * 1024, key_range=key_range), None
 
