@@ -153,6 +153,17 @@ int luda_build_from_sorted(const uint8_t* dev_user_keys, uint32_t user_key_len,
                            uint32_t bits_per_key, uint64_t sst_size_target,
                            luda_job_result* result, void* stream);
 
+/* As luda_build_from_sorted, but cut an output SST every `entries_per_file`
+ * entries (the last SST may hold fewer; sst_size_target is then unused):
+ * synthesises input levels whose file boundaries are known in advance
+ * (bench_c5.py: BASELINE config 5's global job). 0 = size cut. */
+int luda_build_files_from_sorted(const uint8_t* dev_user_keys, uint32_t user_key_len,
+                                 const uint64_t* dev_trailers, const uint8_t* dev_values,
+                                 const uint64_t* dev_value_off, const uint32_t* dev_value_len,
+                                 uint64_t n, uint32_t block_size, uint32_t restart_interval,
+                                 uint32_t bits_per_key, uint64_t sst_size_target,
+                                 uint64_t entries_per_file, luda_job_result* result, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -383,7 +383,8 @@ int run_chain(cudaStream_t st, Scratch& scratch, const uint32_t* jmp, uint32_t n
 struct EmitParams {
   uint32_t K, block_size, ri, bpk;
   uint64_t sst_target;
-  uint32_t min_entry;  // lower bound of one encoded entry (sizes the planner halo)
+  uint32_t min_entry;         // lower bound of one encoded entry (sizes the planner halo)
+  uint64_t file_entries = 0;  // > 0: cut an SST every file_entries entries instead of by size
 };
 
 // Plan + encode the survivors `S[0..n)` whose values live in `varena`.
@@ -408,7 +409,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(jmp, uint32_t, n, false);
   GET(bsz, uint32_t, n, false);
   GET(ctl, unsigned int, 4, true);  // jmax, overflow, jmax_sst
-  BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1};
+  BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1, p.file_entries};
   const size_t jsm = (2ull * (kJumpTile + halo) + 1) * 4;
   CK(cudaFuncSetAttribute(block_jump_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
   KT_START(2, st);
@@ -441,7 +442,10 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   }
   // ---- SST cut ----
   GET(sjmp, uint32_t, nblk, false);
-  sst_jump_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, p.sst_target, sjmp, ctl + 2);
+  if (p.file_entries)
+    sst_jump_files_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_first, nblk, p.file_entries, sjmp, ctl + 2);
+  else
+    sst_jump_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, p.sst_target, sjmp, ctl + 2);
   ++g_launches;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(hctl, ctl, 16, cudaMemcpyDeviceToHost, st));
@@ -936,6 +940,14 @@ int luda_build_from_sorted(const uint8_t* keys, uint32_t L, const uint64_t* trai
                            const uint64_t* voff, const uint32_t* vlen, uint64_t n, uint32_t block_size,
                            uint32_t restart_interval, uint32_t bits_per_key, uint64_t sst_size_target,
                            luda_job_result* res, void* stream) {
+  return luda_build_files_from_sorted(keys, L, trailers, values, voff, vlen, n, block_size, restart_interval,
+                                      bits_per_key, sst_size_target, 0, res, stream);
+}
+
+int luda_build_files_from_sorted(const uint8_t* keys, uint32_t L, const uint64_t* trailers, const uint8_t* values,
+                                 const uint64_t* voff, const uint32_t* vlen, uint64_t n, uint32_t block_size,
+                                 uint32_t restart_interval, uint32_t bits_per_key, uint64_t sst_size_target,
+                                 uint64_t entries_per_file, luda_job_result* res, void* stream) {
   if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
   std::lock_guard<std::mutex> lock(g_job_mu);
   memset(res, 0, sizeof(*res));
@@ -944,7 +956,7 @@ int luda_build_from_sorted(const uint8_t* keys, uint32_t L, const uint64_t* trai
   cudaStream_t st = (cudaStream_t)stream;
   Scratch scratch(st);
   // duplicates of a user key may share up to K-1 bytes → entry >= 4 B
-  EmitParams ep{L + 8, block_size, restart_interval, bits_per_key, sst_size_target, 4};
+  EmitParams ep{L + 8, block_size, restart_interval, bits_per_key, sst_size_target, 4, entries_per_file};
   const uint32_t W = std::max<uint32_t>(1, (L + 7) / 8);
   int rc;
   switch (W) {

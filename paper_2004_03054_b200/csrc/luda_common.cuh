@@ -343,15 +343,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp is parked (no issue slots
+// spent spinning) until the phase completes or the hint elapses.
+constexpr uint32_t kMbarSuspendNs = 20000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       " .reg .pred P1;\n"
       "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       " @!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(kMbarSuspendNs)
       : "memory");
 }
 // smem → global bulk copy (TMA store; 16-byte aligned addresses and size),

@@ -691,6 +691,14 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
 
 // ---- per-SST filter + index + footer -----------------------------------------------------
 constexpr int kMetaThreads = 512;
+constexpr int kMetaUnroll = 4;  // records in flight per thread in the bloom loop
+
+// a mod d for 32-bit a, d >= 1 with rcp = floor((2^64 - 1) / d) + 1
+// (Lemire, Kaser, Kurz: "Faster remainder by direct computation").
+__device__ __forceinline__ uint32_t fastmod_u32(uint32_t a, uint64_t rcp, uint32_t d) {
+  const uint64_t low = rcp * a;
+  return (uint32_t)__umul64hi(low, d);
+}
 constexpr int kMetaBuf = kMetaBufBytes;
 constexpr int kMetaSmem = (int)sizeof(CrcSmem) + kEncPre + kMetaBuf + 64;
 
@@ -763,16 +771,36 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
     __syncthreads();
     // ---- bloom bits: positions (h + j*delta) mod n_bits, 64-bit (bloom.py:81-87) ----
     if (nbits < (1ull << 31)) {
+      // 32-bit positions; h mod n and delta mod n by Lemire's fastmod (one
+      // 64-bit reciprocal per SST). Records are loaded kMetaUnroll at a time
+      // so the loop is not one DRAM latency per key.
       const uint32_t nb32 = (uint32_t)nbits;
-      for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
-        const uint32_t h = user_key_crc<W>(a.rec[e], L, tl);
-        const uint32_t delta = (h >> 17) | (h << 15);
-        uint32_t p = h % nb32;
-        const uint32_t step = delta % nb32;
-        for (uint32_t j = 0; j < a.kprobes; ++j) {
-          atomicOr(bits + (p >> 5), 1u << (p & 31));
-          p += step;
-          if (p >= nb32) p -= nb32;
+      const uint64_t rcp = ~0ull / nb32 + 1;
+      const uint64_t e_end = fe + ne;
+      for (uint64_t e0 = fe + tid; e0 < e_end; e0 += kMetaUnroll * kMetaThreads) {
+        Rec<W> r[kMetaUnroll];
+#pragma unroll
+        for (int u = 0; u < kMetaUnroll; ++u) {
+          const uint64_t e = e0 + (uint64_t)u * kMetaThreads;
+          r[u] = a.rec[e < e_end ? e : fe];
+        }
+        // the kMetaUnroll key hashes are independent table chains: computed
+        // together (ILP) before any probe
+        uint32_t h[kMetaUnroll];
+#pragma unroll
+        for (int u = 0; u < kMetaUnroll; ++u) h[u] = user_key_crc<W>(r[u], L, tl);
+#pragma unroll
+        for (int u = 0; u < kMetaUnroll; ++u) {
+          if (e0 + (uint64_t)u * kMetaThreads < e_end) {
+            const uint32_t delta = (h[u] >> 17) | (h[u] << 15);
+            uint32_t p = fastmod_u32(h[u], rcp, nb32);
+            const uint32_t step = fastmod_u32(delta, rcp, nb32);
+            for (uint32_t j = 0; j < a.kprobes; ++j) {
+              atomicOr(bits + (p >> 5), 1u << (p & 31));
+              p += step;
+              if (p >= nb32) p -= nb32;
+            }
+          }
         }
       }
     } else {

@@ -44,6 +44,7 @@ struct BlockJumpArgs {
   uint32_t* bsz;      // out [n]: block size incl. crc if a block starts here
   unsigned int* jmax;
   unsigned int* overflow;
+  uint64_t file_entries;  // > 0: a block never crosses a multiple of this (file-cut builds)
 };
 
 // Block size if a block started at local index i held n entries:
@@ -102,7 +103,11 @@ __global__ void __launch_bounds__(kJumpThreads) block_jump_kernel(BlockJumpArgs<
   for (uint32_t i = threadIdx.x; i < (uint32_t)kJumpTile; i += kJumpThreads) {
     const uint64_t j = t0 + i;
     if (j >= a.n) break;
-    const uint64_t rem64 = a.n - j;
+    uint64_t rem64 = a.n - j;
+    if (a.file_entries) {
+      const uint64_t to_file_end = a.file_entries - j % a.file_entries;
+      rem64 = rem64 < to_file_end ? rem64 : to_file_end;
+    }
     const uint32_t lim = (uint32_t)(rem64 < (uint64_t)(span - i) ? rem64 : (uint64_t)(span - i));  // entries available
     uint32_t fixed = 0;  // sum of D over restart entries of groups < k, plus group k's once added
     uint32_t best = 1, m = 0;
@@ -153,6 +158,28 @@ __global__ void sst_jump_kernel(const uint64_t* pos, uint32_t nb, uint64_t targe
     while (lo < hi) {
       const uint32_t mid = lo + ((hi - lo) >> 1);
       if (pos[mid] >= want) hi = mid;
+      else lo = mid + 1;
+    }
+    j = lo - b;
+    jmp[b] = j;
+  }
+  j = warp_max(j);
+  if (lane_id() == 0) atomicMax(jmax, j);
+}
+
+// File-cut builds: every output SST holds exactly `fe` entries (the last
+// fewer); its blocks end at the file boundary (block_jump clamps), so the SST
+// jump from block b is to the first block starting at the next multiple of fe.
+__global__ void sst_jump_files_kernel(const uint32_t* blk_first, uint32_t nb, uint64_t fe, uint32_t* jmp,
+                                      unsigned int* jmax) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t j = 0;
+  if (b < nb) {
+    const uint64_t want = ((uint64_t)blk_first[b] / fe + 1) * fe;
+    uint32_t lo = b + 1, hi = nb;  // first e in (b, nb] with blk_first[e] >= want (e = nb: end)
+    while (lo < hi) {
+      const uint32_t mid = lo + ((hi - lo) >> 1);
+      if ((uint64_t)blk_first[mid] >= want) hi = mid;
       else lo = mid + 1;
     }
     j = lo - b;

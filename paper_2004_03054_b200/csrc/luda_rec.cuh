@@ -15,8 +15,10 @@
 
 namespace luda {
 
+// 16-byte aligned when the record size allows (W = 2, 4: 32 / 48 bytes), so
+// record copies are LDG/STG.128.
 template <int W>
-struct alignas(8) Rec {
+struct alignas((8 * (W + 2)) % 16 == 0 ? 16 : 8) Rec {
   uint64_t k[W];
   uint64_t t;
   uint64_t h;

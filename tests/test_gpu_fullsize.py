@@ -151,56 +151,6 @@ def check_against_generator(w, n, decoded):
         assert [bytes(r) for r in vals] == [v for _, v in pairs], i
 
 
-def _synth_c4_runs(L, runs, n, seed, stream):
-    """BASELINE c4 (scaled): `runs` L0 files, each a sorted run of n uniform
-    24-byte keys with 256-byte values, file i newer than file i+1, each built
-    as ONE SST (sst_size_target 2^31, under the u32 4 GiB cap) by the device
-    builder. Returns (arena tensor, file offsets, file lengths)."""
-    import torch
-    from paper_2004_03054_b200 import _native
-    dev = torch.device("cuda", 0)
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-    vlen, klen = 256, 24
-    values = torch.empty(n * vlen + 4096, dtype=torch.uint8, device=dev).random_(0, 256, generator=g)
-    idx = torch.arange(n, device=dev, dtype=torch.int64)
-    voff = idx * vlen
-    vl = torch.full((n,), vlen, dtype=torch.int32, device=dev)
-    outs = []
-    for r in range(runs):
-        while True:
-            hi = torch.randint(-2**63, 2**63 - 1, (n,), generator=g, device=dev, dtype=torch.int64)
-            hi, _ = torch.sort(hi)
-            if bool((hi[1:] != hi[:-1]).all()):
-                break
-        hi = hi ^ torch.tensor(-2**63, dtype=torch.int64, device=dev)  # signed order -> unsigned byte order
-        mid = torch.randint(-2**63, 2**63 - 1, (n,), generator=g, device=dev, dtype=torch.int64)
-        lo = torch.randint(-2**63, 2**63 - 1, (n,), generator=g, device=dev, dtype=torch.int64)
-        words = torch.stack([hi, mid, lo], 1).contiguous()
-        keys = words.view(torch.uint8).view(n, 3, 8).flip(2).reshape(n * klen).contiguous()
-        seq0 = (runs - 1 - r) * n  # file 0 is the newest
-        tr = ((idx + seq0 + 1) << 8) | 1
-        torch.cuda.synchronize(dev)
-        res = _native.JobResult()
-        _native.check(L.luda_build_from_sorted(keys.data_ptr(), klen, tr.data_ptr(), values.data_ptr(),
-                                               voff.data_ptr(), vl.data_ptr(), n, 4096, 16, 10, 1 << 31,
-                                               ctypes.byref(res), stream))
-        assert res.n_sst == 1
-        outs.append(res)
-    total = sum(r.out_bytes for r in outs)
-    arena = torch.zeros(total + 4096, dtype=torch.uint8, device=dev)
-    offs, lens, at = [], [], 0
-    for r in outs:
-        _native.check(L.luda_memcpy_d2d_async(arena.data_ptr() + at, r.out, r.out_bytes, stream))
-        offs.append(at)
-        lens.append(r.out_bytes)
-        at += r.out_bytes
-    _native.check(L.luda_stream_sync(stream))
-    for r in outs:
-        L.luda_job_release(ctypes.byref(r))
-    return arena, offs, lens
-
-
 def _desc(_native, arena_ptr, arena_bytes, offs, lens, run_first):
     fo = (ctypes.c_uint64 * len(offs))(*offs)
     fl = (ctypes.c_uint64 * len(lens))(*lens)
@@ -226,7 +176,8 @@ def test_c4_scaled_eight_runs_accounting_and_recompaction_identity():
     n = int(os.environ.get("LUDA_C4_KEYS", 1 << 22))
     s = ctypes.c_void_p()
     _native.check(L.luda_stream_create(ctypes.byref(s)))
-    arena, offs, lens = _synth_c4_runs(L, 8, n, 0xC4, s.value)
+    import bench
+    arena, offs, lens = bench.synth_c4(L, 8, n, 0xC4, s.value)
     desc, keep = _desc(_native, arena.data_ptr(), arena.numel(), offs, lens, list(range(9)))
     res = _native.JobResult()
     _native.check(L.luda_compact(ctypes.byref(desc), ctypes.byref(res), s.value))
