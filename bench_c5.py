@@ -224,6 +224,8 @@ def build_files(L, synth: Synth, level: str, f0: int, f1: int, stream, values_po
     span = values_pool.numel() - spec.vlen
     voff = (idx * (2654435761 if level == "up" else 40503) + (0 if level == "up" else 7)) % span
     vl = torch.full((n,), spec.vlen, dtype=torch.int32, device=hi.device)
+    # the builder runs on its own stream: torch's producers of keys/tr/voff/vl must be done
+    torch.cuda.current_stream(hi.device).synchronize()
     res = _native.JobResult()
     _native.check(L.luda_build_files_from_sorted(keys.data_ptr(), spec.klen, tr.data_ptr(), values_pool.data_ptr(),
                                                  voff.data_ptr(), vl.data_ptr(), n, 4096, 16, 10, 1 << 31, F,
@@ -259,6 +261,7 @@ def stage_range(L, synth, bounds_up, bounds_lo, lo_key, hi_key, stream, pool, de
         parts.append(("up", u0, build_files(L, synth, "up", u0, u1, stream, pool)))
     total = sum(r.out_bytes for _, _, r in parts) + 4096
     arena = torch.empty(total, dtype=torch.uint8, device=device)
+    torch.cuda.current_stream(device).synchronize()  # (the block may come from a tensor torch just freed)
     offs, lens, at, owned = [], [], 0, 0
     for level, f0, r in parts:
         _native.check(L.luda_memcpy_d2d_async(arena.data_ptr() + at, r.out, r.out_bytes, stream))

@@ -138,6 +138,8 @@ typedef struct {
   double k_ms[8];               /* kernels: decode, merge(final), block_jump, encode, meta, -, -, - */
   uint64_t launches;            /* kernels launched by this job                   */
   void* priv;
+  uint32_t* sst_key_len;        /* host[n_sst*2]: internal key lengths of sst_keys;
+                                   key_len is then the slot size per key           */
 } luda_job_result;
 
 int luda_compact(const luda_job_desc* job, luda_job_result* result, void* stream);

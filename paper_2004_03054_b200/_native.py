@@ -63,6 +63,7 @@ class JobResult(ctypes.Structure):
         ("k_ms", ctypes.c_double * 8),
         ("launches", ctypes.c_uint64),
         ("priv", ctypes.c_void_p),
+        ("sst_key_len", ctypes.POINTER(ctypes.c_uint32)),
     ]
 
 
@@ -143,6 +144,18 @@ def lib(device_ordinal: int = 0):
 
 
 OPT_PLANNER_TILE = 1  # include/luda_b200.h enum luda_option
+
+
+def sst_key_pairs(res):
+    """[(smallest, largest)] internal keys of a JobResult's SSTs (slots of
+    res.key_len bytes holding res.sst_key_len[i] key bytes)."""
+    S = res.key_len
+    keys = ctypes.string_at(res.sst_keys, 2 * S * res.n_sst)
+    out = []
+    for i in range(res.n_sst):
+        a, b = res.sst_key_len[2 * i], res.sst_key_len[2 * i + 1]
+        out.append((keys[2 * S * i:2 * S * i + a], keys[2 * S * i + S:2 * S * i + S + b]))
+    return out
 
 
 def check(status: int):

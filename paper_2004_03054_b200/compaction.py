@@ -212,11 +212,9 @@ class JobRunner:
         _native.check(self.L.luda_stage_out_async(self.pin_out.ptr, res.out, n, s_out))
         _native.check(self.L.luda_stream_sync(s_out))
         raw = bytes(self.pin_out.view(n))
-        K = res.key_len
-        keys = ctypes.string_at(res.sst_keys, 2 * K * res.n_sst)
-        for i in range(res.n_sst):
+        for i, (sm, lg) in enumerate(_native.sst_key_pairs(res)):
             o, ln = res.sst_off[i], res.sst_len[i]
-            outs.append((raw[o:o + ln], keys[2 * K * i:2 * K * i + K], keys[2 * K * i + K:2 * K * (i + 1)]))
+            outs.append((raw[o:o + ln], sm, lg))
         return outs
 
     def run(self, pj: PreparedJob, n_lower_files: int):

@@ -147,6 +147,7 @@ struct Scratch {
 struct JobPriv {
   std::vector<uint64_t> off, len;
   std::vector<uint8_t> keys;
+  std::vector<uint32_t> klens;
   cudaStream_t st = nullptr;  // stream the output buffer was allocated on
 };
 
@@ -198,6 +199,7 @@ const char* block_msg(uint32_t code) {
     case B_TRAILING: return "trailing garbage in block entries";
     case B_KEYLEN: return "keys of differing lengths in one job are not supported by the b200 fast path";
     case B_VALUE_BIG: return "value longer than 16 MiB (or arena beyond 1 TiB) not supported by the b200 fast path";
+    case B_KEYLONG: return "user keys longer than 71 bytes (or internal keys shorter than the 8-byte trailer) are not supported by the b200 path";
     default: return "block error";
   }
 }
@@ -234,6 +236,23 @@ KeyBound make_bound(const uint8_t* key, uint32_t klen, uint32_t L, bool lower, b
   if (lower) b.incl = klen <= L;
   else if (closed) b.incl = klen >= L;
   else b.incl = klen > L;
+  return b;
+}
+
+// Var jobs (luda_rec.cuh): the bound is represented exactly — padded to
+// 8 kVarW - 1 bytes plus its length byte — so comparisons are exact.
+KeyBound make_bound_var(const uint8_t* key, uint32_t klen, bool lower, bool closed) {
+  KeyBound b{};
+  b.present = 1;
+  uint8_t pad[8 * kVarW] = {0};
+  memcpy(pad, key, std::min<uint32_t>(klen, kVarMaxLen));
+  pad[8 * kVarW - 1] = (uint8_t)klen;
+  for (int w = 0; w < kVarW; ++w) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v = (v << 8) | pad[8 * w + i];
+    b.k[w] = v;
+  }
+  b.incl = lower ? 1u : (closed ? 1u : 0u);
   return b;
 }
 
@@ -385,6 +404,7 @@ struct EmitParams {
   uint64_t sst_target;
   uint32_t min_entry;         // lower bound of one encoded entry (sizes the planner halo)
   uint64_t file_entries = 0;  // > 0: cut an SST every file_entries entries instead of by size
+  bool var = false;           // generic-length keys (W = kVarW records)
 };
 
 // Plan + encode the survivors `S[0..n)` whose values live in `varena`.
@@ -409,7 +429,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(jmp, uint32_t, n, false);
   GET(bsz, uint32_t, n, false);
   GET(ctl, unsigned int, 4, true);  // jmax, overflow, jmax_sst
-  BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1, p.file_entries};
+  BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1, p.file_entries, p.var};
   const size_t jsm = (2ull * (kJumpTile + halo) + 1) * 4;
   CK(cudaFuncSetAttribute(block_jump_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
   KT_START(2, st);
@@ -460,7 +480,21 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(sst_nent, uint64_t, nsst, false);
   GET(sst_last, uint32_t, nsst, false);
   GET(sst_off, uint64_t, nsst + 1, false);
-  SstLayoutArgs la{sch.nodes, nsst, nblk, blk_first, blk_pos, n, p.K, p.bpk, sst_size, sst_data, sst_nent, sst_last};
+  uint64_t* blk_ipos = nullptr;  // var jobs: index entries differ in size
+  if (p.var) {
+    GET(isz, uint32_t, nblk, false);
+    GET(ipos, uint64_t, nblk + 1, false);
+    index_entry_size_kernel<W><<<(nblk + 255) / 256, 256, 0, st>>>(S, blk_first, blk_n, nblk, isz);
+    ++g_launches;
+    const uint64_t nt = std::max<uint64_t>(1, (nblk + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
+    GET(lb, uint64_t, nt, true);
+    GET(ctr, unsigned int, 1, true);
+    scan_excl_kernel<uint32_t><<<(unsigned)nt, kScanThreads, 0, st>>>(isz, nblk, ipos, lb, ctr);
+    ++g_launches;
+    blk_ipos = ipos;
+  }
+  SstLayoutArgs la{sch.nodes, nsst, nblk, blk_first, blk_pos, n, p.K, p.bpk, sst_size, sst_data, sst_nent, sst_last,
+                   blk_ipos};
   sst_layout_kernel<<<(nsst + 255) / 256, 256, 0, st>>>(la);
   ++g_launches;
   {
@@ -502,7 +536,9 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(bigs, uint32_t, big_words + 16, true);
   GET(d_soff, uint64_t, nsst, false);
   CK(cudaMemcpyAsync(d_soff, soff.data(), 8ull * nsst, cudaMemcpyHostToDevice, st));
-  GET(d_keys, uint8_t, 2ull * nsst * p.K, false);
+  const uint32_t key_slot = p.var ? 8 * kVarW + 8 : p.K;
+  GET(d_keys, uint8_t, 2ull * nsst * key_slot, false);
+  GET(d_klen, uint32_t, 2ull * nsst, false);
   // ---- encode data blocks ----
   GET(blk_out, uint64_t, nblk, false);
   block_out_kernel<<<(nblk + 255) / 256, 256, 0, st>>>(blk_pos, nblk, sch.nodes, nsst, sst_off, blk_out);
@@ -513,7 +549,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   const uint32_t s_edbg = 0;
 #endif
   EncodeArgs<W> ea{varena, S, p.K, p.ri, nblk, blk_first, blk_n, blk_size, blk_pos, sch.nodes, nsst, sst_off,
-                   blk_out, res->out, s_edbg};
+                   blk_out, res->out, s_edbg, p.var};
   const size_t esm = sizeof(CrcSmem) + (size_t)kEncPairs * sizeof(EncPairSmem) + sizeof(EncCtaSmem);
   CK(cudaFuncSetAttribute(encode_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
   const unsigned egrid = (unsigned)std::min<uint64_t>((nblk + kEncPairs - 1) / kEncPairs, (uint64_t)g_num_sms);
@@ -525,7 +561,8 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   // ---- filter / index / footer ----
   const uint32_t kprobes = std::max(1, std::min(30, (int)std::lround(p.bpk * std::log(2.0))));
   MetaArgs<W> ma{S, p.K, p.bpk, kprobes, nsst, sch.nodes, sst_last, sst_off, sst_data, sst_nent, sst_size,
-                 blk_first, blk_n, blk_size, blk_pos, res->out, bigs, d_soff, d_keys};
+                 blk_first, blk_n, blk_size, blk_pos, res->out, bigs, d_soff, d_keys, d_klen, key_slot, p.var,
+                 blk_ipos};
   CK(cudaFuncSetAttribute(sst_meta_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMetaSmem));
   KT_START(4, st);
   sst_meta_kernel<W><<<std::min<uint32_t>(nsst, (uint32_t)g_num_sms), kMetaThreads, kMetaSmem, st>>>(ma);
@@ -533,21 +570,27 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   KT_STOP(4, st);
   CK(cudaGetLastError());
   if (ev) CK(cudaEventRecord(ev[1], st));
-  priv->keys.resize(2ull * nsst * p.K);
+  priv->keys.resize(2ull * nsst * key_slot);
+  priv->klens.resize(2ull * nsst);
   CK(cudaMemcpyAsync(priv->keys.data(), d_keys, priv->keys.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(priv->klens.data(), d_klen, 4ull * priv->klens.size(), cudaMemcpyDeviceToHost, st));
   rc = sync(st);
   if (rc) return rc;
   res->n_sst = nsst;
   res->sst_off = priv->off.data();
   res->sst_len = priv->len.data();
   res->sst_keys = priv->keys.data();
+  res->sst_key_len = priv->klens.data();
+  res->key_len = key_slot;
   return LUDA_OK;
 }
+
+constexpr int kRetryVar = 100;  // internal: a fixed-K job met another key length → rerun as a var job
 
 template <int W>
 int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_job_result* res, uint32_t K,
               uint32_t nblk, const BlockTable& bt, const uint32_t* d_file_blk_base,
-              cudaEvent_t* ev) {
+              cudaEvent_t* ev, bool var) {
   const uint32_t L = K - 8;
   res->blocks_in = nblk;
   // ---- decode ----
@@ -580,7 +623,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
 #else
     const uint32_t s_dbg = 0;
 #endif
-    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, errs, errs + 1, s_dbg};
+    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, errs, errs + 1, s_dbg, var};
     KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
     ++g_launches;
@@ -601,6 +644,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
       const uint32_t b = (uint32_t)(e >> 8), code = (uint32_t)(e & 0xFF);
       uint32_t foff = 0;
       CK(cudaMemcpy(&foff, bt.foff + b, 4, cudaMemcpyDeviceToHost));
+      if (!ref && code == B_KEYLEN && !var) return kRetryVar;
       if (!ref) return fail(LUDA_UNSUPPORTED, block_msg(code));
       if (code == B_CRC) return fail(LUDA_CORRUPT, block_msg(code), foff);
       return fail(LUDA_FORMAT, block_msg(code));
@@ -641,9 +685,11 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     const uint8_t* kp = jd->deeper_keys;
     for (uint32_t i = 0; i < jd->n_deeper; ++i) {
       const uint32_t llo = jd->deeper_lens[2 * i], lhi = jd->deeper_lens[2 * i + 1];
-      bounds.push_back(make_bound(kp, llo, L, true, true));
+      if (var && (llo > kVarMaxLen || lhi > kVarMaxLen))
+        return fail(LUDA_UNSUPPORTED, "key-range bound longer than 71 bytes");
+      bounds.push_back(var ? make_bound_var(kp, llo, true, true) : make_bound(kp, llo, L, true, true));
       kp += llo;
-      bounds.push_back(make_bound(kp, lhi, L, false, true));
+      bounds.push_back(var ? make_bound_var(kp, lhi, false, true) : make_bound(kp, lhi, L, false, true));
       kp += lhi;
     }
   }
@@ -655,8 +701,14 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   }
   ra.deeper = d_bounds;
   ra.n_deeper = jd->n_deeper;
-  if (jd->range_lo) ra.range_lo = make_bound(jd->range_lo, jd->range_lo_len, L, true, true);
-  if (jd->range_hi) ra.range_hi = make_bound(jd->range_hi, jd->range_hi_len, L, false, false);
+  if (var && ((jd->range_lo && jd->range_lo_len > kVarMaxLen) || (jd->range_hi && jd->range_hi_len > kVarMaxLen)))
+    return fail(LUDA_UNSUPPORTED, "key-range bound longer than 71 bytes");
+  if (jd->range_lo)
+    ra.range_lo = var ? make_bound_var(jd->range_lo, jd->range_lo_len, true, true)
+                      : make_bound(jd->range_lo, jd->range_lo_len, L, true, true);
+  if (jd->range_hi)
+    ra.range_hi = var ? make_bound_var(jd->range_hi, jd->range_hi_len, false, false)
+                      : make_bound(jd->range_hi, jd->range_hi_len, L, false, false);
   ra.resolve = true;
   // runs in merge-priority order; a run with a violated file seam is split into per-file runs
   std::vector<RunSeg> runs;
@@ -687,7 +739,9 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   }
   if (ev) CK(cudaEventRecord(ev[3], st));
   // survivors have distinct user keys → LCP < L → unshared >= 9 → entry >= 12 B
-  EmitParams ep{K, jd->block_size, jd->restart_interval, jd->bits_per_key, jd->sst_size_target, 12};
+  // fixed K: survivors have distinct user keys → LCP < L → unshared >= 9 → entry >= 12 B; var: >= 4 B
+  EmitParams ep{K, jd->block_size, jd->restart_interval, jd->bits_per_key, jd->sst_size_target, var ? 4u : 12u, 0,
+                var};
   return plan_and_emit<W>(st, scratch, S, n_out, jd->arena, ep, res, ev ? ev + 4 : nullptr);
 }
 
@@ -1098,10 +1152,10 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   }
   const uint32_t nblk = fbb[nf];
   if (nblk == 0) return LUDA_OK;  // no data blocks: empty output
-  if (mixed) return fail(LUDA_UNSUPPORTED, "keys of differing lengths in one job are not supported by the b200 fast path");
-  if (K < 8) return fail(LUDA_UNSUPPORTED, "internal keys shorter than the 8-byte trailer");
-  const uint32_t L = K - 8;
-  if (L > 32) return fail(LUDA_UNSUPPORTED, "user keys longer than 32 bytes are not supported by the b200 fast path");
+  // Fixed-K records when every index key has one length <= 32 bytes; else
+  // (mixed lengths, longer keys) the generic-length "var" records.
+  bool var = mixed || K < 8 || K - 8 > 32;
+  const uint32_t L = var ? 8 * kVarW : K - 8;
   GET(d_fbb, uint32_t, nf + 1, false);
   CK(cudaMemcpyAsync(d_fbb, fbb.data(), 4ull * (nf + 1), cudaMemcpyHostToDevice, st));
   BlockTable bt{};
@@ -1121,12 +1175,20 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   const uint32_t W = std::max<uint32_t>(1, (L + 7) / 8);
   CK(cudaEventRecord(ev[1], st));
   cudaEvent_t* pev = ev;
-  switch (W) {
-    case 1: rc = compact_w<1>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
-    case 2: rc = compact_w<2>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
-    case 3: rc = compact_w<3>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
-    default: rc = compact_w<4>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev); break;
+  if (!var) {
+    switch (W) {
+      case 1: rc = compact_w<1>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev, false); break;
+      case 2: rc = compact_w<2>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev, false); break;
+      case 3: rc = compact_w<3>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev, false); break;
+      default: rc = compact_w<4>(st, scratch, jd, res, K, nblk, bt, d_fbb, pev, false); break;
+    }
+    if (rc == kRetryVar) {  // a data block holds another key length than the index keys
+      luda_job_release(res);
+      memset(res, 0, sizeof(*res));
+      var = true;
+    }
   }
+  if (var) rc = compact_w<kVarW>(st, scratch, jd, res, 8 * kVarW + 8, nblk, bt, d_fbb, pev, true);
   if (rc) {
     luda_job_release(res);
     return rc;

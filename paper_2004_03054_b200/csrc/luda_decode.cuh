@@ -48,6 +48,7 @@ enum BlockCode : uint32_t {
   B_TRAILING = 7,       // trailing garbage in block entries
   B_KEYLEN = 8,         // (unsupported) key length differs from the job's K
   B_VALUE_BIG = 9,      // (unsupported) value length >= 2^24 or arena offset >= 2^40
+  B_KEYLONG = 10,       // (unsupported) user key longer than kVarMaxLen (71) bytes
 };
 
 // Paired warps: a PARSE warp (producer + walk + records) and a CRC warp share
@@ -100,6 +101,7 @@ struct DecodeArgs {
   unsigned long long* err_ref;
   unsigned long long* err_unsup;
   uint32_t dbg;             // ablation switches (LUDA_ABLATION builds only)
+  bool var;                 // generic-length keys (W = kVarW records, dec_var_block)
 };
 
 // Block range of warp segment w of nw: [w*nblk/nw, (w+1)*nblk/nw).
@@ -573,6 +575,81 @@ __device__ __forceinline__ void dec_phase2(const DecodeArgs<W>& a, uint32_t b, D
   }
 }
 
+// Var jobs (keys of any length <= 71 bytes): lane 0 walks the block exactly
+// like decode_data_block (blocks.py:151-164: sequential, restart offsets
+// ignored, the same error order), rebuilds every internal key in `kbuf`
+// (prev[:shared] ∥ key bytes) and writes kVarW records (luda_rec.cuh).
+// Returns the block's entry count (records beyond `cap` are not written; the
+// host re-runs with a larger segment capacity).
+template <int W>
+__device__ uint64_t dec_var_block(const DecodeArgs<W>& a, uint32_t b, uint64_t addr, uint32_t len, const uint8_t* d,
+                                  uint64_t base, uint64_t cap, uint8_t* kbuf) {
+  uint64_t n = 0;
+  uint32_t code = 0, unsup = 0;
+  if (lane_id() == 0) {
+    if (len < 12) {
+      code = B_SHORT;
+    } else {
+      const uint32_t nres = ld_u32_le(d + len - 8);
+      const int64_t entries_end = (int64_t)len - 8 - 4 * (int64_t)nres;
+      if (nres < 1 || entries_end < 0) {
+        code = B_RESTART;
+      } else {
+        const uint64_t payload = len - 4, ee = (uint64_t)entries_end;
+        uint64_t pos = 0, prev_len = 0;
+        while (pos < ee) {
+          uint64_t sh, u, vl;
+          int r;
+          if ((r = varint_read(d, payload, pos, sh)) || (r = varint_read(d, payload, pos, u)) ||
+              (r = varint_read(d, payload, pos, vl))) {
+            code = r == 1 ? B_VARINT_TRUNC : B_VARINT_LONG;
+            break;
+          }
+          if (sh > prev_len || u > ee || vl > ee || pos + u + vl > ee) {
+            code = B_TRUNC_ENTRY;
+            break;
+          }
+          const uint64_t ke = sh + u;
+          if (ke < 8 || ke - 8 > kVarMaxLen) unsup = unsup ? unsup : (uint32_t)B_KEYLONG;
+          if (vl > kMaxValueLen) unsup = unsup ? unsup : (uint32_t)B_VALUE_BIG;
+          if (!unsup) {
+            for (uint32_t j = 0; j < (uint32_t)u; ++j) kbuf[sh + j] = d[pos + j];
+            if (base + n < cap) {
+              const uint32_t lr = (uint32_t)ke - 8;
+              Rec<W> rec;
+#pragma unroll
+              for (int w = 0; w < W; ++w) {
+                uint64_t v = 0;
+                for (int q = 0; q < 8; ++q) {
+                  const uint32_t idx = 8u * w + q;
+                  v = (v << 8) | (idx < lr ? kbuf[idx] : 0u);
+                }
+                rec.k[w] = v;
+              }
+              rec.k[W - 1] |= lr;  // byte 71: the length (always padding: lr <= 71)
+              uint64_t tr = 0;
+              for (int q = 7; q >= 0; --q) tr = (tr << 8) | kbuf[lr + q];
+              rec.t = ~tr;
+              rec.h = handle_pack(addr + pos + u, vl);
+              a.out[base + n] = rec;
+            }
+          }
+          prev_len = ke;
+          pos += u + vl;
+          ++n;
+        }
+        if (!code && pos != ee) code = B_TRAILING;
+      }
+    }
+  }
+  n = __shfl_sync(0xFFFFFFFFu, n, 0);
+  code = __shfl_sync(0xFFFFFFFFu, code, 0);
+  unsup = __shfl_sync(0xFFFFFFFFu, unsup, 0);
+  if (lane_id() == 0 && code) atomicMin(a.err_ref, ((unsigned long long)b << 8) | code);
+  if (lane_id() == 0 && !code && unsup) atomicMin(a.err_unsup, ((unsigned long long)b << 8) | unsup);
+  return code || unsup ? 0 : n;
+}
+
 // CRC-32 of a staged block's payload [data, data + n), n >= 4, WITHOUT
 // touching any byte the parse warp reads: the <= 15 garbage bytes between
 // the TMA window start and `data` and the <= 3 stored-CRC bytes after the
@@ -673,7 +750,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       const uint8_t* gp = a.arena + mt.addr;
       if (lane == 0) a.blk_local[b] = (uint32_t)cnt;
       uint64_t n = 0;
-      if (!LUDA_ABLATE(a, 4)) {
+      if (a.var) {
+        const uint8_t* d = mt.staged ? ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15) : gp;
+        n = dec_var_block<W>(a, b, mt.addr, mt.len, d, seg0 + cnt, seg1, ps.entries);
+      } else if (!LUDA_ABLATE(a, 4)) {
         if (mt.staged) {
           const uint8_t* d = ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15);
           DecState stt = dec_phase1<W, true>(a, b, mt.addr, mt.len, d, slots);

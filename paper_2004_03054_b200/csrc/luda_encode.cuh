@@ -257,6 +257,7 @@ struct EncodeArgs {
   const uint64_t* blk_out;   // output offset of every block
   uint8_t* out;
   uint32_t dbg;              // ablation switches (LUDA_ABLATION builds only)
+  bool var;                  // generic-length keys: K per record, generic block path
 };
 
 // Output offset of every block: its SST's offset + its data offset in the SST.
@@ -307,9 +308,11 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
     prev_rec.t = __shfl_sync(0xFFFFFFFFu, r.t, 31);
     uint32_t s = 0, u = 0, vl = 0, hv = 0, esz = 0;
     uint64_t voff = 0;
+    uint32_t Lr = L;
     if (act) {
-      if (i % ri != 0) s = ikey_lcp(pr, r, L);
-      u = K - s;
+      Lr = rec_ulen(r, a.var, L);
+      if (i % ri != 0) s = ikey_lcp_any(pr, r, a.var, L);
+      u = Lr + 8 - s;
       vl = handle_len(r.h);
       voff = handle_off(r.h);
       hv = varint_size(s) + varint_size(u) + varint_size(vl);
@@ -323,7 +326,7 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
       uint32_t h = put_varint(p, s);
       h += put_varint(p + h, u);
       h += put_varint(p + h, vl);
-      put_key_tail<W>(p + h, r, L, s);
+      put_key_tail<W>(p + h, r, Lr, s);
       if (i % ri == 0) put_u32(dst + entries_end + 4 * (i / ri), off);
     }
     __syncwarp();  // headers/keys written before values (edge words are read-modified-written)
@@ -452,7 +455,7 @@ __device__ __forceinline__ void enc_load(const EncodeArgs<W>& a, uint32_t k, Enc
 template <int W>
 __device__ __forceinline__ void enc_layout(const EncodeArgs<W>& a, EncLane<W>& e) {
   const uint32_t lane = lane_id();
-  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage && a.K < 128;
+  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage && a.K < 128 && !a.var;
   if (!e.fast) return;
   const uint32_t K = a.K, L = K - 8;
   const bool act = lane < e.cnt;
@@ -722,7 +725,11 @@ struct MetaArgs {
   uint8_t* out;
   uint32_t* scratch;           // zeroed, for filters larger than kMetaBuf
   const uint64_t* scratch_off; // per SST word offset into scratch (or ~0)
-  uint8_t* sst_keys;           // [nsst][2][K]
+  uint8_t* sst_keys;           // [nsst][2][key_slot]
+  uint32_t* sst_key_len;       // [nsst][2] internal key lengths
+  uint32_t key_slot;           // bytes per key slot (K, or 8 kVarW + 8 for var jobs)
+  bool var;
+  const uint64_t* blk_ipos;    // var jobs: index-entry offsets (luda_plan.cuh), else nullptr
 };
 
 // Bloom hash h = crc32(user key) (bloom.py:28-29): 4-byte words of the key
@@ -788,7 +795,7 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
         // together (ILP) before any probe
         uint32_t h[kMetaUnroll];
 #pragma unroll
-        for (int u = 0; u < kMetaUnroll; ++u) h[u] = user_key_crc<W>(r[u], L, tl);
+        for (int u = 0; u < kMetaUnroll; ++u) h[u] = user_key_crc<W>(r[u], rec_ulen(r[u], a.var, L), tl);
 #pragma unroll
         for (int u = 0; u < kMetaUnroll; ++u) {
           if (e0 + (uint64_t)u * kMetaThreads < e_end) {
@@ -805,7 +812,8 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
       }
     } else {
       for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
-        const uint32_t h = user_key_crc<W>(a.rec[e], L, tl);
+        const Rec<W> re = a.rec[e];
+        const uint32_t h = user_key_crc<W>(re, rec_ulen(re, a.var, L), tl);
         const uint32_t delta = (h >> 17) | (h << 15);
         uint64_t p = (uint64_t)h % nbits;
         const uint64_t step = (uint64_t)delta % nbits;
@@ -831,19 +839,20 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
     const uint32_t vK = varint_size(K);
     const uint64_t E = vK + K + 8;
     const uint32_t nb = eb - fb;
-    const uint64_t ibody = (uint64_t)nb * E + 4;  // entries ∥ count
+    const uint64_t ibody = (a.blk_ipos ? a.blk_ipos[eb] - a.blk_ipos[fb] : (uint64_t)nb * E) + 4;  // entries ∥ count
     const bool ismall = ibody <= (uint64_t)kMetaBuf;
     uint8_t* ib = ismall ? buf : fout + data + flen;
     for (uint32_t i = tid; i < nb; i += kMetaThreads) {
       const uint32_t b = fb + i;
-      uint8_t* p = ib + (uint64_t)i * E;
-      put_varint(p, K);
       const Rec<W> last = a.rec[(uint64_t)a.blk_first[b] + a.blk_n[b] - 1];
-      put_key_tail<W>(p + vK, last, L, 0);
-      put_u32(p + vK + K, (uint32_t)(a.blk_pos[b] - a.blk_pos[fb]));
-      put_u32(p + vK + K + 4, a.blk_size[b]);
+      const uint32_t Lb = rec_ulen(last, a.var, L), Kb = Lb + 8;
+      uint8_t* p = ib + (a.blk_ipos ? a.blk_ipos[b] - a.blk_ipos[fb] : (uint64_t)i * E);
+      const uint32_t vKb = put_varint(p, Kb);
+      put_key_tail<W>(p + vKb, last, Lb, 0);
+      put_u32(p + vKb + Kb, (uint32_t)(a.blk_pos[b] - a.blk_pos[fb]));
+      put_u32(p + vKb + Kb + 4, a.blk_size[b]);
     }
-    if (tid == 0) put_u32(ib + (uint64_t)nb * E, nb);
+    if (tid == 0) put_u32(ib + ibody - 4, nb);
     __syncthreads();
     if (!ismall) __threadfence();
     __syncthreads();
@@ -864,7 +873,9 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
     // smallest / largest internal keys
     if (tid < 2 && ne > 0) {
       const Rec<W> r = a.rec[tid == 0 ? fe : fe + ne - 1];
-      put_key_tail<W>(a.sst_keys + ((uint64_t)s * 2 + tid) * K, r, L, 0);
+      const uint32_t Lr = rec_ulen(r, a.var, L);
+      put_key_tail<W>(a.sst_keys + ((uint64_t)s * 2 + tid) * a.key_slot, r, Lr, 0);
+      a.sst_key_len[(uint64_t)s * 2 + tid] = Lr + 8;
     }
     __syncthreads();  // buf is reused by the next SST
   }

@@ -26,7 +26,7 @@ constexpr int kMergeItems = 6;
 constexpr int kMergeTile = kMergeThreads * kMergeItems;
 
 struct KeyBound {
-  uint64_t k[4];
+  uint64_t k[kVarW];
   uint32_t incl;
   uint32_t present;
 };

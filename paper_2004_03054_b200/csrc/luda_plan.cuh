@@ -45,6 +45,7 @@ struct BlockJumpArgs {
   unsigned int* jmax;
   unsigned int* overflow;
   uint64_t file_entries;  // > 0: a block never crosses a multiple of this (file-cut builds)
+  bool var;               // generic-length keys: K per record (luda_rec.cuh)
 };
 
 // Block size if a block started at local index i held n entries:
@@ -75,10 +76,11 @@ __global__ void __launch_bounds__(kJumpThreads) block_jump_kernel(BlockJumpArgs<
       const Rec<W> cur = a.rec[j];
       const uint32_t vl = handle_len(cur.h);
       const uint32_t vv = varint_size(vl);
+      const uint32_t Kc = a.var ? rec_ulen(cur, true, 0) + 8 : K;
       uint32_t sh = 0;
-      if (j > 0) sh = ikey_lcp(a.rec[j - 1], cur, L);
-      sbv = varint_size(sh) + varint_size(K - sh) + vv + (K - sh) + vl;
-      D[i] = (1 + vK + vv + K + vl) - sbv;
+      if (j > 0) sh = ikey_lcp_any(a.rec[j - 1], cur, a.var, L);
+      sbv = varint_size(sh) + varint_size(Kc - sh) + vv + (Kc - sh) + vl;
+      D[i] = (1 + (a.var ? varint_size(Kc) : vK) + vv + Kc + vl) - sbv;
     } else if (i < span) {
       D[i] = 0;
     }
@@ -355,6 +357,17 @@ __global__ void __launch_bounds__(kChainThreads) chain_emit_kernel(ChainArgs c, 
 }
 
 // ---- block descriptors + exclusive prefix of sizes ----------------------------------
+// Var jobs: index entry size of every block (varint(K) ∥ last key ∥ u32 ∥ u32,
+// sst.py:67-76) with K the block's last internal key length.
+template <int W>
+__global__ void index_entry_size_kernel(const Rec<W>* rec, const uint32_t* blk_first, const uint32_t* blk_n,
+                                        uint32_t nb, uint32_t* isz) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  const uint32_t K = rec_ulen(rec[(uint64_t)blk_first[k] + blk_n[k] - 1], true, 0) + 8;
+  isz[k] = varint_size(K) + K + 8;
+}
+
 __global__ void block_desc_kernel(const uint32_t* nodes, uint32_t nb, const uint32_t* jmp, const uint32_t* bsz,
                                   uint32_t* blk_first, uint32_t* blk_n, uint32_t* blk_size) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -427,6 +440,7 @@ struct SstLayoutArgs {
   uint64_t* sst_data;             // out: data bytes
   uint64_t* sst_nent;             // out: entries
   uint32_t* sst_last_blk;         // out: one past last block
+  const uint64_t* blk_ipos;       // var jobs: exclusive prefix of index-entry sizes [nblk+1], else nullptr
 };
 
 __global__ void sst_layout_kernel(SstLayoutArgs a) {
@@ -442,7 +456,7 @@ __global__ void sst_layout_kernel(SstLayoutArgs a) {
   if (nbits < 64) nbits = 64;
   nbits = (nbits + 7) & ~7ull;
   const uint64_t flen = nbits / 8 + 1 + 4;
-  const uint64_t ilen = (uint64_t)(eb - fb) * (varint_size(a.K) + a.K + 8) + 8;
+  const uint64_t ilen = (a.blk_ipos ? a.blk_ipos[eb] - a.blk_ipos[fb] : (uint64_t)(eb - fb) * (varint_size(a.K) + a.K + 8)) + 8;
   a.sst_size[s] = data + flen + ilen + 24;
   a.sst_data[s] = data;
   a.sst_nent[s] = ne;

@@ -85,6 +85,21 @@ __device__ __forceinline__ uint32_t ikey_lcp(const Rec<W>& a, const Rec<W>& b, u
   return L + (uint32_t)(__ffsll((long long)x) - 1) / 8;
 }
 
+// ---- generic-length keys ("var" jobs) ---------------------------------------
+// A job whose user keys differ in length, or are longer than 32 bytes, uses
+// W = kVarW records: the key area holds the user key zero-padded to 71 bytes
+// and its LENGTH in the last byte (byte 71 = low byte of k[8]). For keys of
+// length <= 71, padded bytes then length is exactly Python's bytes order
+// (keys.py:60-63): when the padded bytes agree, the shorter key is a prefix of
+// the longer one and sorts first.
+constexpr int kVarW = 9;
+constexpr uint32_t kVarMaxLen = 8 * kVarW - 1;  // 71
+
+template <int W>
+__device__ __forceinline__ uint32_t rec_ulen(const Rec<W>& r, bool var, uint32_t L) {
+  return var ? (uint32_t)(r.k[W - 1] & 0xFFu) : L;
+}
+
 // Byte j (0-based) of the internal key encoded by `r` (user key length L).
 template <int W>
 __device__ __forceinline__ uint32_t ikey_byte(const Rec<W>& r, uint32_t L, uint32_t j) {
@@ -152,6 +167,46 @@ __device__ __forceinline__ void words_to_rec(const uint32_t (&kw)[NW], uint32_t 
   const uint32_t lo = __funnelshift_r(a, b, sh);
   const uint32_t hi = __funnelshift_r(b, c, sh);
   r.t = ~(((uint64_t)hi << 32) | lo);
+}
+
+// Longest common prefix (bytes) of two internal keys of a var job (user keys
+// of any lengths <= 71, blocks.py:33-38 over user_key ∥ trailer): when one user
+// key is a proper prefix of the other, the shorter key's trailer is compared
+// with the longer key's next user bytes (the prefix may run into the trailer).
+template <int W>
+__device__ __forceinline__ uint32_t ikey_lcp_var(const Rec<W>& a, const Rec<W>& b) {
+  const uint32_t la = rec_ulen(a, true, 0), lb = rec_ulen(b, true, 0);
+  uint32_t p = 8u * W - 1;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    uint64_t x = a.k[i] ^ b.k[i];
+    if (i == W - 1) x &= ~0xFFull;  // length byte
+    if (x) {
+      p = 8u * i + (uint32_t)(__clzll((long long)x) >> 3);
+      break;
+    }
+  }
+  const uint32_t m = la < lb ? la : lb;
+  if (p < m) return p;
+  if (la == lb) {
+    const uint64_t x = a.t ^ b.t;
+    if (!x) return la + 8;
+    return la + (uint32_t)(__ffsll((long long)x) - 1) / 8;
+  }
+  const Rec<W>& sh = la < lb ? a : b;
+  const Rec<W>& lg = la < lb ? b : a;
+  const uint32_t ll = la < lb ? lb : la;
+  uint32_t n = m;
+  for (uint32_t j = 0; j < 8; ++j) {
+    if (ikey_byte(sh, m, m + j) != ikey_byte(lg, ll, m + j)) break;
+    ++n;
+  }
+  return n;
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t ikey_lcp_any(const Rec<W>& a, const Rec<W>& b, bool var, uint32_t L) {
+  return var ? ikey_lcp_var(a, b) : ikey_lcp(a, b, L);
 }
 
 }  // namespace luda

@@ -88,12 +88,10 @@ def result_files(res, stream):
         _native.check(L.luda_stage_out_async(buf, res.out, res.out_bytes, stream))
         _native.check(L.luda_stream_sync(stream))
         raw = buf.raw
-        K = res.key_len
-        keys = ctypes.string_at(res.sst_keys, 2 * K * res.n_sst)
         out = []
-        for i in range(res.n_sst):
+        for i, (sm, lg) in enumerate(_native.sst_key_pairs(res)):
             o, n = res.sst_off[i], res.sst_len[i]
-            out.append((raw[o:o + n], keys[2 * K * i:2 * K * i + K], keys[2 * K * i + K:2 * K * (i + 1)]))
+            out.append((raw[o:o + n], sm, lg))
         return out
     finally:
         L.luda_job_release(ctypes.byref(res))

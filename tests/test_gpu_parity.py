@@ -354,3 +354,52 @@ def test_block_entry_format_errors(dev, damage):
         gpu_compact(dev, job, lower, upper, {})
     assert type(got.value).__name__ == type(want.value).__name__, (got.value, want.value)
     assert str(want.value) in str(got.value)
+
+
+@pytest.mark.parametrize("name", [n for n, _, _ in VARKEY_CASES])
+def test_generic_key_lengths(dev, name):
+    """Mixed user-key lengths (0..64 B, prefixes of each other, bytes that
+    collide with trailer bytes) and fixed lengths > 32 B: the generic-length
+    record path (luda_rec.cuh kVarW) vs the oracle and the reference goldens."""
+    check_case(dev, name)
+
+
+@pytest.mark.parametrize("name", [n for n, _, _ in VARKEY_CASES[:6]])
+def test_generic_key_lengths_multitile_planner(dev, small_planner_tiles, name):
+    check_case(dev, name)
+
+
+def test_index_keys_one_length_data_keys_mixed(dev):
+    """Index keys (block last keys) all of one length but data keys of others:
+    the fixed-length decode meets another length and the job is re-run on the
+    generic-length path."""
+    from paper_2004_03054_b200.compaction import compact_files
+    from paper_2004_03054_b200.config import StoreConfig
+    rng = random.Random(0x71)
+    files = []
+    seq = 1
+    for f in range(3):
+        keys = sorted({bytes([f]) + rng.randbytes(rng.randint(0, 14)) for _ in range(12)})
+        keys = [k for k in keys if len(k) < 16][:10] + [bytes([f]) + b"\xff" * 15]
+        pairs = []
+        for k in keys:
+            pairs.append((O.make_ikey(k, seq, O.KIND_PUT), rng.randbytes(8)))
+            seq += 1
+        files.append(O.build_table(pairs, sst_size_target=2**31))
+        assert len(O.open_table(files[-1])[1]) == 1  # one block: the index holds only the 16-byte last key
+    want = O.reference_compact(files[::-1])
+    got = compact_files(dev, files[::-1], [], source_level=0, config=StoreConfig())
+    assert [g[0] for g in got] == [w[0] for w in want]
+    assert [(g[1], g[2]) for g in got] == [(w[1], w[2]) for w in want]
+
+
+def test_user_keys_longer_than_71_bytes_unsupported(dev):
+    from paper_2004_03054_b200 import UnsupportedInputError
+    from paper_2004_03054_b200.compaction import compact_files
+    rng = random.Random(0x72)
+    pairs = sorted(((O.make_ikey(rng.randbytes(80), i + 1, O.KIND_PUT), b"v") for i in range(50)),
+                   key=lambda kv: O.order_key(kv[0]))
+    f = O.build_table(pairs)
+    O.reference_compact([f])  # the reference accepts them
+    with pytest.raises(UnsupportedInputError):
+        compact_files(dev, [f], [], source_level=0)
