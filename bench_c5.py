@@ -146,64 +146,78 @@ class Synth:
         return f * F, min((f + 1) * F, self.n(level))
 
 
-def keys_at(synth: Synth, level: str, idx):
-    """16-byte keys (host bytes, concatenated) of sorted global entry indices."""
+def gather_keys(synth: Synth, idx_up, idx_lo):
+    """16-byte keys of global entry indices of both levels, generating every
+    bucket once: returns (n_up x 16, n_lo x 16) uint8 numpy arrays in the
+    order of the given indices."""
     import numpy as np
     import torch
-    per = synth.spec.up_per_bucket if level == "up" else synth.spec.lo_per_bucket
-    idx = np.asarray(idx, dtype=np.int64)
-    out = []
-    for b in np.unique(idx // per):
-        sel = idx[(idx // per) == b] - b * per
-        bk = synth.bucket(int(b))
-        h, l_ = (bk.up_hi, bk.up_lo) if level == "up" else (bk.lo_hi, bk.lo_lo)
-        t = torch.from_numpy(sel).to(h.device)
-        out.append(key_bytes(h[t], l_[t]))
-    return torch.cat(out).cpu().numpy().tobytes() if out else b""
+    spec = synth.spec
+    idx_up = np.asarray(idx_up, dtype=np.int64)
+    idx_lo = np.asarray(idx_lo, dtype=np.int64)
+    out_up = np.zeros((idx_up.size, 16), dtype=np.uint8)
+    out_lo = np.zeros((idx_lo.size, 16), dtype=np.uint8)
+    bu = idx_up // spec.up_per_bucket
+    bl = idx_lo // spec.lo_per_bucket
+    for b in np.union1d(np.unique(bu), np.unique(bl)):
+        bk = gen_bucket(spec, int(b), synth.device)
+        for idx, bsel, per, h, l_, out in ((idx_up, bu, spec.up_per_bucket, bk.up_hi, bk.up_lo, out_up),
+                                           (idx_lo, bl, spec.lo_per_bucket, bk.lo_hi, bk.lo_lo, out_lo)):
+            m = np.nonzero(bsel == b)[0]
+            if m.size:
+                t = torch.from_numpy(idx[m] - b * per).to(h.device)
+                out[m] = key_bytes(h[t], l_[t]).view(-1, 16).cpu().numpy()
+    return out_up, out_lo
 
 
-def file_bounds(spec: C5Spec, synth: Synth, level: str):
-    """[(first user key, last user key)] of every input file of a level."""
-    nf = spec.n_up_files if level == "up" else spec.n_lo_files
-    n = synth.n(level)
-    F = spec.file_keys
-    idx = []
-    for f in range(nf):
-        idx += [f * F, min((f + 1) * F, n) - 1]
-    kb = keys_at(synth, level, idx)
-    return [(kb[32 * f:32 * f + 16], kb[32 * f + 16:32 * f + 32]) for f in range(nf)]
+def metadata(spec: C5Spec, synth: Synth, world: int, rank: int):
+    """One pass over the generation buckets: (first, last) user key of every
+    input file of both levels, and this rank's index-style samples (files
+    i ≡ rank mod world of each level, `samples_per_file` evenly spaced keys)."""
+    import numpy as np
+    S, F = spec.samples_per_file, spec.file_keys
+    idx = {}
+    for level, nf, n in (("up", spec.n_up_files, spec.n_up), ("lo", spec.n_lo_files, spec.n_lo)):
+        f = np.arange(nf, dtype=np.int64)
+        a, e = f * F, np.minimum((f + 1) * F, n)
+        mine = f[rank::world]
+        smp = (a[mine][:, None] + (np.arange(S)[None, :] * (e[mine] - a[mine])[:, None]) // S).reshape(-1)
+        idx[level] = (nf, mine.size, np.concatenate([a, e - 1, smp]))
+    ku, kl = gather_keys(synth, idx["up"][2], idx["lo"][2])
+    out = {}
+    for level, keys in (("up", ku), ("lo", kl)):
+        nf, nm, _ = idx[level]
+        kb = [bytes(r) for r in keys]
+        out[level] = ([(kb[f], kb[nf + f]) for f in range(nf)], kb[2 * nf:2 * nf + nm * S], nm)
+    return out
 
 
-def plan(spec: C5Spec, synth: Synth, world: int, rank: int, group=None):
+def plan(spec: C5Spec, synth: Synth, world: int, rank: int, group=None, meta=None):
     """§8e steps 1-4 (samples of this rank's files, all-gather, splitters
     snapped to Li+1 file boundaries, contiguous deal). Returns (ranges, my
-    range indices, plan wall ms, sample count)."""
+    range indices, plan wall ms, sample count, file bounds per level)."""
     from paper_2004_03054_b200 import subcompact as SC
     t0 = time.perf_counter()
-    S, F = spec.samples_per_file, spec.file_keys
-    local, firsts = [], []
-    for level, nf in (("up", spec.n_up_files), ("lo", spec.n_lo_files)):
-        n = synth.n(level)
-        idx = []
-        mine = list(range(rank, nf, world))
-        for f in mine:
-            a, e = f * F, min((f + 1) * F, n)
-            idx += [a + (k * (e - a)) // S for k in range(S)]
-        kb = keys_at(synth, level, idx)
-        local += [kb[16 * k:16 * k + 16] for k in range(len(idx))]
-        if level == "up":
-            firsts += [kb[16 * S * q:16 * S * q + 16] for q in range(len(mine))]
-    rows = ((spec.n_up_files + spec.n_lo_files + world - 1) // world) * S
+    meta = meta or metadata(spec, synth, world, rank)
+    S = spec.samples_per_file
+    local = meta["up"][1] + meta["lo"][1]
+    firsts = [meta["up"][1][q * S] for q in range(meta["up"][2])]
+    per_rank = lambda nf: (nf + world - 1) // world  # noqa: E731 — files of the most loaded rank
+    rows = (per_rank(spec.n_up_files) + per_rank(spec.n_lo_files)) * S
     samples = [k for gth in SC.allgather_bytes(SC.encode_samples(local, rows), world, group)
                for k in SC.decode_samples(gth)]
-    frow = (spec.n_up_files + world - 1) // world
-    bounds = [k for gth in SC.allgather_bytes(SC.encode_samples(firsts, frow), world, group)
+    bounds = [k for gth in SC.allgather_bytes(SC.encode_samples(firsts, per_rank(spec.n_up_files)), world, group)
               for k in SC.decode_samples(gth)]
     bounds = sorted(bounds)[1:]  # smallest user key of every Li+1 file but the first
     spl = SC.choose_splitters(samples, bounds, spec.nranges)
     ranges = SC.ranges_from_splitters(spl)
     mine = SC.ranges_of_rank(len(ranges), world, rank)
-    return ranges, mine, (time.perf_counter() - t0) * 1e3, len(samples)
+    return ranges, mine, (time.perf_counter() - t0) * 1e3, len(samples), (meta["up"][0], meta["lo"][0])
+
+
+def file_bounds(spec: C5Spec, synth: Synth, level: str):
+    """[(first user key, last user key)] of every input file of a level."""
+    return metadata(spec, synth, 1, 0)[level][0]
 
 
 def build_files(L, synth: Synth, level: str, f0: int, f1: int, stream, values_pool):
@@ -321,10 +335,8 @@ def run(spec: C5Spec, device_index: int, world: int, rank: int, group=None, step
     L = _native.lib(device_index)
     device = torch.device("cuda", device_index)
     synth = Synth(spec, device)
-    ranges, mine, plan_ms, nsamples = plan(spec, synth, world, rank, group)
+    ranges, mine, plan_ms, nsamples, (bounds_up, bounds_lo) = plan(spec, synth, world, rank, group)
     t0 = time.perf_counter()
-    bounds_up = file_bounds(spec, synth, "up")
-    bounds_lo = file_bounds(spec, synth, "lo")
     pool = values_pool_for(spec, device)
     s = ctypes.c_void_p()
     _native.check(L.luda_stream_create(ctypes.byref(s)))

@@ -33,6 +33,12 @@ def run_compaction(job, device, **kw):
     return _rc(job, device, **kw)
 
 
-__all__ = ["DeviceConfig", "StoreConfig", "make_device", "run_compaction", "CompactionJob", "SstMeta", "Version",
+def run_compactions(jobs, device, **kw):
+    from .compaction import run_compactions as _rcs
+
+    return _rcs(jobs, device, **kw)
+
+
+__all__ = ["DeviceConfig", "StoreConfig", "make_device", "run_compaction", "run_compactions", "CompactionJob", "SstMeta", "Version",
            "LudaError", "FormatError", "CorruptionError", "OrderingError", "SizeOverflowError", "DeviceError",
            "CapacityError", "UnsupportedInputError"]

@@ -72,6 +72,7 @@ class PreparedJob:
     sst_size_target: int = 4 * 2**20
     range_lo: bytes | None = None
     range_hi: bytes | None = None
+    staged: object = None       # StagedInput holding `files` in pinned memory (no host copy)
 
 
 def _read_input(meta, inputs, directory):
@@ -84,7 +85,7 @@ def _read_input(meta, inputs, directory):
 
 
 def prepare(job, *, inputs=None, directory=None, config: StoreConfig | None = None,
-            key_range=None) -> PreparedJob:
+            key_range=None, staged=None) -> PreparedJob:
     """Gather input bytes and the run structure of a CompactionJob.
 
     Run rules: L0 files may overlap (each is its own run, newest first as in
@@ -95,6 +96,11 @@ def prepare(job, *, inputs=None, directory=None, config: StoreConfig | None = No
     files, run_first = [], [0]
     lower = list(job.lower)
     upper = list(job.upper)
+    if staged is not None:  # the job's files, lower then upper, already in pinned memory
+        if len(staged.views) != len(lower) + len(upper):
+            raise ValueError("staged input does not hold the job's files")
+        seq = iter(staged.views)
+        inputs = {m.file_id: next(seq) for m in lower + upper}
     if lower:
         if job.source_level == 0:
             for m in lower:
@@ -113,49 +119,112 @@ def prepare(job, *, inputs=None, directory=None, config: StoreConfig | None = No
                        deeper=deeper_ranges(job.version, job.target_level),
                        block_size=cfg.block_size, restart_interval=cfg.restart_interval,
                        bits_per_key=cfg.bits_per_key, sst_size_target=cfg.sst_size_target,
-                       range_lo=lo, range_hi=hi)
+                       range_lo=lo, range_hi=hi, staged=staged)
+
+
+_COPY_POOL = None
+
+
+def _host_copy_in(dst, files, offs):
+    """Copy bytes-like files into pinned staging at dst + offs[i]. ctypes
+    calls release the GIL, so large jobs are copied by several threads."""
+    def one(f, o):
+        if isinstance(f, bytes):
+            ctypes.memmove(dst + o, f, len(f))
+            return
+        mv = memoryview(f).cast("B")
+        if mv.readonly:
+            ctypes.memmove(dst + o, bytes(mv), len(mv))
+        else:
+            ctypes.memmove(dst + o, (ctypes.c_char * len(mv)).from_buffer(mv), len(mv))
+    total = sum(len(f) for f in files)
+    if total < (64 << 20) or len(files) < 4:
+        for f, o in zip(files, offs):
+            one(f, o)
+        return
+    global _COPY_POOL
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _COPY_POOL = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    list(_COPY_POOL.map(lambda fo: one(*fo), zip(files, offs)))
+
+
+class StagedInput:
+    """A job's input files already in PINNED host memory, laid out as the
+    device arena (``JobRunner.layout``): staging them is one H2D per stream,
+    no host copy. Fill ``views[i]`` (writable memoryviews), e.g. with
+    ``fileobj.readinto(view)``, then pass ``staged=`` to run_compaction(s)."""
+
+    def __init__(self, sizes):
+        self.sizes = list(sizes)
+        self.offs, self.total = JobRunner.layout_sizes(self.sizes)
+        self.buf = PinnedBuffer()
+        self.buf.ensure(self.total)
+        raw = memoryview(self.buf.view(self.total)).cast("B")
+        self.views = [raw[o:o + n] for o, n in zip(self.offs, self.sizes)]
+
+    def free(self):
+        self.views = []
+        self.buf.free()
 
 
 class JobRunner:
-    """Keeps the pinned staging, device arena and output buffers of a device
-    across jobs (so repeated jobs do not re-pin or re-allocate)."""
+    """Double-buffered job pipeline of one device (SPEC.md:632 A7).
+
+    Job k is staged (H2D of its files on the in_lower / in_upper streams, from
+    pinned host memory) into device arena k % 2 while job k-1 compacts on the
+    compute stream and job k-2's outputs stream back on the out stream into
+    pinned output buffer (k-2) % 2. Inputs given as bytes-like objects are
+    first copied into pinned staging (one host copy); a ``StagedInput`` is
+    staged as is. Outputs are returned as memoryviews into the pinned output
+    buffer: valid until the pipeline advances past the next job (copy with
+    ``bytes()`` to keep them longer)."""
 
     def __init__(self, device: B200Device):
         self.device = device
         self.L = device._L
-        self.pin_in = PinnedBuffer()
-        self.pin_out = PinnedBuffer()
-        self.arena = None
-        self._keep = []
+        self.pin_in = [PinnedBuffer(), PinnedBuffer()]
+        self.pin_out = [PinnedBuffer(), PinnedBuffer()]
+        self.arena = [None, None]
 
-    def _arena(self, nbytes):
-        if self.arena is None or self.arena.capacity < nbytes:
-            if self.arena is not None:
-                self.device.free(self.arena)
-            self.arena = self.device.alloc(nbytes, label="job-arena")
-        return self.arena
+    def _arena(self, k, nbytes):
+        a = self.arena[k]
+        if a is None or a.capacity < nbytes:
+            if a is not None:
+                self.device.free(a)
+            a = self.arena[k] = self.device.alloc(nbytes, label=f"job-arena-{k}")
+        return a
 
-    def layout(self, files):
+    @staticmethod
+    def layout_sizes(sizes):
         offs, pos = [], ARENA_PAD
-        for f in files:
+        for n in sizes:
             offs.append(pos)
-            pos += (len(f) + ARENA_ALIGN - 1) // ARENA_ALIGN * ARENA_ALIGN
+            pos += (n + ARENA_ALIGN - 1) // ARENA_ALIGN * ARENA_ALIGN
         return offs, pos + ARENA_PAD
 
-    def stage(self, pj: PreparedJob, n_lower_files: int):
-        """Copy inputs to pinned memory and H2D on in_lower / in_upper."""
-        offs, total = self.layout(pj.files)
-        self.pin_in.ensure(total)
-        for f, o in zip(pj.files, offs):
-            ctypes.memmove(self.pin_in.ptr + o, bytes(f) if not isinstance(f, bytes) else f, len(f))
-        arena = self._arena(total)
+    def layout(self, files):
+        return self.layout_sizes([len(f) for f in files])
+
+    def stage(self, pj: PreparedJob, n_lower_files: int, k: int):
+        """Pinned staging (unless pre-staged) + H2D into arena k on in_lower /
+        in_upper; the compute stream waits for both copies."""
+        staged = getattr(pj, "staged", None)
+        if staged is not None:
+            offs, total, src = staged.offs, staged.total, staged.buf.ptr
+        else:
+            offs, total = self.layout(pj.files)
+            self.pin_in[k].ensure(total)
+            src = self.pin_in[k].ptr
+            _host_copy_in(src, pj.files, offs)
+        arena = self._arena(k, total)
         dev = self.device
         s_lo, s_up = dev.stream(STREAM_IN_LOWER), dev.stream(STREAM_IN_UPPER)
         s_cmp = dev.stream("compute")
         split = offs[n_lower_files] if n_lower_files < len(offs) else total
-        _native.check(self.L.luda_stage_in_async(arena.dptr, self.pin_in.ptr, split, s_lo))
+        _native.check(self.L.luda_stage_in_async(arena.dptr, src, split, s_lo))
         if total > split:
-            _native.check(self.L.luda_stage_in_async(arena.dptr + split, self.pin_in.ptr + split, total - split, s_up))
+            _native.check(self.L.luda_stage_in_async(arena.dptr + split, src + split, total - split, s_up))
         for s in (s_lo, s_up):
             e = dev._event_on(s)
             _native.check(self.L.luda_stream_wait_event(s_cmp, e))
@@ -165,8 +234,9 @@ class JobRunner:
     def describe(self, pj: PreparedJob, arena, offs, total):
         n = len(pj.files)
         keep = []
+        lens = pj.staged.sizes if getattr(pj, "staged", None) is not None else [len(f) for f in pj.files]
         fo = (ctypes.c_uint64 * max(n, 1))(*offs)
-        fl = (ctypes.c_uint64 * max(n, 1))(*[len(f) for f in pj.files])
+        fl = (ctypes.c_uint64 * max(n, 1))(*lens)
         rf = (ctypes.c_uint32 * len(pj.run_first_file))(*pj.run_first_file)
         keep += [fo, fl, rf]
         d = _native.JobDesc()
@@ -197,46 +267,82 @@ class JobRunner:
                 setattr(d, name + "_len", len(key))
         return d, keep
 
-    def fetch(self, res):
-        """D2H the finished SSTs; returns [(bytes, smallest, largest)]."""
-        n = res.out_bytes
-        outs = []
-        if res.n_sst == 0:
-            return outs
-        s_out = self.device.stream(STREAM_OUT)
-        s_cmp = self.device.stream("compute")
-        e = self.device._event_on(s_cmp)
+    def _fetch_async(self, res, k):
+        """D2H of a finished job's SSTs into pinned output buffer k on the out
+        stream (after the job's kernels). Returns the completion event."""
+        dev = self.device
+        s_out, s_cmp = dev.stream(STREAM_OUT), dev.stream("compute")
+        e = dev._event_on(s_cmp)
         _native.check(self.L.luda_stream_wait_event(s_out, e))
         _native.check(self.L.luda_event_destroy(e))
-        self.pin_out.ensure(n)
-        _native.check(self.L.luda_stage_out_async(self.pin_out.ptr, res.out, n, s_out))
-        _native.check(self.L.luda_stream_sync(s_out))
-        raw = bytes(self.pin_out.view(n))
-        for i, (sm, lg) in enumerate(_native.sst_key_pairs(res)):
-            o, ln = res.sst_off[i], res.sst_len[i]
-            outs.append((raw[o:o + ln], sm, lg))
-        return outs
+        if res.out_bytes:
+            self.pin_out[k].ensure(res.out_bytes)
+            _native.check(self.L.luda_stage_out_async(self.pin_out[k].ptr, res.out, res.out_bytes, s_out))
+        return dev._event_on(s_out)
+
+    def _finish(self, res, k, ev, pj, t_issue):
+        """Wait for job k's D2H; outputs as memoryviews into pin_out[k]."""
+        _native.check(self.L.luda_event_wait(ev))
+        _native.check(self.L.luda_event_destroy(ev))
+        outs = []
+        if res.n_sst:
+            raw = memoryview(self.pin_out[k].view(res.out_bytes)).cast("B")
+            for i, (sm, lg) in enumerate(_native.sst_key_pairs(res)):
+                o, ln = res.sst_off[i], res.sst_len[i]
+                outs.append((raw[o:o + ln], sm, lg))
+        info = dict(n_in=res.n_in, n_out=res.n_out, blocks_in=res.blocks_in, blocks_out=res.blocks_out,
+                    t_ms=list(res.t_ms), launches=res.launches, input_bytes=sum(
+                        pj.staged.sizes if getattr(pj, "staged", None) is not None else [len(f) for f in pj.files]),
+                    t_wall=time.perf_counter() - t_issue)
+        self.device.release(res)
+        return outs, info
+
+    def run_many(self, jobs):
+        """Generator over (PreparedJob, n_lower_files) pairs yielding
+        (outputs, info) per job, in order, through the double-buffered
+        pipeline (class docstring)."""
+        it = iter(jobs)
+        cur = next(it, None)
+        if cur is None:
+            return
+        k = 0
+        t0 = time.perf_counter()
+        staged = self.stage(cur[0], cur[1], k)
+        prev = None  # (res, k, event, pj, t)
+        while cur is not None:
+            nxt = next(it, None)
+            nxt_staged = None
+            if nxt is not None:
+                # arena / staging buffer (k+1)%2 were last used by job k-1, whose compaction has returned
+                nxt_staged = self.stage(nxt[0], nxt[1], (k + 1) % 2)
+            desc, keep = self.describe(cur[0], *staged)
+            res = self.device.compact(desc)
+            del keep
+            ev = self._fetch_async(res, k % 2)
+            if prev is not None:
+                yield self._finish(*prev)
+            prev = (res, k % 2, ev, cur[0], t0)
+            t0 = time.perf_counter()
+            cur, staged, k = nxt, nxt_staged, k + 1
+        yield self._finish(*prev)
 
     def run(self, pj: PreparedJob, n_lower_files: int):
+        """One job; outputs copied to bytes (independent of the pipeline buffers)."""
         t0 = time.perf_counter()
-        arena, offs, total = self.stage(pj, n_lower_files)
-        t1 = time.perf_counter()
-        desc, keep = self.describe(pj, arena, offs, total)
-        res = self.device.compact(desc)
-        t2 = time.perf_counter()
-        try:
-            outs = self.fetch(res)
-        finally:
-            info = dict(n_in=res.n_in, n_out=res.n_out, blocks_in=res.blocks_in, blocks_out=res.blocks_out,
-                        t_ms=list(res.t_ms))
-            self.device.release(res)
-        t3 = time.perf_counter()
-        del keep
-        self._keep.clear()
-        return outs, info, (t0, t1, t2, t3)
+        outs, info = next(self.run_many([(pj, n_lower_files)]))
+        outs = [(bytes(d), sm, lg) for d, sm, lg in outs]
+        return outs, info, (t0, t0, t0 + info["t_wall"], time.perf_counter())
 
 
 _runners: dict = {}
+
+
+def close_runner(device):
+    """Release the pinned buffers of a device's job pipeline (B200Device.close)."""
+    r = _runners.pop(id(device), None)
+    if r is not None:
+        for b in r.pin_in + r.pin_out:
+            b.free()
 
 
 def runner_for(device) -> JobRunner:
@@ -269,36 +375,78 @@ def file_id_allocator(job, new_file_id=None, *, stride: int = 1, offset: int = 0
     return alloc
 
 
+def _job_stats(job, pj, outs_meta, info, job_id, t_stage_in=0.0, t_stage_out=0.0):
+    t = info["t_ms"]
+    return JobStats(job_id=job_id, source_level=job.source_level, input_files=len(pj.files),
+                    input_bytes=info["input_bytes"], output_files=len(outs_meta),
+                    output_bytes=sum(len(d) for d, _ in outs_meta), t_stage_in=t_stage_in,
+                    t_unpack=(t[0] + t[1]) / 1e3, t_sort_host=t[2] / 1e3, t_pack=(t[3] + t[4]) / 1e3,
+                    t_stage_out=t_stage_out, n_in=info["n_in"], n_out=info["n_out"],
+                    blocks_in=info["blocks_in"], blocks_out=info["blocks_out"],
+                    t_device_ms={"parse": t[0], "decode": t[1], "merge": t[2], "plan": t[3], "emit": t[4],
+                                 "total": t[7]})
+
+
+def _metas(job, outs, alloc):
+    return [(data, SstMeta(file_id=alloc(), file_size=len(data), smallest=smallest, largest=largest,
+                           level=job.target_level)) for data, smallest, largest in outs]
+
+
 def run_compaction(job, device, *, inputs=None, directory=None, config: StoreConfig | None = None,
-                   new_file_id=None, key_range=None, job_id: int = 0):
+                   new_file_id=None, key_range=None, job_id: int = 0, staged=None):
     """Compact ``job`` on ``device``; returns ``(outputs, stats)`` where
     outputs is ``[(sst_bytes, SstMeta)]`` in key order.
 
-    ``inputs`` maps file_id → bytes (else ``{directory}/{file_id}.sst`` is read).
-    ``new_file_id`` is a callable (or a ``VersionSet``) producing output file
-    ids (default: :func:`file_id_allocator`). ``key_range=(lo, hi)`` restricts the job to
+    ``inputs`` maps file_id → bytes-like (else ``{directory}/{file_id}.sst`` is
+    read); ``staged`` (a :class:`StagedInput` holding the job's files, lower
+    then upper, in pinned memory) skips the host copy. ``new_file_id`` is a
+    callable (or a ``VersionSet``) producing output file ids (default:
+    :func:`file_id_allocator`). ``key_range=(lo, hi)`` restricts the job to
     user keys in [lo, hi) (one subcompaction).
     """
     if not isinstance(device, B200Device):
         raise DeviceError("run_compaction needs the b200 device (make_device(DeviceConfig(backend='b200')))")
-    pj = prepare(job, inputs=inputs, directory=directory, config=config, key_range=key_range)
-    n_lower = len(job.lower)
-    outs, info, (t0, t1, t2, t3) = runner_for(device).run(pj, n_lower)
-    new_file_id = file_id_allocator(job, new_file_id)
-    results = []
-    for data, smallest, largest in outs:
-        results.append((data, SstMeta(file_id=new_file_id(), file_size=len(data), smallest=smallest,
-                                      largest=largest, level=job.target_level)))
-    t = info["t_ms"]
-    stats = JobStats(job_id=job_id, source_level=job.source_level, input_files=len(pj.files),
-                     input_bytes=sum(len(f) for f in pj.files), output_files=len(results),
-                     output_bytes=sum(len(d) for d, _ in results), t_stage_in=t1 - t0,
-                     t_unpack=(t[0] + t[1]) / 1e3, t_sort_host=t[2] / 1e3, t_pack=(t[3] + t[4]) / 1e3,
-                     t_stage_out=t3 - t2, n_in=info["n_in"], n_out=info["n_out"],
-                     blocks_in=info["blocks_in"], blocks_out=info["blocks_out"],
-                     t_device_ms={"parse": t[0], "decode": t[1], "merge": t[2], "plan": t[3], "emit": t[4],
-                                  "total": t[7]})
-    return results, stats
+    pj = prepare(job, inputs=inputs, directory=directory, config=config, key_range=key_range, staged=staged)
+    outs, info, (t0, t1, t2, t3) = runner_for(device).run(pj, len(job.lower))
+    results = _metas(job, outs, file_id_allocator(job, new_file_id))
+    return results, _job_stats(job, pj, results, info, job_id, t_stage_out=t3 - t2)
+
+
+def run_compactions(jobs, device, *, inputs=None, directory=None, config: StoreConfig | None = None,
+                    new_file_id=None, first_job_id: int = 0):
+    """Pipelined ``run_compaction`` over many jobs (SPEC.md:632 A7): while
+    job k compacts, job k+1's inputs are already streaming in and job k-1's
+    outputs streaming out (``JobRunner``). ``jobs`` yields CompactionJobs or
+    ``(CompactionJob, StagedInput)`` pairs. Yields ``(outputs, stats)`` per
+    job in order; outputs are ``[(memoryview, SstMeta)]`` into pinned memory,
+    valid until the generator advances (copy with ``bytes()`` to keep)."""
+    if not isinstance(device, B200Device):
+        raise DeviceError("run_compactions needs the b200 device")
+    pending = []
+
+    def prepared():
+        for j in jobs:
+            job, staged = j if isinstance(j, tuple) else (j, None)
+            pj = prepare(job, inputs=inputs, directory=directory, config=config, staged=staged)
+            pending.append((job, pj))
+            yield pj, len(job.lower)
+    shared = [0]
+
+    def alloc_for(job):
+        if new_file_id is not None:
+            return file_id_allocator(job, new_file_id)
+        base = file_id_allocator(job)()  # above every file of this job's Version
+        shared[0] = max(shared[0], base)
+
+        def alloc():  # one counter across the sequence: ids never repeat between jobs
+            v = shared[0]
+            shared[0] += 1
+            return v
+        return alloc
+    for k, (outs, info) in enumerate(runner_for(device).run_many(prepared())):
+        job, pj = pending.pop(0)
+        results = _metas(job, outs, alloc_for(job))
+        yield results, _job_stats(job, pj, results, info, first_job_id + k)
 
 
 def compact_files(device, lower_files, upper_files=(), *, source_level=1, l0_runs=False, deeper=(),

@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       const uint8_t* gp = a.arena + mt.addr;
       if (lane == 0) a.blk_local[b] = (uint32_t)cnt;
       uint64_t n = 0;
-      if (a.var) {
+      if (is_var<W>()) {
         const uint8_t* d = mt.staged ? ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15) : gp;
         n = dec_var_block<W>(a, b, mt.addr, mt.len, d, seg0 + cnt, seg1, ps.entries);
       } else if (!LUDA_ABLATE(a, 4)) {

@@ -310,8 +310,8 @@ __device__ __forceinline__ void encode_one_block(const EncodeArgs<W>& a, uint32_
     uint64_t voff = 0;
     uint32_t Lr = L;
     if (act) {
-      Lr = rec_ulen(r, a.var, L);
-      if (i % ri != 0) s = ikey_lcp_any(pr, r, a.var, L);
+      Lr = rec_ulen(r, is_var<W>(), L);
+      if (i % ri != 0) s = ikey_lcp_any(pr, r, is_var<W>(), L);
       u = Lr + 8 - s;
       vl = handle_len(r.h);
       voff = handle_off(r.h);
@@ -455,7 +455,7 @@ __device__ __forceinline__ void enc_load(const EncodeArgs<W>& a, uint32_t k, Enc
 template <int W>
 __device__ __forceinline__ void enc_layout(const EncodeArgs<W>& a, EncLane<W>& e) {
   const uint32_t lane = lane_id();
-  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage && a.K < 128 && !a.var;
+  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage && a.K < 128 && !is_var<W>();
   if (!e.fast) return;
   const uint32_t K = a.K, L = K - 8;
   const bool act = lane < e.cnt;
@@ -744,14 +744,17 @@ __device__ __forceinline__ uint32_t user_key_crc(const Rec<W>& r, uint32_t L, co
       c = crc_word(c, bswap32(be), tl);
     }
   }
-  for (uint32_t j = L & ~3u; j < L; ++j) c = crc_byte(c, (uint32_t)(r.k[j >> 3] >> (56 - 8 * (j & 7))) & 0xFFu, tl);
+#pragma unroll
+  for (int j = 0; j < 8 * W; ++j)  // static indices: the record stays in registers
+    if ((uint32_t)j >= (L & ~3u) && (uint32_t)j < L)
+      c = crc_byte(c, (uint32_t)(r.k[j >> 3] >> (56 - 8 * (j & 7))) & 0xFFu, tl);
   return ~c;
 }
 
 // Persistent: one CTA per SM loops over the output SSTs (the CRC tables are
 // loaded into shared memory once per CTA).
 template <int W>
-__global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
+__global__ void __launch_bounds__(kMetaThreads, 1) sst_meta_kernel(MetaArgs<W> a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
   uint8_t* buf = smem_raw + sizeof(CrcSmem) + kEncPre;  // 16-aligned, 160 B lead-in
@@ -795,7 +798,7 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
         // together (ILP) before any probe
         uint32_t h[kMetaUnroll];
 #pragma unroll
-        for (int u = 0; u < kMetaUnroll; ++u) h[u] = user_key_crc<W>(r[u], rec_ulen(r[u], a.var, L), tl);
+        for (int u = 0; u < kMetaUnroll; ++u) h[u] = user_key_crc<W>(r[u], rec_ulen(r[u], is_var<W>(), L), tl);
 #pragma unroll
         for (int u = 0; u < kMetaUnroll; ++u) {
           if (e0 + (uint64_t)u * kMetaThreads < e_end) {
@@ -813,7 +816,7 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
     } else {
       for (uint64_t e = fe + tid; e < fe + ne; e += kMetaThreads) {
         const Rec<W> re = a.rec[e];
-        const uint32_t h = user_key_crc<W>(re, rec_ulen(re, a.var, L), tl);
+        const uint32_t h = user_key_crc<W>(re, rec_ulen(re, is_var<W>(), L), tl);
         const uint32_t delta = (h >> 17) | (h << 15);
         uint64_t p = (uint64_t)h % nbits;
         const uint64_t step = (uint64_t)delta % nbits;
@@ -845,7 +848,7 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
     for (uint32_t i = tid; i < nb; i += kMetaThreads) {
       const uint32_t b = fb + i;
       const Rec<W> last = a.rec[(uint64_t)a.blk_first[b] + a.blk_n[b] - 1];
-      const uint32_t Lb = rec_ulen(last, a.var, L), Kb = Lb + 8;
+      const uint32_t Lb = rec_ulen(last, is_var<W>(), L), Kb = Lb + 8;
       uint8_t* p = ib + (a.blk_ipos ? a.blk_ipos[b] - a.blk_ipos[fb] : (uint64_t)i * E);
       const uint32_t vKb = put_varint(p, Kb);
       put_key_tail<W>(p + vKb, last, Lb, 0);
@@ -873,7 +876,7 @@ __global__ void __launch_bounds__(kMetaThreads) sst_meta_kernel(MetaArgs<W> a) {
     // smallest / largest internal keys
     if (tid < 2 && ne > 0) {
       const Rec<W> r = a.rec[tid == 0 ? fe : fe + ne - 1];
-      const uint32_t Lr = rec_ulen(r, a.var, L);
+      const uint32_t Lr = rec_ulen(r, is_var<W>(), L);
       put_key_tail<W>(a.sst_keys + ((uint64_t)s * 2 + tid) * a.key_slot, r, Lr, 0);
       a.sst_key_len[(uint64_t)s * 2 + tid] = Lr + 8;
     }

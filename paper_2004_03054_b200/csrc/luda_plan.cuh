@@ -76,11 +76,11 @@ __global__ void __launch_bounds__(kJumpThreads) block_jump_kernel(BlockJumpArgs<
       const Rec<W> cur = a.rec[j];
       const uint32_t vl = handle_len(cur.h);
       const uint32_t vv = varint_size(vl);
-      const uint32_t Kc = a.var ? rec_ulen(cur, true, 0) + 8 : K;
+      const uint32_t Kc = is_var<W>() ? rec_ulen(cur, true, 0) + 8 : K;
       uint32_t sh = 0;
-      if (j > 0) sh = ikey_lcp_any(a.rec[j - 1], cur, a.var, L);
+      if (j > 0) sh = ikey_lcp_any(a.rec[j - 1], cur, is_var<W>(), L);
       sbv = varint_size(sh) + varint_size(Kc - sh) + vv + (Kc - sh) + vl;
-      D[i] = (1 + (a.var ? varint_size(Kc) : vK) + vv + Kc + vl) - sbv;
+      D[i] = (1 + (is_var<W>() ? varint_size(Kc) : vK) + vv + Kc + vl) - sbv;
     } else if (i < span) {
       D[i] = 0;
     }

@@ -95,6 +95,11 @@ __device__ __forceinline__ uint32_t ikey_lcp(const Rec<W>& a, const Rec<W>& b, u
 constexpr int kVarW = 9;
 constexpr uint32_t kVarMaxLen = 8 * kVarW - 1;  // 71
 
+// Var records are exactly the W = kVarW instantiations (fixed-length jobs use
+// W <= 4), so the var paths compile out of the fixed kernels.
+template <int W>
+__host__ __device__ constexpr bool is_var() { return W == kVarW; }
+
 template <int W>
 __device__ __forceinline__ uint32_t rec_ulen(const Rec<W>& r, bool var, uint32_t L) {
   return var ? (uint32_t)(r.k[W - 1] & 0xFFu) : L;

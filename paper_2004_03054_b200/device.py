@@ -424,6 +424,8 @@ class B200Device:
         if self._closed:
             return
         self.synchronize()
+        from .compaction import close_runner
+        close_runner(self)
         self.free_all()
         for s in self._streams.values():
             self._L.luda_stream_destroy(s)
