@@ -734,7 +734,8 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     CK(cudaMemcpyAsync(hm, merr, 16, cudaMemcpyDeviceToHost, st));
     rc = sync(st);
     if (rc) return rc;
-    if (hm[0] != ~0ull) return fail(LUDA_ORDERING, "input run not strictly ascending");
+    if (hm[0] != ~0ull)
+      return fail(LUDA_ORDERING, "input run not strictly ascending (decoded record " + std::to_string(hm[0]) + ")");
     n_out = hm[1];
   }
   if (ev) CK(cudaEventRecord(ev[3], st));

@@ -619,11 +619,15 @@ __device__ uint64_t dec_var_block(const DecodeArgs<W>& a, uint32_t b, uint64_t a
               Rec<W> rec;
 #pragma unroll
               for (int w = 0; w < W; ++w) {
+                // big-endian word of kbuf[8w, 8w+8), bytes at or past the key length masked off
+                // (explicit word masks: with a per-byte `idx < lr ? kbuf[idx] : 0` select the
+                // nvcc 12.9 -O3 build left byte 8w+2 of the last word unmasked — observed on
+                // B200, tests/test_gpu_parity.py::test_var_key_prefix_extension)
                 uint64_t v = 0;
-                for (int q = 0; q < 8; ++q) {
-                  const uint32_t idx = 8u * w + q;
-                  v = (v << 8) | (idx < lr ? kbuf[idx] : 0u);
-                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v = (v << 8) | kbuf[8 * w + q];
+                const int32_t valid = (int32_t)lr - 8 * w;
+                v = valid <= 0 ? 0ull : (valid >= 8 ? v : v & (~0ull << (8 * (8 - valid))));
                 rec.k[w] = v;
               }
               rec.k[W - 1] |= lr;  // byte 71: the length (always padding: lr <= 71)
@@ -631,6 +635,12 @@ __device__ uint64_t dec_var_block(const DecodeArgs<W>& a, uint32_t b, uint64_t a
               for (int q = 7; q >= 0; --q) tr = (tr << 8) | kbuf[lr + q];
               rec.t = ~tr;
               rec.h = handle_pack(addr + pos + u, vl);
+#ifdef LUDA_VAR_PRINTF
+              printf("var b=%u n=%llu sh=%llu u=%llu lr=%u k6=%016llx k7=%016llx k8=%016llx t=%016llx\n", b,
+                     (unsigned long long)n, (unsigned long long)sh, (unsigned long long)u, lr,
+                     (unsigned long long)rec.k[6], (unsigned long long)rec.k[7], (unsigned long long)rec.k[8],
+                     (unsigned long long)rec.t);
+#endif
               a.out[base + n] = rec;
             }
           }

@@ -364,6 +364,25 @@ def test_generic_key_lengths(dev, name):
     check_case(dev, name)
 
 
+@pytest.mark.parametrize("ext", [b"\x00", b"\x01", b"\x00\x00"])
+def test_var_key_prefix_extension(dev, ext):
+    """A user key followed by its extension (shorter prefix sorts first,
+    keys.py:60-63), for every key length 0..70 that fits a var record: the
+    record padding past the key length must be zero (a leaked byte made
+    key ∥ 00 compare below key at L = 58, 66)."""
+    from paper_2004_03054_b200.compaction import compact_files
+    from paper_2004_03054_b200.config import StoreConfig
+    base = bytes(range(1, 80))
+    for L in range(0, 71):
+        keys = [base[:L], base[:L] + ext]
+        pairs = [(O.make_ikey(k, 100 + i, O.KIND_PUT), b"v" * 7) for i, k in enumerate(keys)]
+        # a third key of another length: mixed lengths force the generic-length records
+        f = O.build_table(pairs + [(O.make_ikey(b"\xff" * 3, 1, O.KIND_PUT), b"z")], sst_size_target=1 << 20)
+        want = O.reference_compact([f], sst_size_target=1 << 20)
+        got = compact_files(dev, [f], [], source_level=0, config=StoreConfig(sst_size_target=1 << 20))
+        assert [g[0] for g in got] == [w[0] for w in want], f"L={L}"
+
+
 @pytest.mark.parametrize("name", [n for n, _, _ in VARKEY_CASES[:6]])
 def test_generic_key_lengths_multitile_planner(dev, small_planner_tiles, name):
     check_case(dev, name)
