@@ -382,8 +382,8 @@ def e2e_public_api(w, steps):
              for i, ln in enumerate(w.file_len)]
     job = CompactionJob(source_level=1, lower=metas[:w.n_lower], upper=metas[w.n_lower:], target_level=2,
                         version=Version.empty())
-    # one untimed job: grows the pipeline's arenas and pinned output buffers
-    for outs, st in run_compactions([(job, staged)], dev):
+    # two untimed jobs: grow BOTH double-buffer slots (device arena + pinned output buffer of each)
+    for outs, st in run_compactions([(job, staged)] * 2, dev):
         pass
     t0 = time.perf_counter()
     out_bytes, n_out = 0, 0

@@ -63,18 +63,49 @@ constexpr int kZoneMax = 8192;
 __device__ uint32_t g_zone[kZoneMax];    // Z_n(0xFFFFFFFF): the ~0 preset advanced over n bytes
 
 // Shared-memory CRC state: the lane-replicated slicing-by-2 tables (64 KB),
-// the per-lane nibble tables (16 KB) and the Z_2176 byte tables (4 KB).
+// the per-lane nibble tables of Z_{44d} (16 KB) and the Z_1408 byte tables
+// (4 KB). (LUDA_CRC_SMEM_COMBINE=0 reads the two combine tables through the
+// read-only path from global memory instead, freeing 20 KB of shared memory:
+// measured slower — decode 4.27 → 4.55 ms on c3 — the L1 left over misses.)
+#ifndef LUDA_CRC_SMEM_COMBINE
+#define LUDA_CRC_SMEM_COMBINE 1
+#endif
 struct CrcSmem {
   uint32_t s2[256 * 64];  // row idx: [T1 lane 0..31][T0 lane 0..31]
+#if LUDA_CRC_SMEM_COMBINE
   uint32_t nib[8 * 16 * 32];
   uint32_t half[4 * 256];
+#endif
 };
 
 __device__ __forceinline__ void crc_smem_init(CrcSmem& s) {
   for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x)
     s.s2[i] = (i & 32) ? g_crc_tab[i >> 6] : g_crc_tab1[i >> 6];
+#if LUDA_CRC_SMEM_COMBINE
   for (int i = threadIdx.x; i < 8 * 16 * 32; i += blockDim.x) s.nib[i] = g_seg_nib[i];
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) s.half[i] = g_half_tab[i];
+#endif
+}
+__device__ __forceinline__ const uint32_t* crc_nib_tab(const CrcSmem& s) {
+#if LUDA_CRC_SMEM_COMBINE
+  return s.nib;
+#else
+  return g_seg_nib;
+#endif
+}
+__device__ __forceinline__ const uint32_t* crc_half_tab(const CrcSmem& s) {
+#if LUDA_CRC_SMEM_COMBINE
+  return s.half;
+#else
+  return g_half_tab;
+#endif
+}
+__device__ __forceinline__ uint32_t crc_tab_ld(const uint32_t* p) {
+#if LUDA_CRC_SMEM_COMBINE
+  return *p;
+#else
+  return __ldg(p);
+#endif
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -119,13 +150,14 @@ __device__ __forceinline__ uint32_t crc_byte(uint32_t c, uint32_t b, const CrcLa
 __device__ __forceinline__ uint32_t seg_shift(uint32_t c, const uint32_t* __restrict__ nl) {
   uint32_t r = 0;
 #pragma unroll
-  for (int n = 0; n < 8; ++n) r ^= nl[((n << 4) | ((c >> (4 * n)) & 0xFu)) << 5];
+  for (int n = 0; n < 8; ++n) r ^= crc_tab_ld(nl + (((n << 4) | ((c >> (4 * n)) & 0xFu)) << 5));
   return r;
 }
 
 // Z_1408(c) (byte tables).
 __device__ __forceinline__ uint32_t half_shift(uint32_t c, const uint32_t* __restrict__ ht) {
-  return ht[c & 0xFFu] ^ ht[256 + ((c >> 8) & 0xFFu)] ^ ht[512 + ((c >> 16) & 0xFFu)] ^ ht[768 + (c >> 24)];
+  return crc_tab_ld(ht + (c & 0xFFu)) ^ crc_tab_ld(ht + 256 + ((c >> 8) & 0xFFu)) ^
+         crc_tab_ld(ht + 512 + ((c >> 16) & 0xFFu)) ^ crc_tab_ld(ht + 768 + (c >> 24));
 }
 
 // Apply a 32x32 GF(2) operator given by its columns (constant memory; the
@@ -175,8 +207,8 @@ __device__ __forceinline__ SegPtr seg_ptr(const uint8_t* p) {
 __device__ __forceinline__ uint32_t lane_combine(const uint32_t (&r)[kChains], const CrcSmem& cs, uint32_t lane) {
   uint32_t v = r[kChains - 1];
 #pragma unroll
-  for (int c = kChains - 2; c >= 0; --c) v = half_shift(v, cs.half) ^ r[c];
-  return seg_shift(v, cs.nib + lane);
+  for (int c = kChains - 2; c >= 0; --c) v = half_shift(v, crc_half_tab(cs)) ^ r[c];
+  return seg_shift(v, crc_nib_tab(cs) + lane);
 }
 
 // Warp: un-combined pass value of pass q over prepared smem data of length n:

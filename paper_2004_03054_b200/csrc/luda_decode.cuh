@@ -54,7 +54,10 @@ enum BlockCode : uint32_t {
 // Paired warps: a PARSE warp (producer + walk + records) and a CRC warp share
 // a pair of staging slots; both consume every block of the pair's contiguous
 // block range concurrently (the CRC never modifies bytes the parse warp reads).
-constexpr int kDecPairs = 14;
+#ifndef LUDA_DEC_PAIRS
+#define LUDA_DEC_PAIRS 14
+#endif
+constexpr int kDecPairs = LUDA_DEC_PAIRS;
 constexpr int kDecWarps = 2 * kDecPairs;
 constexpr int kDecNSlot = 2;                     // staging slots per pair (1 block in flight)
 constexpr int kDecLead = 48;                     // zero lead before the TMA window (never written by TMA)

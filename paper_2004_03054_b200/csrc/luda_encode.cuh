@@ -25,10 +25,25 @@
 
 namespace luda {
 
-// Pairs: a BUILDER warp (records, layout, value TMA, assembly) and a CRC warp
-// (CRC + copy-out) hand assembled blocks over through two buffers.
-constexpr int kEncPairs = 10;
-constexpr int kEncWarps = 2 * kEncPairs;
+// Default (LUDA_ENC_FUSED=1): 15 warps per SM, each builds AND finishes its
+// own blocks (records, layout, value TMA, assembly, then CRC + bulk store)
+// with one assembly buffer — the next block's value gather is in flight while
+// the current one is CRC'd. LUDA_ENC_FUSED=0: pairs of a BUILDER warp and a
+// CRC warp (CRC + copy-out) hand blocks over through two buffers. Measured on
+// c3: pairs x10 3.17 ms, fused x12 3.17, x14 3.05, x15 2.89 ms (shared
+// memory bounds the warp count: 84 KB CRC tables + 9.5 KB per warp).
+#ifndef LUDA_ENC_FUSED
+#define LUDA_ENC_FUSED 1
+#endif
+#ifndef LUDA_ENC_PAIRS
+#define LUDA_ENC_PAIRS (LUDA_ENC_FUSED ? 15 : 10)
+#endif
+// LUDA_ENC_FUSED: every warp builds AND finishes (CRC + bulk store) its own
+// blocks — one assembly buffer per warp instead of a builder/CRC pair with two.
+constexpr bool kEncFused = LUDA_ENC_FUSED != 0;
+constexpr int kEncPairs = LUDA_ENC_PAIRS;  // fused: warps
+constexpr int kEncWarps = kEncFused ? kEncPairs : 2 * kEncPairs;
+constexpr int kEncBufs = kEncFused ? 1 : 2;
 constexpr int kEncStage = 4608;                        // blocks up to this size are assembled in smem
 constexpr int kEncPre = 160;
 constexpr int kEncBuf = kEncPre + 16 + kEncStage + 64;
@@ -40,7 +55,7 @@ struct EncMeta {
   uint32_t skip;  // the builder finished the block itself (generic path)
 };
 struct alignas(16) EncPairSmem {
-  uint8_t buf[2][kEncBuf];
+  uint8_t buf[kEncBufs][kEncBuf];
   uint8_t stg[kEncStg];
   uint64_t bar;                 // value TMA
   uint64_t full[2], empty[2];
@@ -600,7 +615,7 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
   CrcSmem& cs = *reinterpret_cast<CrcSmem*>(smem_raw);
   EncPairSmem* pairs = reinterpret_cast<EncPairSmem*>(smem_raw + sizeof(CrcSmem));
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const bool builder = warp < kEncPairs;
+  const bool builder = kEncFused || warp < kEncPairs;
   const uint32_t p = warp % kEncPairs;
   EncPairSmem& ps = pairs[p];
   EncCtaSmem& cta = *reinterpret_cast<EncCtaSmem*>(smem_raw + sizeof(CrcSmem) + kEncPairs * sizeof(EncPairSmem));
@@ -626,10 +641,15 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
     enc_layout(a, cur);
     if (cur.fast) enc_issue(a, cur, ps.stg, &ps.bar);
     for (uint32_t i = 0; cur.valid; ++i) {
-      const uint32_t b = i & 1u;
+      const uint32_t b = kEncFused ? 0u : (i & 1u);
       uint8_t* wbuf = ps.buf[b];
       ENC_T0();
-      if (i >= 2) mbar_wait(&ps.empty[b], ((i - 2) >> 1) & 1u);  // the CRC warp is done with block i-2
+      if (kEncFused) {
+        if (lane == 0) bulk_wait_read0();  // the previous block's bulk store has read the buffer
+        __syncwarp();
+      } else if (i >= 2) {
+        mbar_wait(&ps.empty[b], ((i - 2) >> 1) & 1u);  // the CRC warp is done with block i-2
+      }
       ENC_T(0);
       enc_load(a, cur.k + nw, nxt);  // records of the next block: loads in flight
       ENC_T(1);
@@ -658,13 +678,18 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
         enc_layout(a, nxt);
         if (nxt.fast) enc_issue(a, nxt, ps.stg, &ps.bar);
       }
-      if (lane == 0) ps.meta[b] = mt;
-      fence_proxy_async_smem();  // the assembled bytes are read by the CRC warp's bulk store
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ps.full[b]);  // release: the assembled block and its meta
+      if (kEncFused) {
+        if (!mt.skip) enc_finish(a, cur, wbuf, cs);  // CRC + bulk store; the buffer is waited for above
+      } else {
+        if (lane == 0) ps.meta[b] = mt;
+        fence_proxy_async_smem();  // the assembled bytes are read by the CRC warp's bulk store
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ps.full[b]);  // release: the assembled block and its meta
+      }
       cur = nxt;
       ENC_T(7);
     }
+    if (kEncFused && lane == 0) bulk_wait0();
   } else {
     // CRC warp: CRC + copy-out of the blocks the builder assembled, in order
     for (uint32_t i = 0, k = gw; k < a.nblk; ++i, k += nw) {

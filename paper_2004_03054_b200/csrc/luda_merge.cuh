@@ -21,8 +21,14 @@
 
 namespace luda {
 
-constexpr int kMergeThreads = 256;
-constexpr int kMergeItems = 6;
+#ifndef LUDA_MERGE_THREADS
+#define LUDA_MERGE_THREADS 256
+#endif
+#ifndef LUDA_MERGE_ITEMS
+#define LUDA_MERGE_ITEMS 6
+#endif
+constexpr int kMergeThreads = LUDA_MERGE_THREADS;
+constexpr int kMergeItems = LUDA_MERGE_ITEMS;
 constexpr int kMergeTile = kMergeThreads * kMergeItems;
 
 struct KeyBound {

@@ -7,7 +7,7 @@ set -u
 TAG=${1:-r1}
 RE=${2:-"decode_kernel|encode_kernel|merge_kernel|sst_meta_kernel|block_scan_kernel|block_jump_kernel"}
 mkdir -p gpurun_out
-BENCH="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu"
+BENCH="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu --extras ''"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file gpurun_out/launches_${TAG}.csv $BENCH > gpurun_out/launches_${TAG}.log 2>&1
 # the synthesis step builds the inputs with encode/sst_meta too: skip those launches (-s counts filtered launches)
