@@ -1,7 +1,7 @@
 """LUDA compaction benchmark on B200 (BASELINE.json metric: compaction input
 MB/s and keys/s per B200 at 1/2/4/8 GPUs; % of HBM roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--extras c2,c4,c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--extras c2,c4,reads,c5]
 
 N = 1 (headline): a step = one full compaction job of BASELINE config 3
 (luda_compact: parse → decode → merge/resolve → plan → encode →
@@ -499,6 +499,96 @@ def measure_c4(L, stream, steps=5, warmup=2, n=1 << 22, peak=6539.5):
                           "sst_meta": round(kms[4], 3)}}
 
 
+def measure_reads(L, desc, st, n_lookups=1 << 22, steps=10, warmup=3):
+    """Batched point lookups over the c3 job's output SSTs,
+    opened in place in HBM (987 x 4 MiB SSTs, 26.8M entries): half the keys
+    present (index keys of the outputs), half absent random 16 B keys, probed
+    in store order over the one output level (range binary search → bloom →
+    index → block). Device: the lookup kernel alone over device-resident keys
+    (CUDA events). e2e: luda_tables_get with host keys (H2D keys, lookups,
+    packing, D2H of the found keys and values)."""
+    import random
+    import struct as _st
+
+    import torch
+    from paper_2004_03054_b200 import _native
+    res = compact_once(L, desc, st)
+    try:
+        n_sst = res.n_sst
+        offs = [res.sst_off[i] for i in range(n_sst)]
+        lens = [res.sst_len[i] for i in range(n_sst)]
+        # present keys: the outputs' index keys (last key of every block), read back from the device
+        foot = (ctypes.c_uint8 * 24)()
+        present = []
+        for i in range(n_sst):
+            _native.check(L.luda_stage_out_async(foot, res.out + offs[i] + lens[i] - 24, 24, st))
+            _native.check(L.luda_stream_sync(st))
+            _, _, ioff, ilen, _ = _st.unpack("<IIIIQ", bytes(foot))
+            ib = (ctypes.c_uint8 * ilen)()
+            _native.check(L.luda_stage_out_async(ib, res.out + offs[i] + ioff, ilen, st))
+            _native.check(L.luda_stream_sync(st))
+            b = bytes(ib)
+            p = 0
+            while p < ilen - 8:
+                kl = b[p]
+                present.append(b[p + 1:p + 1 + kl - 8])
+                p += 1 + kl + 8
+        rng = random.Random(0x7EAD)
+        keys = [rng.choice(present) if i % 2 == 0 else rng.randbytes(16) for i in range(n_lookups)]
+        blob = b"".join(keys)
+        h = ctypes.c_void_p()
+        off_arr = (ctypes.c_uint64 * n_sst)(*offs)
+        len_arr = (ctypes.c_uint64 * n_sst)(*lens)
+        t0 = time.perf_counter()
+        _native.check(L.luda_tables_open(res.out, off_arr, len_arr, n_sst, ctypes.byref(h), st))
+        open_ms = (time.perf_counter() - t0) * 1e3
+        sk = _native.sst_key_pairs(res)
+        rk = b"".join(a[:-8] + b[:-8] for a, b in sk)
+        rl = [x for a, b in sk for x in (len(a) - 8, len(b) - 8)]
+        plan = _native.ProbePlan(0, None, 1, (ctypes.c_uint32 * 2)(0, n_sst),
+                                 (ctypes.c_uint32 * n_sst)(*range(n_sst)),
+                                 (ctypes.c_uint8 * len(rk)).from_buffer_copy(rk), (ctypes.c_uint32 * len(rl))(*rl))
+        _native.check(L.luda_tables_set_plan(h.value, ctypes.byref(plan), st))
+        dk = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda()
+        dko = (torch.arange(n_lookups, dtype=torch.int64) * 16).cuda()
+        dkl = torch.full((n_lookups,), 16, dtype=torch.int32).cuda()
+        torch.cuda.synchronize()
+        for _ in range(warmup):
+            _native.check(L.luda_tables_lookup_dev(h.value, dk.data_ptr(), dko.data_ptr(), dkl.data_ptr(),
+                                                   n_lookups, None, 256, st))
+        tm = Timer(L)
+        tm.start(st)
+        for _ in range(steps):
+            _native.check(L.luda_tables_lookup_dev(h.value, dk.data_ptr(), dko.data_ptr(), dkl.data_ptr(),
+                                                   n_lookups, None, 256, st))
+        ms = tm.stop(st) / steps
+        # e2e through the C ABI with host keys
+        kb = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        ko = (ctypes.c_uint64 * n_lookups)(*range(0, 16 * n_lookups, 16))
+        kl = (ctypes.c_uint32 * n_lookups)(*([16] * n_lookups))
+        r = _native.GetResult()
+        _native.check(L.luda_tables_get(h.value, kb, len(blob), ko, kl, n_lookups, None, 256, ctypes.byref(r), st))
+        e2e = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            _native.check(L.luda_tables_get(h.value, kb, len(blob), ko, kl, n_lookups, None, 256, ctypes.byref(r),
+                                            st))
+            e2e.append(time.perf_counter() - t0)
+        found = sum(1 for i in range(n_lookups) if r.status[i] == 1)
+        e2e_s = min(e2e)
+        out = {"workload": "Batched point lookups (Table.get in store order) over the c3 job's %d output SSTs "
+                           "resident in HBM: %d keys, 50%% present / 50%% absent" % (n_sst, n_lookups),
+               "lookups": n_lookups, "found": found, "ms": round(ms, 3),
+               "value": round(n_lookups / (ms * 1e-3), 1), "unit": "lookups/s", "open_ms": round(open_ms, 2),
+               "e2e": {"value": round(n_lookups / e2e_s, 1), "unit": "lookups/s", "ms": round(e2e_s * 1e3, 2),
+                       "h2d_bytes": len(blob) + 12 * n_lookups, "d2h_bytes": int(r.packed_bytes) + 32 * n_lookups,
+                       "t_ms": [round(x, 3) for x in r.t_ms]}}
+        L.luda_tables_close(h.value)
+        return out
+    finally:
+        L.luda_job_release(ctypes.byref(res))
+
+
 def measure_c5(world, rank, local, steps, warmup, group=None, total_gb=256.0):
     import bench_c5
     spec = bench_c5.C5Spec(total_gb=total_gb)
@@ -564,7 +654,7 @@ def parse_args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--keys", type=int, default=1 << 25, help="c3: distinct keys per run (2^25 → 64M entries)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--extras", default="c2,c4,c5", help="other BASELINE configs measured at N=1 ('' = none)")
+    ap.add_argument("--extras", default="c2,c4,reads,c5", help="other BASELINE configs measured at N=1 ('' = none)")
     ap.add_argument("--c5-gb", type=float, default=256.0, help="c5: global job size (GB of input)")
     ap.add_argument("--cpu-keys", type=int, default=1 << 17,
                     help="reference arm: distinct keys per run of each worker's sample job")
@@ -805,6 +895,8 @@ def main_c3(args, local):
         workloads["c2"] = measure_c2(L, st)
     if "c4" in extras:
         workloads["c4_scaled"] = measure_c4(L, st, peak=hbm)
+    if "reads" in extras:
+        workloads["reads"] = measure_reads(L, desc, st)
     if "c5" in extras:
         spec, tot = measure_c5(1, 0, local, max(1, args.steps // 5), 1, total_gb=args.c5_gb)
         workloads["c5_1gpu"] = {

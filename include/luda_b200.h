@@ -166,6 +166,60 @@ int luda_build_files_from_sorted(const uint8_t* dev_user_keys, uint32_t user_key
                                  uint32_t bits_per_key, uint64_t sst_size_target,
                                  uint64_t entries_per_file, luda_job_result* result, void* stream);
 
+/* ---- batched read path ------------------------------- */
+/* A set of SSTs resident in device memory (host-staged files, or a job's
+ * output buffer, zero-copy). Replaces, per file, Table.__init__
+ * (sst.py:284-310: footer, magic, filter and index checks — the first failing
+ * file's error is returned) and verifies every data block's CRC once
+ * (Table._raw_block, sst.py:322-340); a block's outcome is raised only by a
+ * lookup that reads it, as in the reference. */
+typedef struct luda_tables luda_tables;
+int luda_tables_open(const uint8_t* dev_arena, const uint64_t* file_off, const uint64_t* file_len,
+                     uint32_t n_files, luda_tables** out, void* stream);
+int luda_tables_close(luda_tables* t);
+int luda_tables_info(luda_tables* t, uint32_t* n_tables, uint32_t* n_blocks);
+/* Table.filter_rejects / Table.data_block_reads (sst.py:296-297), host[n_files] each. */
+int luda_tables_counters(luda_tables* t, uint64_t* filter_rejects, uint64_t* block_reads);
+/* The store's probe order for a get: the L0 tables newest
+ * first, then per level >= 1 the one file whose [smallest, largest] user-key
+ * range holds the key (binary search over ascending ranges); the first table
+ * whose Table.get returns an entry answers. */
+typedef struct {
+  uint32_t n_l0;
+  const uint32_t* l0;            /* host[n_l0]: table ids, newest first           */
+  uint32_t n_levels;
+  const uint32_t* level_first;   /* host[n_levels+1]: into level_tables           */
+  const uint32_t* level_tables;  /* host: table ids, ascending ranges per level   */
+  const uint8_t* range_keys;     /* host: smallest ∥ largest user key per entry   */
+  const uint32_t* range_lens;    /* host[2 * entries]                             */
+} luda_probe_plan;
+int luda_tables_set_plan(luda_tables* t, const luda_probe_plan* plan, void* stream);
+typedef struct {
+  uint32_t n;
+  const uint32_t* status;     /* host[n]: 0 = None, 1 = (key, value), >1 = error  */
+  const uint32_t* table;      /* host[n]: table that answered                     */
+  const uint32_t* key_len;    /* host[n]: internal key length of a found entry     */
+  const uint32_t* value_len;  /* host[n]                                           */
+  const uint64_t* pos;        /* host[n+1]: found entry i = packed[pos[i] ..]: key ∥ value */
+  const uint8_t* packed;      /* host                                              */
+  uint64_t packed_bytes;
+  const int64_t* err_off;     /* host[n]: block offset of a CorruptionError, else -1 */
+  int64_t fail_index;         /* first failing lookup (its error is the return value) or -1 */
+  double t_ms[4];             /* H2D, lookup + scan, pack, D2H                     */
+} luda_get_result;
+/* Table.get (sst.py:342-368) for n keys (key i = keys[key_off[i] .. + key_len[i]],
+ * host memory): on table table_of_key[i], or in the plan's store order when
+ * table_of_key is NULL. Found keys longer than key_cap fail (LUDA_UNSUPPORTED).
+ * Result arrays are owned by the table set and valid until its next get.
+ * Synchronous on `stream`. */
+int luda_tables_get(luda_tables* t, const uint8_t* keys, uint64_t keys_bytes, const uint64_t* key_off,
+                    const uint32_t* key_len, uint32_t n, const uint32_t* table_of_key, uint32_t key_cap,
+                    luda_get_result* result, void* stream);
+/* The lookup kernel alone over device-resident keys (throughput measurement);
+ * results stay on the device. Asynchronous on `stream`. */
+int luda_tables_lookup_dev(luda_tables* t, const uint8_t* dev_keys, const uint64_t* dev_key_off,
+                           const uint32_t* dev_key_len, uint32_t n, const uint32_t* dev_table_of_key,
+                           uint32_t key_cap, void* stream);
 #ifdef __cplusplus
 }
 #endif

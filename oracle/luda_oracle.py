@@ -425,6 +425,131 @@ def scan_table(data, index):
 
 
 # --------------------------------------------------------------------------
+# Read path: Table.get over an in-memory file
+# --------------------------------------------------------------------------
+
+SEEK_TRAILER = (((1 << 56) - 1) << 8) | KIND_PUT  # seek_key (keys.py:66-68)
+
+
+def _sort_key(ikey):
+    """keys.py:60-63 (struct.error on keys shorter than the trailer, as there)."""
+    trailer = U64.unpack_from(ikey, len(ikey) - TRAILER)[0]
+    return (ikey[:-TRAILER], -trailer)
+
+
+class BlockReader:
+    """DataBlockReader (blocks.py:168-226) over a checksum-verified raw block."""
+
+    def __init__(self, data: bytes):
+        self.data = data
+        payload_len = len(data) - 4
+        n_restarts = U32.unpack_from(data, payload_len - 4)[0]
+        self.entries_end = payload_len - 4 - 4 * n_restarts
+        if n_restarts < 1 or self.entries_end < 0:
+            raise FormatError("bad restart array")
+        self.restarts = [U32.unpack_from(data, self.entries_end + 4 * i)[0] for i in range(n_restarts)]
+
+    def entry_at(self, pos: int, prev_key: bytes):
+        """blocks.py:188-196: prefix slices and value slices clamp silently."""
+        d = self.data
+        shared, pos = varint_read(d, pos)
+        unshared, pos = varint_read(d, pos)
+        vlen, pos = varint_read(d, pos)
+        key = prev_key[:shared] + d[pos:pos + unshared]
+        pos += unshared
+        return key, d[pos:pos + vlen], pos + vlen
+
+    def seek(self, target):
+        """blocks.py:202-218: rightmost restart <= target, then one interval."""
+        lo, hi = 0, len(self.restarts) - 1
+        while lo < hi:
+            mid = (lo + hi + 1) // 2
+            if _sort_key(self.entry_at(self.restarts[mid], b"")[0]) <= target:
+                lo = mid
+            else:
+                hi = mid - 1
+        pos = self.restarts[lo]
+        prev = b""
+        while pos < self.entries_end:
+            key, value, pos = self.entry_at(pos, prev)
+            if _sort_key(key) >= target:
+                return key, value
+            prev = key
+        return None
+
+
+class MemTable:
+    """Table (sst.py:284-368) over SST bytes held in memory, no block cache:
+    the same checks at open, the same counters, the same get."""
+
+    def __init__(self, data):
+        self.data = bytes(data)
+        (bits, self.k), self.index = open_table(self.data)
+        self.bits = bits
+        self.index_sort_keys = [_sort_key(k) for k, _, _ in self.index]  # sst.py:309
+        self.filter_rejects = 0
+        self.data_block_reads = 0
+
+    def raw_block(self, offset: int, length: int) -> bytes:
+        """sst.py:322-340 without a cache."""
+        data = _pread(self.data, length, offset)
+        if len(data) != length:
+            raise FormatError("short block read")
+        self.data_block_reads += 1
+        stored = U32.unpack_from(data, length - 4)[0]
+        if crc32(data[:-4]) != stored:
+            raise CorruptionError("data block checksum mismatch", offset=offset)
+        return data
+
+    def get(self, user_key: bytes):
+        """sst.py:342-368."""
+        if not bloom_may_contain(self.bits, self.k, user_key):
+            self.filter_rejects += 1
+            return None
+        target = (user_key, -SEEK_TRAILER)
+        lo, hi = 0, len(self.index)
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if self.index_sort_keys[mid] < target:
+                lo = mid + 1
+            else:
+                hi = mid
+        if lo == len(self.index):
+            return None
+        _, off, ln = self.index[lo]
+        found = BlockReader(self.raw_block(off, ln)).seek(target)
+        if found is None or found[0][:-TRAILER] != user_key:
+            return None
+        return found
+
+
+def store_get(tables, l0, levels, user_key: bytes):
+    """SPEC.md:185-189 over SSTs only: ``l0`` table ids newest first, then
+    ``levels`` = [[(table id, smallest user key, largest user key)] ascending]
+    — the one file whose range holds the key; the first table whose get
+    returns an entry answers (its kind decides Put vs not-found upstream)."""
+    for t in l0:
+        r = tables[t].get(user_key)
+        if r is not None:
+            return t, r
+    for files in levels:
+        lo, hi = 0, len(files)
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if files[mid][2] < user_key:
+                lo = mid + 1
+            else:
+                hi = mid
+        if lo == len(files) or files[lo][1] > user_key:
+            continue
+        t = files[lo][0]
+        r = tables[t].get(user_key)
+        if r is not None:
+            return t, r
+    return None
+
+
+# --------------------------------------------------------------------------
 # Kernel work items (kernels.py) — used for dispatch-level parity tests
 # --------------------------------------------------------------------------
 

@@ -67,6 +67,34 @@ class JobResult(ctypes.Structure):
     ]
 
 
+class ProbePlan(ctypes.Structure):
+    _fields_ = [
+        ("n_l0", ctypes.c_uint32),
+        ("l0", c_u32p),
+        ("n_levels", ctypes.c_uint32),
+        ("level_first", c_u32p),
+        ("level_tables", c_u32p),
+        ("range_keys", c_u8p),
+        ("range_lens", c_u32p),
+    ]
+
+
+class GetResult(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_uint32),
+        ("status", c_u32p),
+        ("table", c_u32p),
+        ("key_len", c_u32p),
+        ("value_len", c_u32p),
+        ("pos", c_u64p),
+        ("packed", c_u8p),
+        ("packed_bytes", ctypes.c_uint64),
+        ("err_off", c_i64p),
+        ("fail_index", ctypes.c_int64),
+        ("t_ms", ctypes.c_double * 4),
+    ]
+
+
 _SIGS = {
     "luda_init": (ctypes.c_int, [ctypes.c_int]),
     "luda_shutdown": (ctypes.c_int, []),
@@ -107,6 +135,17 @@ _SIGS = {
                                                     ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
                                                     ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
                                                     ctypes.POINTER(JobResult), ctypes.c_void_p]),
+    # batched read path (luda_read.cuh)
+    "luda_tables_open": (ctypes.c_int, [ctypes.c_void_p, c_u64p, c_u64p, ctypes.c_uint32,
+                                        ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]),
+    "luda_tables_close": (ctypes.c_int, [ctypes.c_void_p]),
+    "luda_tables_info": (ctypes.c_int, [ctypes.c_void_p, c_u32p, c_u32p]),
+    "luda_tables_counters": (ctypes.c_int, [ctypes.c_void_p, c_u64p, c_u64p]),
+    "luda_tables_set_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ProbePlan), ctypes.c_void_p]),
+    "luda_tables_get": (ctypes.c_int, [ctypes.c_void_p, c_u8p, ctypes.c_uint64, c_u64p, c_u32p, ctypes.c_uint32,
+                                       c_u32p, ctypes.c_uint32, ctypes.POINTER(GetResult), ctypes.c_void_p]),
+    "luda_tables_lookup_dev": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                              ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -33,6 +33,7 @@
 #include "luda_merge.cuh"
 #include "luda_parse.cuh"
 #include "luda_plan.cuh"
+#include "luda_read.cuh"
 #include "luda_rec.cuh"
 #include "luda_tables.cuh"
 
@@ -186,6 +187,27 @@ const char* file_msg(uint32_t code) {
     case F_IDX_TRAILING: return "trailing garbage in index block";
     default: return "format error";
   }
+}
+
+// Table.__init__ (sst.py:284-310) outcome of one parsed file, in the
+// reference's check order: footer/magic/filter length, filter CRC, probe
+// count, index length, index CRC, index entries. crc/stored: filter, index.
+int check_parsed_file(const FileInfo& fi, const uint32_t* crc, const uint32_t* stored) {
+  char buf[96];
+  if (fi.code == F_MAGIC) {
+    snprintf(buf, sizeof buf, "bad magic 0x%016llx", (unsigned long long)fi.magic);
+    return fail(LUDA_FORMAT, buf);
+  }
+  if (fi.code) return fail(LUDA_FORMAT, file_msg(fi.code));
+  if (crc[0] != stored[0]) return fail(LUDA_CORRUPT, "filter block checksum mismatch", (int64_t)fi.filter_off);
+  if (fi.kbad) {
+    snprintf(buf, sizeof buf, "bad probe count %u", fi.kbyte);
+    return fail(LUDA_FORMAT, buf);
+  }
+  if (fi.icode == F_INDEX_SHORT) return fail(LUDA_FORMAT, file_msg(fi.icode));
+  if (crc[1] != stored[1]) return fail(LUDA_CORRUPT, "index block checksum mismatch", (int64_t)fi.index_off);
+  if (fi.icode) return fail(LUDA_FORMAT, file_msg(fi.icode));
+  return LUDA_OK;
 }
 
 const char* block_msg(uint32_t code) {
@@ -1130,20 +1152,8 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   std::vector<uint32_t> fbb(nf + 1, 0);
   for (uint32_t f = 0; f < nf; ++f) {
     const FileInfo& fi = hinfo[f];
-    char buf[96];
-    if (fi.code == F_MAGIC) {
-      snprintf(buf, sizeof buf, "bad magic 0x%016llx", (unsigned long long)fi.magic);
-      return fail(LUDA_FORMAT, buf);
-    }
-    if (fi.code) return fail(LUDA_FORMAT, file_msg(fi.code));
-    if (hcrc[2 * f] != hst[2 * f]) return fail(LUDA_CORRUPT, "filter block checksum mismatch", (int64_t)fi.filter_off);
-    if (fi.kbad) {
-      snprintf(buf, sizeof buf, "bad probe count %u", fi.kbyte);
-      return fail(LUDA_FORMAT, buf);
-    }
-    if (fi.icode == F_INDEX_SHORT) return fail(LUDA_FORMAT, file_msg(fi.icode));
-    if (hcrc[2 * f + 1] != hst[2 * f + 1]) return fail(LUDA_CORRUPT, "index block checksum mismatch", (int64_t)fi.index_off);
-    if (fi.icode) return fail(LUDA_FORMAT, file_msg(fi.icode));
+    rc = check_parsed_file(fi, hcrc.data() + 2 * f, hst.data() + 2 * f);
+    if (rc) return rc;
     fbb[f + 1] = fbb[f] + fi.nblocks;
     if (fi.nblocks) {
       if (fi.klen == 0xFFFFFFFFu) mixed = true;
@@ -1218,3 +1228,5 @@ int luda_dbg_enc_timing(unsigned long long* out, int reset) {
 }
 #endif
 }  // extern "C"
+
+#include "luda_read_abi.inc"

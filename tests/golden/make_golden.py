@@ -213,7 +213,49 @@ def make_item_goldens():
     return res
 
 
+def make_read_goldens():
+    """Read-path goldens: the reference SstBuilder's files opened with the
+    reference Table (files in a temp dir, no block cache) and probed with
+    Table.get (sst.py:342-368) — per table, or in SPEC store order."""
+    import tempfile
+    from tests.golden import read_cases as RC
+    out = {}
+    for name in RC.READ_CASES:
+        c = RC.build(name, builder=lambda pairs, sst_size_target, **cfg: ref_build_split(pairs, sst_size_target, **cfg))
+        with tempfile.TemporaryDirectory() as d:
+            tables = []
+            for i, f in enumerate(c["files"]):
+                p = os.path.join(d, f"{i}.sst")
+                with open(p, "wb") as fh:
+                    fh.write(f)
+                tables.append(R_sst.open_sst(p))
+            enc = []
+            for t, q in c["queries"]:
+                if c["mode"] == "table":
+                    o = RC.outcome(lambda: tables[t].get(q))
+                else:
+                    o = RC.outcome(lambda: O_store_get(tables, c["l0"], c["levels"], q))
+                enc.append(RC.encode(c["mode"], o))
+            counters = [[tb.filter_rejects, tb.data_block_reads] for tb in tables]
+            for tb in tables:
+                tb.close()
+        out[name] = {"files": [sha(f) for f in c["files"]], "results": RC.summary(enc), "counters": counters}
+        print(f"{name}: {len(c['files'])} files, {RC.summary(enc)}", flush=True)
+    return out
+
+
+def O_store_get(tables, l0, levels, q):
+    from oracle import luda_oracle as O
+    return O.store_get(tables, l0, levels, q)  # SPEC-order composition over the REFERENCE Table objects
+
+
 def main():
+    if sys.argv[1:] == ["reads"]:
+        with open(os.path.join(HERE, "reads.json"), "w") as f:
+            json.dump(make_read_goldens(), f, indent=1, sort_keys=True)
+        return
+    with open(os.path.join(HERE, "reads.json"), "w") as f:
+        json.dump(make_read_goldens(), f, indent=1, sort_keys=True)
     gold = make_compaction_goldens()
     with open(os.path.join(HERE, "compaction.json"), "w") as f:
         json.dump(gold, f, indent=1, sort_keys=True)
