@@ -220,6 +220,21 @@ int luda_tables_get(luda_tables* t, const uint8_t* keys, uint64_t keys_bytes, co
 int luda_tables_lookup_dev(luda_tables* t, const uint8_t* dev_keys, const uint64_t* dev_key_off,
                            const uint32_t* dev_key_len, uint32_t n, const uint32_t* dev_table_of_key,
                            uint32_t key_cap, void* stream);
+/* ---- storage <-> HBM ---------------- */
+/* Read n files (file i's first len[i] bytes) into dev_dst + dst_off[i], or
+ * write dev_src + src_off[i] .. + len[i] to file i (created / truncated),
+ * without a caller-visible host copy: GPUDirect Storage through cuFile
+ * (dlopen'ed; its compatibility mode where nvidia-fs is absent), else a
+ * native multi-threaded pread/pwrite ↔ pinned double-buffer ↔ cudaMemcpyAsync
+ * pipeline. mode: 0 auto, 1 cuFile only, 2 bounce only; *used_mode = 1
+ * (cuFile) or 2 (bounce). Synchronous. Replaces the host file reads / writes
+ * around run_compaction (Table file I/O, sst.py:284-340; build_sst writes). */
+int luda_files_read(const char* const* paths, uint32_t n, void* dev_dst, const uint64_t* dst_off,
+                    const uint64_t* len, int mode, int* used_mode);
+int luda_files_write(const char* const* paths, uint32_t n, const void* dev_src, const uint64_t* src_off,
+                     const uint64_t* len, int mode, int* used_mode);
+/* 1 when the cuFile driver opened (message in why), else 0. */
+int luda_gds_status(char* why, uint32_t cap);
 #ifdef __cplusplus
 }
 #endif

@@ -146,6 +146,12 @@ _SIGS = {
                                        c_u32p, ctypes.c_uint32, ctypes.POINTER(GetResult), ctypes.c_void_p]),
     "luda_tables_lookup_dev": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                               ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]),
+    # storage <-> HBM (luda_io_abi.inc)
+    "luda_files_read": (ctypes.c_int, [ctypes.POINTER(ctypes.c_char_p), ctypes.c_uint32, ctypes.c_void_p, c_u64p,
+                                       c_u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    "luda_files_write": (ctypes.c_int, [ctypes.POINTER(ctypes.c_char_p), ctypes.c_uint32, ctypes.c_void_p, c_u64p,
+                                        c_u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+    "luda_gds_status": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32]),
 }
 
 EXPORTED = tuple(_SIGS)

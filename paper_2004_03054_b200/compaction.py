@@ -73,19 +73,41 @@ class PreparedJob:
     range_lo: bytes | None = None
     range_hi: bytes | None = None
     staged: object = None       # StagedInput holding `files` in pinned memory (no host copy)
+    io_mode: int | None = None  # files are FileRefs read by luda_files_read in this mode
 
 
-def _read_input(meta, inputs, directory):
+class FileRef:
+    """An input SST on storage that ``luda_files_read`` stages straight into
+    the job's device arena (GPUDirect Storage / native bounce; no host copy
+    by the caller). Sized like the bytes it stands for."""
+
+    __slots__ = ("path", "size")
+
+    def __init__(self, path):
+        self.path = os.fspath(path)
+        self.size = os.path.getsize(self.path)
+
+    def __len__(self):
+        return self.size
+
+
+IO_MODES = {"auto": 0, "gds": 1, "bounce": 2}  # luda_files_read / luda_files_write mode
+
+
+def _read_input(meta, inputs, directory, io=None):
     if inputs is not None:
         return inputs[meta.file_id]
     if directory is None:
         raise ValueError("run_compaction needs `inputs` (file_id -> bytes) or `directory`")
-    with open(os.path.join(directory, f"{meta.file_id}.sst"), "rb") as f:
+    path = os.path.join(directory, f"{meta.file_id}.sst")
+    if io is not None:
+        return FileRef(path)
+    with open(path, "rb") as f:
         return f.read()
 
 
 def prepare(job, *, inputs=None, directory=None, config: StoreConfig | None = None,
-            key_range=None, staged=None) -> PreparedJob:
+            key_range=None, staged=None, io=None) -> PreparedJob:
     """Gather input bytes and the run structure of a CompactionJob.
 
     Run rules: L0 files may overlap (each is its own run, newest first as in
@@ -104,22 +126,22 @@ def prepare(job, *, inputs=None, directory=None, config: StoreConfig | None = No
     if lower:
         if job.source_level == 0:
             for m in lower:
-                files.append(_read_input(m, inputs, directory))
+                files.append(_read_input(m, inputs, directory, io))
                 run_first.append(len(files))
         else:
             for m in lower:
-                files.append(_read_input(m, inputs, directory))
+                files.append(_read_input(m, inputs, directory, io))
             run_first.append(len(files))
     if upper:
         for m in upper:
-            files.append(_read_input(m, inputs, directory))
+            files.append(_read_input(m, inputs, directory, io))
         run_first.append(len(files))
     lo, hi = (key_range or (None, None))
     return PreparedJob(files=files, run_first_file=run_first,
                        deeper=deeper_ranges(job.version, job.target_level),
                        block_size=cfg.block_size, restart_interval=cfg.restart_interval,
                        bits_per_key=cfg.bits_per_key, sst_size_target=cfg.sst_size_target,
-                       range_lo=lo, range_hi=hi, staged=staged)
+                       range_lo=lo, range_hi=hi, staged=staged, io_mode=IO_MODES[io] if io else None)
 
 
 _COPY_POOL = None
@@ -209,6 +231,17 @@ class JobRunner:
     def stage(self, pj: PreparedJob, n_lower_files: int, k: int):
         """Pinned staging (unless pre-staged) + H2D into arena k on in_lower /
         in_upper; the compute stream waits for both copies."""
+        if pj.io_mode is not None:  # storage → HBM directly (luda_files_read)
+            offs, total = self.layout(pj.files)
+            arena = self._arena(k, total)
+            n = len(pj.files)
+            paths = (ctypes.c_char_p * max(1, n))(*[f.path.encode() for f in pj.files])
+            used = ctypes.c_int()
+            _native.check(self.L.luda_files_read(paths, n, arena.dptr, (ctypes.c_uint64 * max(1, n))(*offs),
+                                                 (ctypes.c_uint64 * max(1, n))(*[len(f) for f in pj.files]),
+                                                 pj.io_mode, ctypes.byref(used)))
+            self.last_io = {1: "gds", 2: "bounce"}[used.value]
+            return arena, offs, total
         staged = getattr(pj, "staged", None)
         if staged is not None:
             offs, total, src = staged.offs, staged.total, staged.buf.ptr
@@ -326,6 +359,35 @@ class JobRunner:
             cur, staged, k = nxt, nxt_staged, k + 1
         yield self._finish(*prev)
 
+    def run_to_files(self, pj: PreparedJob, n_lower_files: int, alloc, out_directory, io_mode: int):
+        """One job whose output SSTs go from device memory straight to
+        ``{out_directory}/{file_id}.sst`` (luda_files_write); returns
+        ([(path, size, smallest, largest, file_id)], info)."""
+        t0 = time.perf_counter()
+        arena, offs, total = self.stage(pj, n_lower_files, 0)
+        desc, keep = self.describe(pj, arena, offs, total)
+        res = self.device.compact(desc)
+        del keep
+        try:
+            pairs = _native.sst_key_pairs(res)
+            ids = [alloc() for _ in range(res.n_sst)]
+            paths = [os.path.join(out_directory, f"{i}.sst") for i in ids]
+            n = res.n_sst
+            t_w = time.perf_counter()
+            if n:
+                used = ctypes.c_int()
+                _native.check(self.L.luda_files_write((ctypes.c_char_p * n)(*[p.encode() for p in paths]), n,
+                                                      res.out, res.sst_off, res.sst_len, io_mode,
+                                                      ctypes.byref(used)))
+                self.last_io_out = {1: "gds", 2: "bounce"}[used.value]
+            outs = [(paths[i], res.sst_len[i], pairs[i][0], pairs[i][1], ids[i]) for i in range(n)]
+            info = dict(n_in=res.n_in, n_out=res.n_out, blocks_in=res.blocks_in, blocks_out=res.blocks_out,
+                        t_ms=list(res.t_ms), launches=res.launches, input_bytes=sum(len(f) for f in pj.files),
+                        t_wall=time.perf_counter() - t0, t_write=time.perf_counter() - t_w)
+        finally:
+            self.device.release(res)
+        return outs, info
+
     def run(self, pj: PreparedJob, n_lower_files: int):
         """One job; outputs copied to bytes (independent of the pipeline buffers)."""
         t0 = time.perf_counter()
@@ -393,7 +455,8 @@ def _metas(job, outs, alloc):
 
 
 def run_compaction(job, device, *, inputs=None, directory=None, config: StoreConfig | None = None,
-                   new_file_id=None, key_range=None, job_id: int = 0, staged=None):
+                   new_file_id=None, key_range=None, job_id: int = 0, staged=None, io=None,
+                   out_directory=None):
     """Compact ``job`` on ``device``; returns ``(outputs, stats)`` where
     outputs is ``[(sst_bytes, SstMeta)]`` in key order.
 
@@ -403,10 +466,26 @@ def run_compaction(job, device, *, inputs=None, directory=None, config: StoreCon
     callable (or a ``VersionSet``) producing output file ids (default:
     :func:`file_id_allocator`). ``key_range=(lo, hi)`` restricts the job to
     user keys in [lo, hi) (one subcompaction).
+
+    ``io="auto" | "gds" | "bounce"`` reads the inputs from ``directory``
+    straight into device memory (luda_files_read: GPUDirect Storage through
+    cuFile, or the native pinned-bounce pipeline) instead of through Python
+    bytes. ``out_directory`` writes every output SST from device memory to
+    ``{out_directory}/{file_id}.sst`` the same way; outputs are then
+    ``[(path, SstMeta)]``.
     """
     if not isinstance(device, B200Device):
         raise DeviceError("run_compaction needs the b200 device (make_device(DeviceConfig(backend='b200')))")
-    pj = prepare(job, inputs=inputs, directory=directory, config=config, key_range=key_range, staged=staged)
+    pj = prepare(job, inputs=inputs, directory=directory, config=config, key_range=key_range, staged=staged,
+                 io=io)
+    if out_directory is not None:
+        outs, info = runner_for(device).run_to_files(pj, len(job.lower), file_id_allocator(job, new_file_id),
+                                                     out_directory, IO_MODES[io or "auto"])
+        results = [(path, SstMeta(file_id=fid, file_size=size, smallest=sm, largest=lg, level=job.target_level))
+                   for path, size, sm, lg, fid in outs]
+        stats = _job_stats(job, pj, [(range(m.file_size), m) for _, m in results], info, job_id,
+                           t_stage_out=info["t_write"])
+        return results, stats
     outs, info, (t0, t1, t2, t3) = runner_for(device).run(pj, len(job.lower))
     results = _metas(job, outs, file_id_allocator(job, new_file_id))
     return results, _job_stats(job, pj, results, info, job_id, t_stage_out=t3 - t2)

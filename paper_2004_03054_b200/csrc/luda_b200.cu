@@ -1230,3 +1230,4 @@ int luda_dbg_enc_timing(unsigned long long* out, int reset) {
 }  // extern "C"
 
 #include "luda_read_abi.inc"
+#include "luda_io_abi.inc"
