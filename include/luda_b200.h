@@ -226,7 +226,8 @@ int luda_tables_lookup_dev(luda_tables* t, const uint8_t* dev_keys, const uint64
  * without a caller-visible host copy: GPUDirect Storage through cuFile
  * (dlopen'ed; its compatibility mode where nvidia-fs is absent), else a
  * native multi-threaded pread/pwrite ↔ pinned double-buffer ↔ cudaMemcpyAsync
- * pipeline. mode: 0 auto, 1 cuFile only, 2 bounce only; *used_mode = 1
+ * pipeline. mode: 0 auto (cuFile if LUDA_GDS=1 and its driver opens within
+ * LUDA_CUFILE_OPEN_TIMEOUT_S, default 5 s), 1 cuFile only, 2 bounce only; *used_mode = 1
  * (cuFile) or 2 (bounce). Synchronous. Replaces the host file reads / writes
  * around run_compaction (Table file I/O, sst.py:284-340; build_sst writes). */
 int luda_files_read(const char* const* paths, uint32_t n, void* dev_dst, const uint64_t* dst_off,
