@@ -1,7 +1,7 @@
 """LUDA compaction benchmark on B200 (BASELINE.json metric: compaction input
 MB/s and keys/s per B200 at 1/2/4/8 GPUs; % of HBM roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--extras c2,c4,reads,c5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--extras c2,c4,reads,storage,c5]
 
 N = 1 (headline): a step = one full compaction job of BASELINE config 3
 (luda_compact: parse → decode → merge/resolve → plan → encode →
@@ -589,6 +589,60 @@ def measure_reads(L, desc, st, n_lookups=1 << 22, steps=10, warmup=3):
         L.luda_job_release(ctypes.byref(res))
 
 
+def measure_storage(L, w, st, steps=2, root="/tmp/luda_bench_io"):
+    """Storage → HBM → storage: the c3 job's 2,261 input SSTs read from files
+    straight into the device arena (luda_files_read), compacted, and the 987
+    output SSTs written from device memory to files (luda_files_write) —
+    SURVEY §8f row 3. cuFile is used when the host supports GPUDirect Storage
+    (LUDA_GDS=1), else the native 8-thread pread/pwrite ↔ pinned ↔ H2D/D2H
+    pipeline. The input files are written once, untimed (they sit in the page
+    cache: the number is the I/O-path ceiling, not a cold-disk figure)."""
+    import shutil
+
+    import torch
+    from paper_2004_03054_b200 import _native
+    shutil.rmtree(root, ignore_errors=True)
+    os.makedirs(os.path.join(root, "in"))
+    os.makedirs(os.path.join(root, "out"))
+    try:
+        n = len(w.file_off)
+        paths = (ctypes.c_char_p * n)(*[os.path.join(root, "in", f"{i}.sst").encode() for i in range(n)])
+        fo = (ctypes.c_uint64 * n)(*w.file_off)
+        fl = (ctypes.c_uint64 * n)(*w.file_len)
+        used = ctypes.c_int()
+        _native.check(L.luda_files_write(paths, n, w.arena.data_ptr(), fo, fl, 0, ctypes.byref(used)))
+        arena = torch.empty(w.total, dtype=torch.uint8, device="cuda")
+        desc, keep = job_desc(w, arena.data_ptr())
+        torch.cuda.synchronize()
+        t_in, t_job, t_out, out_b = [], [], [], 0
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            _native.check(L.luda_files_read(paths, n, arena.data_ptr(), fo, fl, 0, ctypes.byref(used)))
+            t1 = time.perf_counter()
+            res = compact_once(L, desc, st)
+            _native.check(L.luda_stream_sync(st))
+            t2 = time.perf_counter()
+            m = res.n_sst
+            op = (ctypes.c_char_p * m)(*[os.path.join(root, "out", f"{i}.sst").encode() for i in range(m)])
+            _native.check(L.luda_files_write(op, m, res.out, res.sst_off, res.sst_len, 0, ctypes.byref(used)))
+            t3 = time.perf_counter()
+            out_b = res.out_bytes
+            L.luda_job_release(ctypes.byref(res))
+            t_in.append(t1 - t0)
+            t_job.append(t2 - t1)
+            t_out.append(t3 - t2)
+        tot = min(a + b + c for a, b, c in zip(t_in, t_job, t_out))
+        return {"workload": "c3 job storage -> HBM -> storage (%d input files, %d outputs)" % (n, m),
+                "path": {1: "cuFile (GPUDirect Storage)", 2: "native pread/pwrite <-> pinned <-> H2D/D2H, 8 threads"
+                         }[used.value],
+                "value": round(w.s_in / tot / 1e6, 1), "unit": "MB/s", "s_per_step": round(tot, 3),
+                "read_GBps": round(w.s_in / min(t_in) / 1e9, 2), "write_GBps": round(out_b / min(t_out) / 1e9, 2),
+                "job_ms": round(min(t_job) * 1e3, 2), "input_bytes": w.s_in, "output_bytes": int(out_b),
+                "note": "input files in the page cache (written untimed just before)"}
+    finally:
+        shutil.rmtree(root, ignore_errors=True)
+
+
 def measure_c5(world, rank, local, steps, warmup, group=None, total_gb=256.0):
     import bench_c5
     spec = bench_c5.C5Spec(total_gb=total_gb)
@@ -654,7 +708,7 @@ def parse_args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--keys", type=int, default=1 << 25, help="c3: distinct keys per run (2^25 → 64M entries)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--extras", default="c2,c4,reads,c5", help="other BASELINE configs measured at N=1 ('' = none)")
+    ap.add_argument("--extras", default="c2,c4,reads,storage,c5", help="other BASELINE configs measured at N=1 ('' = none)")
     ap.add_argument("--c5-gb", type=float, default=256.0, help="c5: global job size (GB of input)")
     ap.add_argument("--cpu-keys", type=int, default=1 << 17,
                     help="reference arm: distinct keys per run of each worker's sample job")
@@ -897,6 +951,8 @@ def main_c3(args, local):
         workloads["c4_scaled"] = measure_c4(L, st, peak=hbm)
     if "reads" in extras:
         workloads["reads"] = measure_reads(L, desc, st)
+    if "storage" in extras:
+        workloads["storage"] = measure_storage(L, w, st)
     if "c5" in extras:
         spec, tot = measure_c5(1, 0, local, max(1, args.steps // 5), 1, total_gb=args.c5_gb)
         workloads["c5_1gpu"] = {
