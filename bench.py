@@ -707,7 +707,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--keys", type=int, default=1 << 25, help="c3: distinct keys per run (2^25 → 64M entries)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--extras", default="c2,c4,reads,storage,c5", help="other BASELINE configs measured at N=1 ('' = none)")
     ap.add_argument("--c5-gb", type=float, default=256.0, help="c5: global job size (GB of input)")
     ap.add_argument("--cpu-keys", type=int, default=1 << 17,
@@ -875,6 +875,10 @@ def main_c3(args, local):
 
         def stage(i):
             ar = arenas[i % 2]
+            if i > 0:  # job i's copies start when both of job i-1's have landed (same schedule as run_compactions)
+                for e in ev_in[(i - 1) % 2]:
+                    for sp in (s_lo, s_up):
+                        _native.check(L.luda_stream_wait_event(sp.value, e.value))
             _native.check(L.luda_stage_in_async(ar.data_ptr(), pin_in.ptr, split, s_lo.value))
             _native.check(L.luda_stage_in_async(ar.data_ptr() + split, pin_in.ptr + split, w.total - split,
                                                 s_up.value))

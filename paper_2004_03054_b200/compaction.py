@@ -208,6 +208,7 @@ class JobRunner:
         self.pin_in = [PinnedBuffer(), PinnedBuffer()]
         self.pin_out = [PinnedBuffer(), PinnedBuffer()]
         self.arena = [None, None]
+        self.in_events = []
 
     def _arena(self, k, nbytes):
         a = self.arena[k]
@@ -228,9 +229,10 @@ class JobRunner:
     def layout(self, files):
         return self.layout_sizes([len(f) for f in files])
 
-    def stage(self, pj: PreparedJob, n_lower_files: int, k: int):
+    def stage(self, pj: PreparedJob, n_lower_files: int, k: int, after=None):
         """Pinned staging (unless pre-staged) + H2D into arena k on in_lower /
-        in_upper; the compute stream waits for both copies."""
+        in_upper; the compute stream waits for both copies. ``after``: events
+        the copies wait for (the pipeline's first job gets PCIe to itself)."""
         if pj.io_mode is not None:  # storage → HBM directly (luda_files_read)
             offs, total = self.layout(pj.files)
             arena = self._arena(k, total)
@@ -241,7 +243,8 @@ class JobRunner:
                                                  (ctypes.c_uint64 * max(1, n))(*[len(f) for f in pj.files]),
                                                  pj.io_mode, ctypes.byref(used)))
             self.last_io = {1: "gds", 2: "bounce"}[used.value]
-            return arena, offs, total
+            self.in_events = []  # synchronous: nothing to wait for
+            return arena, offs, total, []
         staged = getattr(pj, "staged", None)
         if staged is not None:
             offs, total, src = staged.offs, staged.total, staged.buf.ptr
@@ -253,16 +256,25 @@ class JobRunner:
         arena = self._arena(k, total)
         dev = self.device
         s_lo, s_up = dev.stream(STREAM_IN_LOWER), dev.stream(STREAM_IN_UPPER)
-        s_cmp = dev.stream("compute")
         split = offs[n_lower_files] if n_lower_files < len(offs) else total
+        for e in after or ():
+            for s in (s_lo, s_up):
+                _native.check(self.L.luda_stream_wait_event(s, e))
         _native.check(self.L.luda_stage_in_async(arena.dptr, src, split, s_lo))
         if total > split:
             _native.check(self.L.luda_stage_in_async(arena.dptr + split, src + split, total - split, s_up))
-        for s in (s_lo, s_up):
-            e = dev._event_on(s)
+        # completion events of both copies: the compute stream waits on them right
+        # before THIS job's compaction (wait_in), not now — a wait queued now would
+        # also hold back the previous job, whose compaction is enqueued later
+        self.in_events = [dev._event_on(s) for s in (s_lo, s_up)]
+        return arena, offs, total, self.in_events
+
+    def wait_in(self, events):
+        """The compute stream waits for a staged job's copies; events released."""
+        s_cmp = self.device.stream("compute")
+        for e in events:
             _native.check(self.L.luda_stream_wait_event(s_cmp, e))
-            _native.check(self.L.luda_event_destroy(e))  # released once the wait is satisfied
-        return arena, offs, total
+            _native.check(self.L.luda_event_destroy(e))
 
     def describe(self, pj: PreparedJob, arena, offs, total):
         n = len(pj.files)
@@ -346,9 +358,13 @@ class JobRunner:
             nxt = next(it, None)
             nxt_staged = None
             if nxt is not None:
-                # arena / staging buffer (k+1)%2 were last used by job k-1, whose compaction has returned
-                nxt_staged = self.stage(nxt[0], nxt[1], (k + 1) % 2)
-            desc, keep = self.describe(cur[0], *staged)
+                # arena / staging buffer (k+1)%2 were last used by job k-1, whose compaction has returned.
+                # Job k+1's copies start when BOTH of job k's have landed: on two streams, the half that
+                # finishes first would otherwise start job k+1's copy and share PCIe with the other half,
+                # delaying job k (whose compaction waits for both) by up to a whole transfer.
+                nxt_staged = self.stage(nxt[0], nxt[1], (k + 1) % 2, after=staged[3])
+            self.wait_in(staged[3])
+            desc, keep = self.describe(cur[0], *staged[:3])
             res = self.device.compact(desc)
             del keep
             ev = self._fetch_async(res, k % 2)
@@ -364,7 +380,8 @@ class JobRunner:
         ``{out_directory}/{file_id}.sst`` (luda_files_write); returns
         ([(path, size, smallest, largest, file_id)], info)."""
         t0 = time.perf_counter()
-        arena, offs, total = self.stage(pj, n_lower_files, 0)
+        arena, offs, total, evs = self.stage(pj, n_lower_files, 0)
+        self.wait_in(evs)
         desc, keep = self.describe(pj, arena, offs, total)
         res = self.device.compact(desc)
         del keep
