@@ -45,8 +45,9 @@ const char* luda_last_error(void);
 int64_t luda_last_error_offset(void); /* block offset of the last LUDA_CORRUPT, or -1 */
 int luda_abi_version(void);
 
-/* Process-wide options. LUDA_OPT_PLANNER_TILE: minimum tile (items) of the
- * greedy-chain block/SST planner, default 8192. Outputs do not depend on it;
+/* Process-wide options. LUDA_OPT_PLANNER_TILE: tile (items) of the greedy-chain
+ * block/SST planner, default 8192 — smaller (floor 256) when an input would
+ * span fewer than 2 tiles per SM, never below the longest jump. Outputs do not depend on it;
  * the parity tests set it to 32 so that small jobs exercise the planner's
  * multi-tile / multi-group composition. */
 enum luda_option { LUDA_OPT_PLANNER_TILE = 1 };

@@ -313,7 +313,9 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& s
                     uint64_t bbase, bool resolve) -> int {
     const uint64_t ntiles = (na + nb + kMergeTile - 1) / kMergeTile;
     GET(split, uint64_t, 3 * (ntiles + 1), false);
-    merge_partition_kernel<W><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, st>>>(A, na, B, nb, ntiles, split);
+    const bool warp_mode = ntiles + 1 <= 32ull * g_num_sms;
+    merge_partition_kernel<W><<<(unsigned)(warp_mode ? (ntiles + 1 + 7) / 8 : (ntiles + 1 + 255) / 256), 256, 0, st>>>(
+        A, na, B, nb, ntiles, split, warp_mode);
     ++g_launches;
     MergeArgs<W> m{};
     m.A = A; m.na = na; m.B = B; m.nb = nb; m.split = split; m.ntiles = ntiles; m.out = out;
@@ -382,7 +384,11 @@ int run_chain(cudaStream_t st, Scratch& scratch, const uint32_t* jmp, uint32_t n
     return LUDA_OK;
   }
   D = std::max<uint32_t>(D, 1);
-  uint32_t T = std::max<uint32_t>(T_min, D);
+  // Tile: T_min (default 8192) for large inputs, shrunk so that small ones still
+  // spread over >= 2 tiles per SM — the map / emit kernels walk a tile serially
+  // (c2: 21.6K survivors in 3 tiles of 8192 made the block chain ~0.2 ms).
+  const uint32_t T_fill = (uint32_t)((n + 2ull * g_num_sms - 1) / (2ull * g_num_sms));
+  uint32_t T = std::max<uint32_t>(std::min<uint32_t>(T_min, std::max<uint32_t>(T_fill, 256)), D);
   T = (T + 31) & ~31u;
   const uint32_t ntiles = (uint32_t)((n + (uint64_t)T - 1) / T);
   const uint32_t G = std::max<uint32_t>(1, (uint32_t)std::ceil(std::sqrt((double)ntiles)));

@@ -152,18 +152,47 @@ __device__ __forceinline__ uint64_t merge_split(const RunView<W>& A, uint64_t na
   return lo;
 }
 
+// Merge-path split by one WARP per diagonal: 32-ary search rounds (each lane
+// tests one candidate; the predicate is monotone, so the ballot's popcount
+// brackets the split), ~log32 instead of log2 dependent steps — every step
+// resolves two segmented-view records (a segment binary search each).
+template <int W>
+__device__ __forceinline__ uint64_t merge_split_warp(const RunView<W>& A, uint64_t na, const RunView<W>& B, uint64_t nb,
+                                                     uint64_t diag) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint64_t lo = diag > nb ? diag - nb : 0;
+  uint64_t hi = diag < na ? diag : na;
+  while (hi > lo) {
+    const uint64_t span = hi - lo;
+    const bool last = span <= 32;
+    const uint64_t m = last ? lo + lane : lo + ((uint64_t)(lane + 1) * span) / 33;
+    const bool p = (!last || lane < span) && rec_le(A[m], B[diag - 1 - m]);
+    const uint32_t c = __popc(__ballot_sync(0xFFFFFFFFu, p));  // P holds on a prefix of the candidates
+    if (last) return lo + c;
+    const uint64_t lo0 = lo;
+    if (c > 0) lo = lo0 + ((uint64_t)c * span) / 33 + 1;
+    if (c < 32) hi = lo0 + ((uint64_t)(c + 1) * span) / 33;
+  }
+  return lo;
+}
+
+// warp_mode: a warp per diagonal (few tiles: latency-bound small jobs), else
+// a thread per diagonal (many tiles: the 32-ary rounds would cost more loads).
 template <int W>
 __global__ void merge_partition_kernel(RunView<W> A, uint64_t na, RunView<W> B, uint64_t nb, uint64_t ntiles,
-                                       uint64_t* split) {
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > ntiles) return;
+                                       uint64_t* split, bool warp_mode) {
+  const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t t = warp_mode ? gt >> 5 : gt;
+  if (t > ntiles) return;  // warp-uniform in warp mode
   uint64_t diag = t * (uint64_t)kMergeTile;
   if (diag > na + nb) diag = na + nb;
-  const uint64_t a = merge_split(A, na, B, nb, diag);
-  split[t] = a;
-  // starting segments of the tile's A / B slices (segmented views)
-  split[(ntiles + 1) + t] = A.lo ? A.seg(A.off + a) : 0u;
-  split[2 * (ntiles + 1) + t] = B.lo ? B.seg(B.off + (diag - a)) : 0u;
+  const uint64_t a = warp_mode ? merge_split_warp(A, na, B, nb, diag) : merge_split(A, na, B, nb, diag);
+  if (!warp_mode || (threadIdx.x & 31u) == 0) {
+    split[t] = a;
+    // starting segments of the tile's A / B slices (segmented views)
+    split[(ntiles + 1) + t] = A.lo ? A.seg(A.off + a) : 0u;
+    split[2 * (ntiles + 1) + t] = B.lo ? B.seg(B.off + (diag - a)) : 0u;
+  }
 }
 
 // Level-run file seams, checked before any merge pass: the last record of
