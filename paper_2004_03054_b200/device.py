@@ -125,6 +125,9 @@ class TransferHandle:
 
 
 class DispatchHandle:
+    """device.py:167-185: completion is observable from any thread; wait()
+    raises the folded error of the first failing item."""
+
     def __init__(self, kind: str, n_items: int):
         self.kind = kind
         self.n_items = n_items
@@ -132,11 +135,14 @@ class DispatchHandle:
         self.t_end = None
         self.results = [None] * n_items
         self.error = None
+        self._event = threading.Event()
 
     def done(self) -> bool:
-        return True
+        return self._event.is_set()
 
     def wait(self, timeout=None):
+        if not self._event.wait(timeout):
+            raise DeviceError(f"{self.kind} dispatch timed out")
         if self.error is not None:
             raise self.error
         return self.results
@@ -223,6 +229,7 @@ class B200Device:
         self._streams: dict[str, int] = {}
         self._seq: dict[str, int] = {}
         self._pinned: list = []  # pinned staging kept alive until transfer completion
+        self._dispatch_lock = threading.Lock()  # one batched kernel at a time, in submission order
 
     # -- streams --------------------------------------------------------------
     def stream(self, name: str) -> int:
@@ -343,15 +350,29 @@ class B200Device:
         self._check_dispatch(spec)
         h = DispatchHandle(spec.kind, len(spec.items))
         t0 = time.monotonic()
-        try:
-            self._run_items(spec, h, on_item)
-        finally:
-            for rid in spec.writes:
-                r = self._regions.get(rid)
-                if r is not None:
-                    r.state = READY
-            h.t_end = time.monotonic()
-            self._stats.dispatch(spec.kind, len(spec.items), h.t_end - t0)
+
+        # Asynchronous like HostParallelDevice.dispatch (device.py:566-607): a
+        # collector thread runs the batched kernel, calls on_item(i, result) in
+        # item order, then releases the written regions and signals the handle.
+        # Dispatches run one at a time per device, in submission order.
+        def collect():
+            with self._dispatch_lock:
+                try:
+                    self._run_items(spec, h, on_item)
+                except Exception as exc:  # noqa: BLE001 — surfaced at wait()
+                    if h.error is None:
+                        h.error = exc if isinstance(exc, (DeviceError, CorruptionError)) else \
+                            DeviceError(f"dispatch failed: {exc}")
+                finally:
+                    for rid in spec.writes:
+                        r = self._regions.get(rid)
+                        if r is not None:
+                            r.state = READY
+                    h.t_end = time.monotonic()
+                    self._stats.dispatch(spec.kind, len(spec.items), h.t_end - t0)
+                    h._event.set()
+
+        threading.Thread(target=collect, name=f"luda-collect-{spec.kind}", daemon=True).start()
         return h
 
     def _run_items(self, spec: KernelSpec, h: DispatchHandle, on_item):

@@ -166,3 +166,44 @@ def test_dispatch_errors_first_item_wins(dev):
     with pytest.raises(DeviceError):
         dev.dispatch(KernelSpec("unpack", small, reads=(src.region_id,), writes=(p.region_id, t.region_id))).wait()
     dev.free_all()
+
+
+def test_dispatch_is_asynchronous_with_ordered_callbacks(dev):
+    """HostParallelDevice semantics (device.py:566-607): dispatch returns a
+    handle at once, a collector thread calls on_item in item order, done()
+    turns true and wait() returns the per-item results; written regions are
+    FILLING until completion, READY after; back-to-back dispatches run in
+    submission order."""
+    import threading
+
+    from paper_2004_03054_b200.device import READY, KernelSpec
+    job = jobgen.c3(n=2000, seed=0xA5, sst_target=64 * 1024)
+    lower, _ = jobgen.materialize(job)
+    data = lower[0]
+    _, index = O.open_table(data)
+    src = region(dev, data)
+    cap = sum(ln for _, _, ln in index) * 4
+    p, t = region(dev, cap=cap), region(dev, cap=cap)
+    items, slot = [], 0
+    for _, off, ln in index:
+        items.append((src.region_id, off, ln, p.region_id, slot, 4 * ln, t.region_id, slot, 4 * ln))
+        slot += 4 * ln
+    seen, tids = [], set()
+
+    def on_item(i, r):
+        seen.append(i)
+        tids.add(threading.get_ident())
+
+    h1 = dev.dispatch(KernelSpec("unpack", tuple(items), reads=(src.region_id,),
+                                 writes=(p.region_id, t.region_id)), on_item=on_item)
+    res1 = h1.wait(timeout=60)
+    assert h1.done()
+    assert seen == list(range(len(items)))
+    assert threading.get_ident() not in tids  # called from the collector thread
+    assert all(r is not None for r in res1)
+    assert p.state == READY and t.region_id in dev._regions
+    # two dispatches in flight: results equal a sequential run
+    h2 = dev.dispatch(KernelSpec("unpack", tuple(items), reads=(src.region_id,), writes=(p.region_id, t.region_id)))
+    h3 = dev.dispatch(KernelSpec("unpack", tuple(items), reads=(src.region_id,), writes=(p.region_id, t.region_id)))
+    assert h2.wait(timeout=60) == res1 and h3.wait(timeout=60) == res1
+    dev.free_all()
