@@ -719,7 +719,9 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
 
 // ---- per-SST filter + index + footer -----------------------------------------------------
 constexpr int kMetaThreads = 512;
-constexpr int kMetaUnroll = 4;  // records in flight per thread in the bloom loop
+// keys in flight per thread in the bloom loop (var records: 4, else they spill)
+template <int W>
+__host__ __device__ constexpr int meta_unroll() { return W <= 4 ? 8 : 4; }
 
 // a mod d for 32-bit a, d >= 1 with rcp = floor((2^64 - 1) / d) + 1
 // (Lemire, Kaser, Kurz: "Faster remainder by direct computation").
@@ -807,25 +809,27 @@ __global__ void __launch_bounds__(kMetaThreads, 1) sst_meta_kernel(MetaArgs<W> a
     // ---- bloom bits: positions (h + j*delta) mod n_bits, 64-bit (bloom.py:81-87) ----
     if (nbits < (1ull << 31)) {
       // 32-bit positions; h mod n and delta mod n by Lemire's fastmod (one
-      // 64-bit reciprocal per SST). Records are loaded kMetaUnroll at a time
+      // 64-bit reciprocal per SST). Records are loaded meta_unroll<W>() at a time
       // so the loop is not one DRAM latency per key.
       const uint32_t nb32 = (uint32_t)nbits;
       const uint64_t rcp = ~0ull / nb32 + 1;
       const uint64_t e_end = fe + ne;
-      for (uint64_t e0 = fe + tid; e0 < e_end; e0 += kMetaUnroll * kMetaThreads) {
-        Rec<W> r[kMetaUnroll];
+      for (uint64_t e0 = fe + tid; e0 < e_end; e0 += meta_unroll<W>() * kMetaThreads) {
+        Rec<W> r[meta_unroll<W>()];  // key words only: the hash never reads the trailer / handle
 #pragma unroll
-        for (int u = 0; u < kMetaUnroll; ++u) {
+        for (int u = 0; u < meta_unroll<W>(); ++u) {
           const uint64_t e = e0 + (uint64_t)u * kMetaThreads;
-          r[u] = a.rec[e < e_end ? e : fe];
+          const Rec<W>& src = a.rec[e < e_end ? e : fe];
+#pragma unroll
+          for (int w = 0; w < W; ++w) r[u].k[w] = src.k[w];
         }
-        // the kMetaUnroll key hashes are independent table chains: computed
+        // the meta_unroll<W>() key hashes are independent table chains: computed
         // together (ILP) before any probe
-        uint32_t h[kMetaUnroll];
+        uint32_t h[meta_unroll<W>()];
 #pragma unroll
-        for (int u = 0; u < kMetaUnroll; ++u) h[u] = user_key_crc<W>(r[u], rec_ulen(r[u], is_var<W>(), L), tl);
+        for (int u = 0; u < meta_unroll<W>(); ++u) h[u] = user_key_crc<W>(r[u], rec_ulen(r[u], is_var<W>(), L), tl);
 #pragma unroll
-        for (int u = 0; u < kMetaUnroll; ++u) {
+        for (int u = 0; u < meta_unroll<W>(); ++u) {
           if (e0 + (uint64_t)u * kMetaThreads < e_end) {
             const uint32_t delta = (h[u] >> 17) | (h[u] << 15);
             uint32_t p = fastmod_u32(h[u], rcp, nb32);
