@@ -237,6 +237,23 @@ int luda_files_write(const char* const* paths, uint32_t n, const void* dev_src, 
                      const uint64_t* len, int mode, int* used_mode);
 /* 1 when the cuFile driver opened (message in why), else 0. */
 int luda_gds_status(char* why, uint32_t cap);
+/* ---- multi-GPU: the splitter all-gather -------- */
+/* The only collective of the key-range-partitioned compaction: every rank's
+ * fixed-size index-key sample array is all-gathered so all ranks pick the same
+ * P - 1 splitters. NCCL over NVLink/NVSwitch; libnccl is dlopen'ed. The
+ * reference is single-host (multi-device is a SPEC non-goal). */
+typedef struct luda_comm luda_comm;
+int luda_nccl_unique_id(uint8_t* out_128_bytes);  /* rank 0 creates, the launcher distributes */
+int luda_nccl_init_rank(int nranks, int rank, const uint8_t* unique_id, luda_comm** comm); /* one process per GPU */
+int luda_nccl_init_all(int ndev, const int* devices, luda_comm** comms);  /* one process, ndev GPUs (comms[ndev]) */
+/* recv = the ranks' send buffers (bytes_per_rank each) in rank order; device
+ * pointers, asynchronous on `stream`. Several communicators of one process:
+ * bracket the calls with luda_nccl_group_start / _end. */
+int luda_allgather_splitters(luda_comm* comm, const void* dev_send, void* dev_recv, uint64_t bytes_per_rank,
+                             void* stream);
+int luda_nccl_group_start(void);
+int luda_nccl_group_end(void);
+int luda_nccl_destroy(luda_comm* comm);
 #ifdef __cplusplus
 }
 #endif

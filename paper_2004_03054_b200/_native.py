@@ -152,6 +152,15 @@ _SIGS = {
     "luda_files_write": (ctypes.c_int, [ctypes.POINTER(ctypes.c_char_p), ctypes.c_uint32, ctypes.c_void_p, c_u64p,
                                         c_u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     "luda_gds_status": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint32]),
+    # multi-GPU splitter all-gather (luda_nccl_abi.inc)
+    "luda_nccl_unique_id": (ctypes.c_int, [c_u8p]),
+    "luda_nccl_init_rank": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_u8p, ctypes.POINTER(ctypes.c_void_p)]),
+    "luda_nccl_init_all": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_void_p)]),
+    "luda_allgather_splitters": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                                ctypes.c_void_p]),
+    "luda_nccl_group_start": (ctypes.c_int, []),
+    "luda_nccl_group_end": (ctypes.c_int, []),
+    "luda_nccl_destroy": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1237,3 +1237,4 @@ int luda_dbg_enc_timing(unsigned long long* out, int reset) {
 
 #include "luda_read_abi.inc"
 #include "luda_io_abi.inc"
+#include "luda_nccl_abi.inc"

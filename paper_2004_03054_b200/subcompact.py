@@ -25,9 +25,12 @@ compactions run independently per range (``tests/test_subcompact.py``).
 
 from __future__ import annotations
 
+import ctypes
+
 import struct
 from dataclasses import dataclass
 
+from . import _native
 from .version import CompactionJob, user_key_of
 
 FOOTER = struct.Struct("<IIIIQ")
@@ -160,19 +163,54 @@ class SplitPlan:
     mine: list              # range indices of this rank
 
 
+_COMMS: dict = {}
+
+
+def _luda_comm(L, world: int, group):
+    """The C-ABI NCCL communicator of this process group (luda_nccl_init_rank;
+    rank 0's unique id travels over the launcher's process group)."""
+    import torch.distributed as dist
+    key = (id(group), world)
+    c = _COMMS.get(key)
+    if c is None:
+        rank = dist.get_rank(group)
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _native.check(L.luda_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        _native.check(L.luda_nccl_init_rank(world, rank, uid, ctypes.byref(h)))
+        c = _COMMS[key] = h.value
+    return c
+
+
 def allgather_bytes(payload: bytes, world: int, group=None) -> list:
-    """All-gather equal-length byte strings over torch.distributed (NCCL when
-    the default process group is NCCL — a CUDA tensor — else gloo/CPU)."""
+    """All-gather equal-length byte strings. On GPUs
+    (NCCL process group) through the C ABI's ``luda_allgather_splitters``
+    over NVLink; on CPU process groups (gloo: the multi-process tests) through
+    torch.distributed."""
     if world <= 1:
         return [payload]
     import torch
     import torch.distributed as dist
     backend = dist.get_backend(group)
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
-    t = torch.frombuffer(bytearray(payload), dtype=torch.uint8).to(dev)
+    if backend == "nccl":
+        L = _native.lib(torch.cuda.current_device())
+        comm = _luda_comm(L, world, group)
+        n = len(payload)
+        send = torch.frombuffer(bytearray(payload), dtype=torch.uint8).cuda()
+        recv = torch.empty(world * n, dtype=torch.uint8, device="cuda")
+        s = torch.cuda.current_stream()
+        _native.check(L.luda_allgather_splitters(comm, send.data_ptr(), recv.data_ptr(), n, s.cuda_stream))
+        s.synchronize()
+        blob = recv.cpu().numpy().tobytes()
+        return [blob[i * n:(i + 1) * n] for i in range(world)]
+    t = torch.frombuffer(bytearray(payload), dtype=torch.uint8)
     outs = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(outs, t, group=group)
-    return [bytes(o.cpu().numpy().tobytes()) for o in outs]
+    return [bytes(o.numpy().tobytes()) for o in outs]
 
 
 def plan_ranges(job: CompactionJob, inputs, *, nranges: int = 64, per_file: int = 64, world: int = 1,
