@@ -189,6 +189,57 @@ const char* file_msg(uint32_t code) {
   }
 }
 
+// Filter / index CRCs of a job's input files, computed on a side stream while
+// the block table and the decode run (jobs are serialised by g_job_mu, so one
+// instance serves every job). h: pinned, crc[2 nf] then stored[2 nf].
+struct DeferredCrc {
+  cudaStream_t side = nullptr;
+  cudaEvent_t parsed = nullptr, done = nullptr;
+  uint32_t* h = nullptr;
+  uint64_t cap = 0;
+  uint32_t nf = 0;
+  bool pending = false;
+  std::vector<FileInfo> info;
+  int prepare(uint32_t n) {
+    pending = false;
+    if (!side) {
+      if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&parsed, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess)
+        return fail(LUDA_DEVICE, "side stream / event creation failed");
+    }
+    if (4ull * n > cap) {
+      if (h) cudaFreeHost(h);
+      cap = std::max<uint64_t>(4ull * n, 1024);
+      if (cudaHostAlloc(&h, cap * 4, cudaHostAllocDefault) != cudaSuccess) {
+        h = nullptr;
+        cap = 0;
+        return fail(LUDA_DEVICE, "pinned CRC staging allocation failed");
+      }
+    }
+    nf = n;
+    info.assign(n, FileInfo{});
+    return LUDA_OK;
+  }
+};
+DeferredCrc g_dcrc;
+
+int check_parsed_file(const FileInfo& fi, const uint32_t* crc, const uint32_t* stored);
+
+// The deferred filter / index CRC comparisons, files in job order (the
+// structural checks of every file passed before the job went on).
+int deferred_crc_check() {
+  DeferredCrc& dc = g_dcrc;
+  if (!dc.pending) return LUDA_OK;
+  dc.pending = false;
+  CK(cudaEventSynchronize(dc.done));
+  for (uint32_t f = 0; f < dc.nf; ++f) {
+    const int rc = check_parsed_file(dc.info[f], dc.h + 2 * f, dc.h + 2 * dc.nf + 2 * f);
+    if (rc) return rc;
+  }
+  return LUDA_OK;
+}
+
 // Table.__init__ (sst.py:284-310) outcome of one parsed file, in the
 // reference's check order: footer/magic/filter length, filter CRC, probe
 // count, index length, index CRC, index entries. crc/stored: filter, index.
@@ -665,6 +716,8 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     CK(cudaMemcpyAsync(&hm[0], d_lo + nw, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hm[1], d_max, 8, cudaMemcpyDeviceToHost, st));
     int rc = sync(st);
+    if (rc) return rc;
+    rc = deferred_crc_check();  // filter / index CRC errors come before any data-block error
     if (rc) return rc;
     if (herr[0] != ~0ull || herr[1] != ~0ull) {
       const bool ref = herr[0] != ~0ull;
@@ -1143,23 +1196,39 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   parse_files_a<<<(nf * 32 + 255) / 256, 256, 0, st>>>(pa);
   ++g_launches;
   CK(cudaGetLastError());
-  int rc = luda_crc32_batch(jd->arena, caddr, clen, 2 * nf, ccrc, st);
+  // Filter / index CRCs on the side stream, concurrently with the block table
+  // and the decode: nothing but error reporting needs them, and the decode
+  // sync (or the end of the job) checks them before any later error.
+  DeferredCrc& dc = g_dcrc;
+  int rc = dc.prepare(nf);
   if (rc) return rc;
-  std::vector<FileInfo> hinfo(nf);
-  std::vector<uint32_t> hcrc(2 * nf), hst(2 * nf);
+  CK(cudaEventRecord(dc.parsed, st));
+  CK(cudaStreamWaitEvent(dc.side, dc.parsed, 0));
+  rc = luda_crc32_batch(jd->arena, caddr, clen, 2 * nf, ccrc, dc.side);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(dc.h, ccrc, 8ull * nf, cudaMemcpyDeviceToHost, dc.side));
+  CK(cudaMemcpyAsync(dc.h + 2 * nf, cstored, 8ull * nf, cudaMemcpyDeviceToHost, dc.side));
+  CK(cudaEventRecord(dc.done, dc.side));
+  std::vector<FileInfo>& hinfo = dc.info;
   CK(cudaMemcpyAsync(hinfo.data(), info, sizeof(FileInfo) * nf, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hcrc.data(), ccrc, 8ull * nf, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hst.data(), cstored, 8ull * nf, cudaMemcpyDeviceToHost, st));
   rc = sync(st);
   if (rc) return rc;
+  bool clean = true;
+  for (uint32_t f = 0; f < nf; ++f) clean &= !hinfo[f].code && !hinfo[f].kbad && !hinfo[f].icode;
+  if (!clean) {  // a structural error: its place in the reference order depends on the CRCs
+    CK(cudaEventSynchronize(dc.done));
+    for (uint32_t f = 0; f < nf; ++f) {
+      rc = check_parsed_file(hinfo[f], dc.h + 2 * f, dc.h + 2 * nf + 2 * f);
+      if (rc) return rc;
+    }
+  }
+  dc.pending = true;
   // Reference order per file (Table.__init__), files in job order.
   uint32_t K = 0xFFFFFFFEu;
   bool mixed = false;
   std::vector<uint32_t> fbb(nf + 1, 0);
   for (uint32_t f = 0; f < nf; ++f) {
     const FileInfo& fi = hinfo[f];
-    rc = check_parsed_file(fi, hcrc.data() + 2 * f, hst.data() + 2 * f);
-    if (rc) return rc;
     fbb[f + 1] = fbb[f] + fi.nblocks;
     if (fi.nblocks) {
       if (fi.klen == 0xFFFFFFFFu) mixed = true;
@@ -1168,7 +1237,7 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
     }
   }
   const uint32_t nblk = fbb[nf];
-  if (nblk == 0) return LUDA_OK;  // no data blocks: empty output
+  if (nblk == 0) return deferred_crc_check();  // no data blocks: empty output
   // Fixed-K records when every index key has one length <= 32 bytes; else
   // (mixed lengths, longer keys) the generic-length "var" records.
   bool var = mixed || K < 8 || K - 8 > 32;
@@ -1206,6 +1275,10 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
     }
   }
   if (var) rc = compact_w<kVarW>(st, scratch, jd, res, 8 * kVarW + 8, nblk, bt, d_fbb, pev, true);
+  {
+    const int crc_rc = deferred_crc_check();  // a filter / index CRC error outranks every later error
+    if (crc_rc) rc = crc_rc;
+  }
   if (rc) {
     luda_job_release(res);
     return rc;

@@ -422,3 +422,53 @@ def test_user_keys_longer_than_71_bytes_unsupported(dev):
     O.reference_compact([f])  # the reference accepts them
     with pytest.raises(UnsupportedInputError):
         compact_files(dev, [f], [], source_level=0)
+
+
+def test_crc_error_outranks_later_data_errors(dev):
+    """The filter / index CRCs are checked on a side stream while the decode
+    runs; their errors still come first: Table.__init__ of every input file
+    precedes the data-block decode, so a bad filter CRC in
+    a later file outranks a corrupt data block in an earlier one."""
+    from paper_2004_03054_b200 import CorruptionError
+    job, lower, upper = _corrupt_case()
+    lower = list(lower)
+    _, index = O.open_table(lower[0])
+    bad = bytearray(lower[0])
+    bad[index[1][1] + 9] ^= 0x20  # data block 1 of the first file
+    lower[0] = bytes(bad)
+    f = bytearray(upper[2])
+    foff = O.FOOTER.unpack_from(f, len(f) - O.FOOTER_SIZE)[0]
+    f[foff + 2] ^= 0x04  # filter of a later file
+    upper = list(upper)
+    upper[2] = bytes(f)
+    with pytest.raises(O.CorruptionError) as want:
+        O.reference_compact(lower + upper)
+    assert want.value.offset == foff
+    with pytest.raises(CorruptionError) as got:
+        gpu_compact(dev, job, lower, upper, {})
+    assert got.value.offset == foff
+
+
+def test_structural_error_before_later_crc_error(dev):
+    """A structural filter error (bad probe count, CRC recomputed so the filter
+    CRC itself passes) in the first file outranks a filter CRC error in a later
+    file — the synchronous check path."""
+    import struct
+
+    from paper_2004_03054_b200 import FormatError
+    job, lower, upper = _corrupt_case()
+    lower = list(lower)
+    f = bytearray(lower[0])
+    foff, flen, _, _, _ = O.FOOTER.unpack_from(f, len(f) - O.FOOTER_SIZE)
+    f[foff + flen - 5] = 40  # probe count k > 30
+    struct.pack_into("<I", f, foff + flen - 4, zlib.crc32(bytes(f[foff:foff + flen - 4])))
+    lower[0] = bytes(f)
+    g = bytearray(upper[1])
+    goff = O.FOOTER.unpack_from(g, len(g) - O.FOOTER_SIZE)[0]
+    g[goff + 1] ^= 0x01
+    upper = list(upper)
+    upper[1] = bytes(g)
+    with pytest.raises(O.FormatError, match="bad probe count"):
+        O.reference_compact(lower + upper)
+    with pytest.raises(FormatError, match="bad probe count"):
+        gpu_compact(dev, job, lower, upper, {})
