@@ -189,6 +189,22 @@ const char* file_msg(uint32_t code) {
   }
 }
 
+// Small pinned host slots for per-job D2H of counters / error words (a D2H
+// into pageable memory would block the host at the copy).
+struct PinnedSlots {
+  unsigned long long* herr = nullptr;
+  uint64_t* hm = nullptr;
+  int init() {
+    if (herr) return LUDA_OK;
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 64, cudaHostAllocDefault) != cudaSuccess) return fail(LUDA_DEVICE, "pinned alloc failed");
+    herr = reinterpret_cast<unsigned long long*>(p);
+    hm = reinterpret_cast<uint64_t*>(herr + 2);
+    return LUDA_OK;
+  }
+};
+PinnedSlots g_pin;
+
 // Filter / index CRCs of a job's input files, computed on a side stream while
 // the block table and the decode run (jobs are serialised by g_job_mu, so one
 // instance serves every job). h: pinned, crc[2 nf] then stored[2 nf].
@@ -692,6 +708,16 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   GET(d_count, uint64_t, nw, false);
   GET(d_lo, uint64_t, nw + 1, false);
   GET(d_max, uint64_t, 1, false);
+  // file seams of every multi-file run, checked (with the file bases) right
+  // after the decode, before any merge pass
+  std::vector<uint32_t> run_first(jd->run_first_file, jd->run_first_file + jd->n_runs + 1);
+  std::vector<uint32_t> first_of_run(jd->n_files, 0), seam_bad(jd->n_files, 0);
+  for (uint32_t r = 0; r + 1 < run_first.size(); ++r)
+    for (uint32_t f = run_first[r]; f < run_first[r + 1] && f < jd->n_files; ++f) first_of_run[f] = run_first[r];
+  GET(d_fbase, uint64_t, jd->n_files + 1, false);
+  GET(d_for, uint32_t, jd->n_files, false);
+  GET(d_bad, uint32_t, jd->n_files, false);
+  CK(cudaMemcpyAsync(d_for, first_of_run.data(), 4ull * jd->n_files, cudaMemcpyHostToDevice, st));
   for (int attempt = 0; attempt < 2; ++attempt) {
     X = scratch.get<Rec<W>>((uint64_t)nw * seg_cap, false);
     if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
@@ -710,11 +736,23 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     CK(cudaGetLastError());
     seg_scan_kernel<<<1, 1024, 0, st>>>(d_count, nw, d_lo, d_max);
     ++g_launches;
-    unsigned long long herr[2];
-    uint64_t hm[2];
+    // file bases and file-seam checks ride on the same sync (meaningless if
+    // the segment capacity overflowed: then they are recomputed)
+    file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_local, d_lo, nblk, nw,
+                                                                            d_file_blk_base, jd->n_files, d_fbase);
+    ++g_launches;
+    {
+      const RunView<W> sv{X, d_lo, seg_cap, nw, 0};
+      seam_check_kernel<W><<<(jd->n_files + 255) / 256, 256, 0, st>>>(sv, d_fbase, d_for, jd->n_files, d_bad);
+      ++g_launches;
+    }
+    unsigned long long* herr = g_pin.herr;
+    uint64_t* hm = g_pin.hm;
     CK(cudaMemcpyAsync(herr, errs, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hm[0], d_lo + nw, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hm[1], d_max, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(seam_bad.data(), d_bad, 4ull * jd->n_files, cudaMemcpyDeviceToHost, st));
     int rc = sync(st);
     if (rc) return rc;
     rc = deferred_crc_check();  // filter / index CRC errors come before any data-block error
@@ -736,27 +774,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     if (attempt == 1) return fail(LUDA_DEVICE, "decode record capacity overflow");
     seg_cap = hm[1];
   }
-  GET(d_fbase, uint64_t, jd->n_files + 1, false);
-  file_entry_base_kernel<<<(jd->n_files + 1 + 255) / 256, 256, 0, st>>>(d_local, d_lo, nblk, nw, d_file_blk_base,
-                                                                          jd->n_files, d_fbase);
-  ++g_launches;
   const RunView<W> segview{X, d_lo, seg_cap, nw, 0};
-  // file seams of every multi-file run, checked before any merge pass
-  std::vector<uint32_t> run_first(jd->run_first_file, jd->run_first_file + jd->n_runs + 1);
-  std::vector<uint32_t> first_of_run(jd->n_files, 0), seam_bad(jd->n_files, 0);
-  for (uint32_t r = 0; r + 1 < run_first.size(); ++r)
-    for (uint32_t f = run_first[r]; f < run_first[r + 1] && f < jd->n_files; ++f) first_of_run[f] = run_first[r];
-  GET(d_for, uint32_t, jd->n_files, false);
-  GET(d_bad, uint32_t, jd->n_files, false);
-  CK(cudaMemcpyAsync(d_for, first_of_run.data(), 4ull * jd->n_files, cudaMemcpyHostToDevice, st));
-  seam_check_kernel<W><<<(jd->n_files + 255) / 256, 256, 0, st>>>(segview, d_fbase, d_for, jd->n_files, d_bad);
-  ++g_launches;
-  CK(cudaMemcpyAsync(fbase.data(), d_fbase, 8ull * (jd->n_files + 1), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(seam_bad.data(), d_bad, 4ull * jd->n_files, cudaMemcpyDeviceToHost, st));
-  {
-    int rc = sync(st);
-    if (rc) return rc;
-  }
   res->n_in = n_in;
   if (ev) CK(cudaEventRecord(ev[2], st));
   // ---- merge + resolve ----
@@ -1168,6 +1186,10 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   std::lock_guard<std::mutex> lock(g_job_mu);
   memset(res, 0, sizeof(*res));
   cudaStream_t st = (cudaStream_t)stream;
+  {
+    const int prc = g_pin.init();
+    if (prc) return prc;
+  }
   KTimer kt;
   g_kt = &kt;
   g_launches = 0;
