@@ -230,6 +230,7 @@ class B200Device:
         self._seq: dict[str, int] = {}
         self._pinned: list = []  # pinned staging kept alive until transfer completion
         self._dispatch_lock = threading.Lock()  # one batched kernel at a time, in submission order
+        self._inflight: set = set()  # dispatch handles whose collector thread still runs
 
     # -- streams --------------------------------------------------------------
     def stream(self, name: str) -> int:
@@ -265,6 +266,10 @@ class B200Device:
             return r
 
     def free(self, region: DeviceRegion):
+        with self._lock:
+            busy = [h for h in self._inflight if region.region_id in h._rids]
+        for h in busy:  # a dispatch still reading / writing the region finishes first
+            h._event.wait()
         with self._lock:
             if self._regions.pop(region.region_id, None) is not None:
                 self._alloc_bytes -= region.capacity
@@ -349,6 +354,7 @@ class B200Device:
             raise DeviceError("device closed")
         self._check_dispatch(spec)
         h = DispatchHandle(spec.kind, len(spec.items))
+        h._rids = set(spec.reads) | set(spec.writes)
         t0 = time.monotonic()
 
         # Asynchronous like HostParallelDevice.dispatch (device.py:566-607): a
@@ -370,9 +376,14 @@ class B200Device:
                             r.state = READY
                     h.t_end = time.monotonic()
                     self._stats.dispatch(spec.kind, len(spec.items), h.t_end - t0)
+                    with self._lock:
+                        self._inflight.discard(h)
                     h._event.set()
 
-        threading.Thread(target=collect, name=f"luda-collect-{spec.kind}", daemon=True).start()
+        with self._lock:
+            self._inflight.add(h)
+        th = threading.Thread(target=collect, name=f"luda-collect-{spec.kind}", daemon=True)
+        th.start()
         return h
 
     def _run_items(self, spec: KernelSpec, h: DispatchHandle, on_item):
@@ -435,6 +446,10 @@ class B200Device:
         return region.state == state
 
     def synchronize(self):
+        with self._lock:
+            pending = list(self._inflight)
+        for h in pending:  # dispatches in flight finish before their regions can go away
+            h._event.wait()
         for s in self._streams.values():
             _native.check(self._L.luda_stream_sync(s))
         for _, pin in self._pinned:
