@@ -209,15 +209,16 @@ typedef struct {
   double t_ms[4];             /* H2D, lookup + scan, pack, D2H                     */
 } luda_get_result;
 /* Table.get (sst.py:342-368) for n keys (key i = keys[key_off[i] .. + key_len[i]],
- * host memory): on table table_of_key[i], or in the plan's store order when
- * table_of_key is NULL. Found keys longer than key_cap fail (LUDA_UNSUPPORTED).
+ * host memory; key_off NULL: n keys of key_len[0] bytes back to back): on table
+ * table_of_key[i], or in the plan's store order when table_of_key is NULL. Found keys longer than key_cap fail (LUDA_UNSUPPORTED).
  * Result arrays are owned by the table set and valid until its next get.
  * Synchronous on `stream`. */
 int luda_tables_get(luda_tables* t, const uint8_t* keys, uint64_t keys_bytes, const uint64_t* key_off,
                     const uint32_t* key_len, uint32_t n, const uint32_t* table_of_key, uint32_t key_cap,
                     luda_get_result* result, void* stream);
-/* The lookup kernel alone over device-resident keys (throughput measurement);
- * results stay on the device. Asynchronous on `stream`. */
+/* The lookup kernel alone over device-resident keys (throughput measurement;
+ * dev_key_off NULL: fixed-length keys as above); results stay on the device.
+ * Asynchronous on `stream`. */
 int luda_tables_lookup_dev(luda_tables* t, const uint8_t* dev_keys, const uint64_t* dev_key_off,
                            const uint32_t* dev_key_len, uint32_t n, const uint32_t* dev_table_of_key,
                            uint32_t key_cap, void* stream);

@@ -237,18 +237,21 @@ __device__ int table_get(const TabView& tv, uint32_t t, const Query& q, uint8_t*
   return block_seek(tv.arena + tv.baddr[b], tv.blen[b], tv.baddr[b], q, slot, cap, f);
 }
 
+// Per-lookup results, structure of arrays (each array D2H'd as is).
 struct GetOut {
-  uint32_t status;  // GetStatus
-  uint32_t table;   // table that answered (found) or failed
-  uint32_t klen, vlen;
-  uint64_t vaddr;
-  int64_t err_off;
+  uint32_t* status;  // GetStatus
+  uint32_t* table;   // table that answered (found) or failed
+  uint32_t* klen;    // found key length (0 otherwise)
+  uint32_t* vlen;    // found value length
+  uint64_t* vaddr;   // arena address of the value
+  int64_t* err_off;  // CorruptionError offset (G_E_CRC) or -1
+  unsigned int* first_fail;  // min index of a failing lookup (0xFFFFFFFF: none)
 };
 
 struct GetArgs {
   TabView tv;
   const uint8_t* keys;
-  const uint64_t* koff;
+  const uint64_t* koff;  // nullptr: fixed-length keys, key i at keys + i * klen[0]
   const uint32_t* klen;
   uint32_t n;
   const uint32_t* qtable;  // per-query table (Table.get mode) or nullptr (store order)
@@ -262,7 +265,7 @@ struct GetArgs {
   const uint64_t* rk_off;
   const uint32_t* rk_len;
   const uint64_t* rk_pfx;
-  GetOut* out;
+  GetOut out;
   uint8_t* slots;  // n × cap bytes: found keys
   uint32_t cap;
   uint32_t* sizes;  // [n] klen + vlen of found entries (packing), else 0
@@ -272,8 +275,13 @@ __global__ void __launch_bounds__(256) get_kernel(GetArgs a) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   Query q;
-  q.key = a.keys + a.koff[i];
-  q.len = a.klen[i];
+  if (a.koff) {
+    q.key = a.keys + a.koff[i];
+    q.len = a.klen[i];
+  } else {
+    q.len = a.klen[0];
+    q.key = a.keys + (uint64_t)i * q.len;
+  }
   q.pfx = be_prefix8(q.key, q.len);
   q.h = key_crc(q.key, q.len);
   uint8_t* slot = a.slots + (uint64_t)i * a.cap;
@@ -305,30 +313,30 @@ __global__ void __launch_bounds__(256) get_kernel(GetArgs a) {
       r = table_get(a.tv, t, q, slot, a.cap, f);
     }
   }
-  GetOut o;
-  o.status = (uint32_t)r;
-  o.table = t;
-  o.klen = r == G_FOUND ? f.klen : 0;
-  o.vlen = r == G_FOUND ? f.vlen : 0;
-  o.vaddr = f.vaddr;
-  o.err_off = f.off;
-  a.out[i] = o;
-  a.sizes[i] = o.klen + o.vlen;
+  const uint32_t kl = r == G_FOUND ? f.klen : 0, vl = r == G_FOUND ? f.vlen : 0;
+  a.out.status[i] = (uint32_t)r;
+  a.out.table[i] = t;
+  a.out.klen[i] = kl;
+  a.out.vlen[i] = vl;
+  a.out.vaddr[i] = f.vaddr;
+  a.out.err_off[i] = r == G_E_CRC ? f.off : -1;
+  if (r > G_FOUND) atomicMin(a.out.first_fail, i);
+  a.sizes[i] = kl + vl;
 }
 
 // Found key ∥ value of query i at packed + pos[i] (pos: exclusive scan of sizes).
-__global__ void __launch_bounds__(256) get_pack_kernel(const GetOut* out, const uint8_t* slots, uint32_t cap,
+__global__ void __launch_bounds__(256) get_pack_kernel(GetOut out, const uint8_t* slots, uint32_t cap,
                                                        const uint8_t* arena, const uint64_t* pos, uint32_t n,
                                                        uint8_t* packed) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = lane_id();
   if (warp >= n) return;
-  const GetOut o = out[warp];
-  if (o.status != G_FOUND) return;
+  if (out.status[warp] != G_FOUND) return;
+  const uint32_t kl = out.klen[warp], vl = out.vlen[warp];
   uint8_t* dst = packed + pos[warp];
   const uint8_t* ks = slots + (uint64_t)warp * cap;
-  for (uint32_t j = lane; j < o.klen; j += 32) dst[j] = ks[j];
-  const uint8_t* v = arena + o.vaddr;
-  for (uint32_t j = lane; j < o.vlen; j += 32) dst[o.klen + j] = v[j];
+  for (uint32_t j = lane; j < kl; j += 32) dst[j] = ks[j];
+  const uint8_t* v = arena + out.vaddr[warp];
+  for (uint32_t j = lane; j < vl; j += 32) dst[kl + j] = v[j];
 }
 
 // ---- table-set open ----------------------------------------------------------------

@@ -161,8 +161,10 @@ class DeviceTables:
         kb = (ctypes.c_uint8 * max(1, len(blob))).from_buffer_copy(blob + b"\0")
         res = GetResult()
         qt = _u32(tables) if tables is not None else None
-        st = self._L.luda_tables_get(self._h, kb, len(blob), _u64(offs), _u32(lens), n, qt, KEY_CAP,
-                                     ctypes.byref(res), self._stream)
+        fixed = len(set(lens)) == 1  # one key length: no per-key offsets / lengths to ship
+        st = self._L.luda_tables_get(self._h, kb, len(blob), None if fixed else _u64(offs),
+                                     _u32(lens[:1] if fixed else lens), n, qt, KEY_CAP, ctypes.byref(res),
+                                     self._stream)
         return st, res
 
     def _decode(self, st, res, n, store, errors_mode):
