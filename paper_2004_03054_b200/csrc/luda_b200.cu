@@ -389,14 +389,16 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& s
     m.a_run_base = abase; m.b_run_base = bbase;
     m.err_order = d_err_order;  // order errors are reported for original runs only
     m.ra.resolve = resolve;
+    uint32_t* tile_cnt = nullptr;
+    Rec<W>* seg_out = out;
     if (resolve) {
       m.ra = ra_final;
       m.ra.resolve = true;
-      GET(lb, uint64_t, ntiles, true);
-      GET(ctr, unsigned int, 1, true);
-      m.lb = lb;
-      m.tile_ctr = ctr;
-      m.n_out = d_nout;
+      GET(tc, uint32_t, ntiles, false);
+      tile_cnt = tc;
+      m.tile_cnt = tc;
+      seg_out = nxt;  // tile segments; the final pass never reads `nxt`
+      m.out = seg_out;
     }
     if (!first_pass) {
       GET(sink, unsigned long long, 1, true);
@@ -405,7 +407,18 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& s
     if (resolve) KT_START(1, st);
     merge_kernel<W><<<(unsigned)ntiles, kMergeThreads, smem, st>>>(m);
     ++g_launches;
-    if (resolve) KT_STOP(1, st);
+    if (resolve) {
+      // tile counts → segment bases → packed survivors in `out`; n_out = total
+      GET(lo, uint64_t, ntiles + 1, false);
+      const uint64_t nt = std::max<uint64_t>(1, (ntiles + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
+      GET(lb, uint64_t, nt, true);
+      GET(ctr, unsigned int, 1, true);
+      scan_excl_kernel<uint32_t><<<(unsigned)nt, kScanThreads, 0, st>>>(tile_cnt, ntiles, lo, lb, ctr);
+      merge_densify_kernel<W><<<(unsigned)ntiles, 256, 0, st>>>(seg_out, lo, ntiles, out);
+      g_launches += 2;
+      CK(cudaMemcpyAsync(d_nout, lo + ntiles, 8, cudaMemcpyDeviceToDevice, st));
+      KT_STOP(1, st);
+    }
     CK(cudaGetLastError());
     return LUDA_OK;
   };
@@ -682,6 +695,8 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
 
 constexpr int kRetryVar = 100;  // internal: a fixed-K job met another key length → rerun as a var job
 
+constexpr uint64_t merge_tile_slack = kMergeTile;
+
 template <int W>
 int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_job_result* res, uint32_t K,
               uint32_t nblk, const BlockTable& bt, const uint32_t* d_file_blk_base,
@@ -719,7 +734,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   GET(d_bad, uint32_t, jd->n_files, false);
   CK(cudaMemcpyAsync(d_for, first_of_run.data(), 4ull * jd->n_files, cudaMemcpyHostToDevice, st));
   for (int attempt = 0; attempt < 2; ++attempt) {
-    X = scratch.get<Rec<W>>((uint64_t)nw * seg_cap, false);
+    X = scratch.get<Rec<W>>((uint64_t)nw * seg_cap + merge_tile_slack, false);
     if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
     CK(cudaMemsetAsync(errs, 0xFF, 16, st));
     CK(cudaMemsetAsync(d_max, 0, 8, st));
@@ -820,7 +835,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
       runs.push_back({fbase[run_first[r]], fbase[run_first[r + 1]] - fbase[run_first[r]]});
     }
   }
-  GET(Y, Rec<W>, n_in, false);
+  GET(Y, Rec<W>, n_in + merge_tile_slack, false);  // + a tile: the resolve pass writes whole tile segments
   GET(S, Rec<W>, n_in, false);
   GET(merr, unsigned long long, 2, false);
   uint64_t n_out = 0;

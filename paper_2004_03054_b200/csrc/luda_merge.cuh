@@ -225,9 +225,7 @@ struct MergeArgs {
   unsigned long long* err_order;    // min(position in decoded array of the later element)
   // resolve pass only
   ResolveArgs ra;
-  uint64_t* lb;
-  unsigned int* tile_ctr;
-  unsigned long long* n_out;
+  uint32_t* tile_cnt;     // resolve pass: survivors of each tile, written at out + tile * kMergeTile
 };
 
 // Shared-memory tile layout: 16 bytes of padding after every 8 records. A
@@ -250,19 +248,11 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   auto SR = [&](uint32_t i) -> const Rec<W>& { return *reinterpret_cast<const Rec<W>*>(Sb + mrg_off<W>(i)); };
   uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + mrg_bytes<W>(kMergeTile));
   uint16_t* comp = perm;  // the resolve pass compacts from registers into the same array
-  __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[kMergeThreads / 32];
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_total;
   const uint32_t tid = threadIdx.x;
-  uint64_t tile;
-  if (m.ra.resolve) {
-    if (tid == 0) s_tile = atomicAdd(m.tile_ctr, 1u);
-    __syncthreads();
-    tile = s_tile;
-  } else {
-    tile = blockIdx.x;
-  }
+  const uint64_t tile = blockIdx.x;
   if (tile >= m.ntiles) return;
   const uint64_t d0 = tile * kMergeTile;
   const uint64_t d1 = (d0 + kMergeTile < m.na + m.nb) ? d0 + kMergeTile : m.na + m.nb;
@@ -404,7 +394,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     }
     return;
   }
-  // ---- CTA exclusive scan of keep counts + decoupled look-back over tiles ----
+  // ---- CTA exclusive scan of keep counts; the tile's survivors go to its own
+  // segment (out + tile * kMergeTile) and merge_densify_kernel packs the
+  // segments once every count is known — no look-back between tiles ----
   const uint32_t lane = lane_id(), wid = tid >> 5;
   const uint32_t incl = warp_incl_scan<uint32_t>(cnt);
   if (lane == 31) s_warp[wid] = incl;
@@ -414,13 +406,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     const uint32_t vi = warp_incl_scan<uint32_t>(v);
     if (lane < kMergeThreads / 32) s_warp[lane] = vi - v;
     const uint32_t total = __shfl_sync(0xFFFFFFFFu, vi, 31);
-    if (lane == 0) lb_publish(m.lb, tile, kLbAgg, total);
-    const uint64_t ex = lb_exclusive(m.lb, tile);
     if (lane == 0) {
-      lb_publish(m.lb, tile, kLbInc, ex + total);
-      s_base = ex;
+      s_base = tile * (uint64_t)kMergeTile;
       s_total = total;
-      if (tile + 1 == m.ntiles) *m.n_out = ex + total;
+      m.tile_cnt[tile] = total;
     }
   }
   __syncthreads();
@@ -442,6 +431,28 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
       for (uint32_t i = tid; i < tot * RW; i += kMergeThreads)
         go[i] = *reinterpret_cast<const uint64_t*>(Sb + mrg_off<W>(comp[i / RW]) + 8 * (i % RW));
     }
+  }
+}
+
+// Packs the resolve pass's tile segments: tile t's cnt survivors (at
+// seg + t * kMergeTile) to out + lo[t] (lo: exclusive scan of the counts).
+template <int W>
+__global__ void __launch_bounds__(256) merge_densify_kernel(const Rec<W>* seg, const uint64_t* lo, uint64_t ntiles,
+                                                            Rec<W>* out) {
+  const uint64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  const uint64_t base = lo[t], cnt = lo[t + 1] - base;
+  const Rec<W>* src = seg + t * (uint64_t)kMergeTile;
+  constexpr int R16 = sizeof(Rec<W>) / 16;
+  if (R16 * 16 == sizeof(Rec<W>) && (base * sizeof(Rec<W>)) % 16 == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(out + base);
+    for (uint64_t i = threadIdx.x; i < cnt * R16; i += blockDim.x) d4[i] = s4[i];
+  } else {
+    constexpr int RW = sizeof(Rec<W>) / 8;
+    const uint64_t* s8 = reinterpret_cast<const uint64_t*>(src);
+    uint64_t* d8 = reinterpret_cast<uint64_t*>(out + base);
+    for (uint64_t i = threadIdx.x; i < cnt * RW; i += blockDim.x) d8[i] = s8[i];
   }
 }
 
