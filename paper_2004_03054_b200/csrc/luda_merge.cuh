@@ -6,16 +6,18 @@
 // Version.covers_below is false — SPEC D12, version.py:122-128).
 //
 // Runs are merged pairwise by MERGE PATH: a partition kernel places every
-// 2048-output tile boundary on the merge diagonal by binary search (ties go
-// to the earlier run, so the merge is stable like heapq.merge over runs in
+// kMergeTile-output tile boundary on the merge diagonal by binary search (ties
+// go to the earlier run, so the merge is stable like heapq.merge over runs in
 // priority order); each CTA loads its A and B slices into shared memory,
-// every thread merges 8 outputs after a local diagonal search, and the
-// merged permutation is written back coalesced. The last pass fuses version
-// resolution: keep flags (new user key, tombstone rule, optional key range)
-// are scanned across the CTA and across tiles by decoupled look-back, and the
-// survivors are written compacted in one pass. Every loaded slice is also
-// checked for strict ascending order (keys.py order); violations are reported
-// as the run position so the host can raise OrderingError.
+// every thread merges kMergeItems outputs after a local diagonal search, and
+// the merged permutation is written back coalesced. The last pass fuses
+// version resolution: keep flags (new user key, tombstone rule, optional key
+// range) are scanned across the CTA and the tile's survivors are written
+// compacted into the tile's own segment; a scan of the tile counts and
+// merge_densify_kernel then pack the segments (no dependency between tiles).
+// Every loaded slice is also checked for strict ascending order (keys.py
+// order); violations are reported as the run position so the host can raise
+// OrderingError.
 #pragma once
 #include "luda_rec.cuh"
 
@@ -260,8 +262,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   uint64_t b0 = d0 - a0, b1 = d1 - a1;
   if (a1 < a0 || b1 < b0) {
     // Split points are monotone only over sorted runs: an unsorted run is an
-    // OrderingError, never an out-of-bounds tile load. The tile is emptied (the
-    // resolve pass still publishes its look-back entry so later tiles proceed).
+    // OrderingError, never an out-of-bounds tile load. The tile is emptied (its
+    // survivor count is 0).
     if (tid == 0) atomicMin(m.err_order, (unsigned long long)(m.a_run_base + a0));
     a1 = a0;
     b1 = b0;
