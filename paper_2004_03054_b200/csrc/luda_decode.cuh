@@ -672,12 +672,6 @@ __device__ uint64_t dec_var_block(const DecodeArgs<W>& a, uint32_t b, uint64_t a
               for (int q = 7; q >= 0; --q) tr = (tr << 8) | kbuf[lr + q];
               rec.t = ~tr;
               rec.h = handle_pack(addr + pos + u, vl);
-#ifdef LUDA_VAR_PRINTF
-              printf("var b=%u n=%llu sh=%llu u=%llu lr=%u k6=%016llx k7=%016llx k8=%016llx t=%016llx\n", b,
-                     (unsigned long long)n, (unsigned long long)sh, (unsigned long long)u, lr,
-                     (unsigned long long)rec.k[6], (unsigned long long)rec.k[7], (unsigned long long)rec.k[8],
-                     (unsigned long long)rec.t);
-#endif
               a.out[base + n] = rec;
             }
           }
