@@ -718,7 +718,10 @@ __global__ void __launch_bounds__(kEncWarps * 32, 1) encode_kernel(EncodeArgs<W>
 }
 
 // ---- per-SST filter + index + footer -----------------------------------------------------
-constexpr int kMetaThreads = 512;
+#ifndef LUDA_META_THREADS
+#define LUDA_META_THREADS 896
+#endif
+constexpr int kMetaThreads = LUDA_META_THREADS;
 // keys in flight per thread in the bloom loop (var records: 4, else they spill)
 template <int W>
 __host__ __device__ constexpr int meta_unroll() { return W <= 4 ? 8 : 4; }
