@@ -29,8 +29,14 @@ namespace luda {
 constexpr uint32_t kChainEnd = 0xFFFFFFFFu;
 
 // ---- block jumps ----------------------------------------------------------------
-constexpr int kJumpThreads = 256;
-constexpr int kJumpTile = 4096;
+#ifndef LUDA_JUMP_THREADS
+#define LUDA_JUMP_THREADS 512
+#endif
+#ifndef LUDA_JUMP_TILE
+#define LUDA_JUMP_TILE 4096
+#endif
+constexpr int kJumpThreads = LUDA_JUMP_THREADS;
+constexpr int kJumpTile = LUDA_JUMP_TILE;
 
 template <int W>
 struct BlockJumpArgs {
