@@ -472,3 +472,42 @@ def test_structural_error_before_later_crc_error(dev):
         O.reference_compact(lower + upper)
     with pytest.raises(FormatError, match="bad probe count"):
         gpu_compact(dev, job, lower, upper, {})
+
+
+def test_spec_a1_randomized_configs(dev):
+    """SPEC A1: 800 more random jobs (with the 200 golden ones:
+    1,000) — 1-6 L0 SSTs, 64 B - 4 KiB values, 0-20 % tombstones — each under a
+    random store configuration (block size, restart interval, bits per key, SST
+    target), byte-compared with the oracle."""
+    rng = random.Random(0x5EC1A)
+    bad = []
+    for s in range(1000, 1800):
+        job = jobgen.spec_a1(s)
+        cfg = dict(block_size=rng.choice([512, 1024, 4096, 8192]), restart_interval=rng.choice([1, 2, 3, 16, 32]),
+                   bits_per_key=rng.choice([1, 7, 10, 13]),
+                   sst_size_target=rng.choice([8, 32, 128, 1024, 4096]) * 1024)
+        blk = {k: cfg[k] for k in ("block_size", "restart_interval")}
+        lower, upper = jobgen.materialize(job, **blk)
+        want = O.reference_compact(lower + upper, deeper=job.deeper, **cfg)
+        got = gpu_compact(dev, job, lower, upper, cfg)
+        if [g[0] for g in got] != [w[0] for w in want] or [g[1:] for g in got] != [w[1:] for w in want]:
+            bad.append((s, cfg))
+    assert not bad, bad[:5]
+
+
+def test_varkey_randomized_configs(dev):
+    """Generic-length keys (0-64 B mixed in one job, prefix-rich) under random
+    store configurations: 150 jobs byte-compared with the oracle."""
+    rng = random.Random(0x7A57)
+    bad = []
+    for s in range(100, 250):
+        job = jobgen.varkey(s, max_len=64, n_space=rng.randint(50, 400))
+        cfg = dict(block_size=rng.choice([512, 1024, 4096]), restart_interval=rng.choice([1, 3, 16]),
+                   bits_per_key=rng.choice([7, 10, 13]), sst_size_target=rng.choice([4, 16, 64]) * 1024)
+        blk = {k: cfg[k] for k in ("block_size", "restart_interval")}
+        lower, upper = jobgen.materialize(job, **blk)
+        want = O.reference_compact(lower + upper, deeper=job.deeper, **cfg)
+        got = gpu_compact(dev, job, lower, upper, cfg)
+        if [g[0] for g in got] != [w[0] for w in want] or [g[1:] for g in got] != [w[1:] for w in want]:
+            bad.append((s, cfg))
+    assert not bad, bad[:5]
