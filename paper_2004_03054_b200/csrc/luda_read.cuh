@@ -271,7 +271,10 @@ struct GetArgs {
   uint32_t* sizes;  // [n] klen + vlen of found entries (packing), else 0
 };
 
-__global__ void __launch_bounds__(256) get_kernel(GetArgs a) {
+#ifndef LUDA_GET_MINB
+#define LUDA_GET_MINB 1
+#endif
+__global__ void __launch_bounds__(256, LUDA_GET_MINB) get_kernel(GetArgs a) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   Query q;
