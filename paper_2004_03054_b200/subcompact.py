@@ -30,7 +30,7 @@ import ctypes
 import struct
 from dataclasses import dataclass
 
-from . import _native
+from . import _native, errors
 from .version import CompactionJob, user_key_of
 
 FOOTER = struct.Struct("<IIIIQ")
@@ -197,16 +197,23 @@ def allgather_bytes(payload: bytes, world: int, group=None) -> list:
     import torch.distributed as dist
     backend = dist.get_backend(group)
     if backend == "nccl":
-        L = _native.lib(torch.cuda.current_device())
-        comm = _luda_comm(L, world, group)
         n = len(payload)
         send = torch.frombuffer(bytearray(payload), dtype=torch.uint8).cuda()
-        recv = torch.empty(world * n, dtype=torch.uint8, device="cuda")
-        s = torch.cuda.current_stream()
-        _native.check(L.luda_allgather_splitters(comm, send.data_ptr(), recv.data_ptr(), n, s.cuda_stream))
-        s.synchronize()
-        blob = recv.cpu().numpy().tobytes()
-        return [blob[i * n:(i + 1) * n] for i in range(world)]
+        try:
+            L = _native.lib(torch.cuda.current_device())
+            comm = _luda_comm(L, world, group)
+            recv = torch.empty(world * n, dtype=torch.uint8, device="cuda")
+            s = torch.cuda.current_stream()
+            _native.check(L.luda_allgather_splitters(comm, send.data_ptr(), recv.data_ptr(), n, s.cuda_stream))
+            s.synchronize()
+            blob = recv.cpu().numpy().tobytes()
+            return [blob[i * n:(i + 1) * n] for i in range(world)]
+        except errors.DeviceError as exc:  # the same NCCL collective through the process group instead
+            import warnings
+            warnings.warn(f"luda_allgather_splitters unavailable ({exc}); all-gather via torch.distributed")
+            outs = [torch.empty_like(send) for _ in range(world)]
+            dist.all_gather(outs, send, group=group)
+            return [bytes(o.cpu().numpy().tobytes()) for o in outs]
     t = torch.frombuffer(bytearray(payload), dtype=torch.uint8)
     outs = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(outs, t, group=group)
