@@ -166,3 +166,27 @@ def test_read_path_over_compaction_output_in_place(dev):
     finally:
         dev.release(res)
         dev.free(region)
+
+
+def test_read_path_randomized_configs(dev):
+    """Table.get over 120 random table sets (SPEC-A1 and mixed-length-key
+    files under random block size / restart interval / bits per key), with
+    present, absent, near-miss and prefix queries: every result equal to the
+    oracle's, and the per-table counters too."""
+    from paper_2004_03054_b200.read import DeviceTables
+    rng = random.Random(0x6E7)
+    for s in range(120):
+        job = jobgen.spec_a1(3000 + s) if s % 2 == 0 else jobgen.varkey(500 + s, max_len=48, n_space=200)
+        cfg = dict(block_size=rng.choice([256, 1024, 4096]), restart_interval=rng.choice([1, 2, 5, 16]),
+                   bits_per_key=rng.choice([1, 4, 10, 16]))
+        lower, upper = jobgen.materialize(job, **cfg)
+        files = lower + upper
+        c = {"files": files, "mode": "table"}
+        qs = []
+        for t, f in enumerate(files):
+            qs += [(t, q) for q in RC._queries(rng, RC._user_keys(f), 40)]
+        c["queries"] = qs
+        want, want_ctr = oracle_run(c)
+        got, got_ctr = run_device(dev, c)
+        assert got == want, (s, cfg)
+        assert got_ctr == want_ctr, (s, cfg)
