@@ -329,14 +329,14 @@ KeyBound make_bound(const uint8_t* key, uint32_t klen, uint32_t L, bool lower, b
 }
 
 // Var jobs (luda_rec.cuh): the bound is represented exactly — padded to
-// 8 kVarW - 1 bytes plus its length byte — so comparisons are exact.
-KeyBound make_bound_var(const uint8_t* key, uint32_t klen, bool lower, bool closed) {
+// 8 W - 1 bytes plus its length byte — so comparisons are exact.
+KeyBound make_bound_var(const uint8_t* key, uint32_t klen, bool lower, bool closed, uint32_t W) {
   KeyBound b{};
   b.present = 1;
-  uint8_t pad[8 * kVarW] = {0};
-  memcpy(pad, key, std::min<uint32_t>(klen, kVarMaxLen));
-  pad[8 * kVarW - 1] = (uint8_t)klen;
-  for (int w = 0; w < kVarW; ++w) {
+  uint8_t pad[8 * kVarWLong] = {0};
+  memcpy(pad, key, std::min<uint32_t>(klen, 8 * W - 1));
+  pad[8 * W - 1] = (uint8_t)klen;
+  for (uint32_t w = 0; w < W; ++w) {
     uint64_t v = 0;
     for (int i = 0; i < 8; ++i) v = (v << 8) | pad[8 * w + i];
     b.k[w] = v;
@@ -366,7 +366,7 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& s
     return LUDA_OK;
   }
   bool first_pass = true;
-  const size_t smem = mrg_bytes<W>(kMergeTile) + 2 * kMergeTile;
+  const size_t smem = mrg_bytes<W>(merge_tile_n<W>()) + 2 * merge_tile_n<W>();
   CK(cudaFuncSetAttribute(merge_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   Rec<W>* cur = X;
   Rec<W>* nxt = Y;
@@ -378,7 +378,7 @@ int merge_runs(cudaStream_t st, Scratch& scratch, Rec<W>* X, const RunView<W>& s
   };
   auto launch = [&](const RunView<W>& A, uint64_t na, const RunView<W>& B, uint64_t nb, Rec<W>* out, uint64_t abase,
                     uint64_t bbase, bool resolve) -> int {
-    const uint64_t ntiles = (na + nb + kMergeTile - 1) / kMergeTile;
+    const uint64_t ntiles = (na + nb + merge_tile_n<W>() - 1) / merge_tile_n<W>();
     GET(split, uint64_t, 3 * (ntiles + 1), false);
     const bool warp_mode = ntiles + 1 <= 32ull * g_num_sms;
     merge_partition_kernel<W><<<(unsigned)(warp_mode ? (ntiles + 1 + 7) / 8 : (ntiles + 1 + 255) / 256), 256, 0, st>>>(
@@ -512,7 +512,7 @@ struct EmitParams {
   uint64_t sst_target;
   uint32_t min_entry;         // lower bound of one encoded entry (sizes the planner halo)
   uint64_t file_entries = 0;  // > 0: cut an SST every file_entries entries instead of by size
-  bool var = false;           // generic-length keys (W = kVarW records)
+  bool var = false;           // generic-length keys (W = kVarW / kVarWLong records)
 };
 
 // Plan + encode the survivors `S[0..n)` whose values live in `varena`.
@@ -644,7 +644,7 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(bigs, uint32_t, big_words + 16, true);
   GET(d_soff, uint64_t, nsst, false);
   CK(cudaMemcpyAsync(d_soff, soff.data(), 8ull * nsst, cudaMemcpyHostToDevice, st));
-  const uint32_t key_slot = p.var ? 8 * kVarW + 8 : p.K;
+  const uint32_t key_slot = p.var ? 8 * W + 8 : p.K;
   GET(d_keys, uint8_t, 2ull * nsst * key_slot, false);
   GET(d_klen, uint32_t, 2ull * nsst, false);
   // ---- encode data blocks ----
@@ -693,9 +693,10 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   return LUDA_OK;
 }
 
-constexpr int kRetryVar = 100;  // internal: a fixed-K job met another key length → rerun as a var job
+constexpr int kRetryVar = 100;   // internal: a fixed-K job met another key length → rerun as a var job
+constexpr int kRetryLong = 101;  // internal: a var job met a user key > 71 bytes → rerun with kVarWLong records
 
-constexpr uint64_t merge_tile_slack = kMergeTile;
+constexpr uint64_t merge_tile_slack = 2048;  // >= merge_tile_n<W>() for every W
 
 template <int W>
 int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_job_result* res, uint32_t K,
@@ -779,6 +780,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
       uint32_t foff = 0;
       CK(cudaMemcpy(&foff, bt.foff + b, 4, cudaMemcpyDeviceToHost));
       if (!ref && code == B_KEYLEN && !var) return kRetryVar;
+      if (!ref && code == B_KEYLONG && W == kVarW) return kRetryLong;  // a user key of 72..255 bytes
       if (!ref) return fail(LUDA_UNSUPPORTED, block_msg(code));
       if (code == B_CRC) return fail(LUDA_CORRUPT, block_msg(code), foff);
       return fail(LUDA_FORMAT, block_msg(code));
@@ -799,11 +801,13 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     const uint8_t* kp = jd->deeper_keys;
     for (uint32_t i = 0; i < jd->n_deeper; ++i) {
       const uint32_t llo = jd->deeper_lens[2 * i], lhi = jd->deeper_lens[2 * i + 1];
-      if (var && (llo > kVarMaxLen || lhi > kVarMaxLen))
-        return fail(LUDA_UNSUPPORTED, "key-range bound longer than 71 bytes");
-      bounds.push_back(var ? make_bound_var(kp, llo, true, true) : make_bound(kp, llo, L, true, true));
+      if (var && (llo > var_maxlen<W>() || lhi > var_maxlen<W>())) {
+        if (W == kVarW) return kRetryLong;
+        return fail(LUDA_UNSUPPORTED, "key-range bound longer than 255 bytes");
+      }
+      bounds.push_back(var ? make_bound_var(kp, llo, true, true, W) : make_bound(kp, llo, L, true, true));
       kp += llo;
-      bounds.push_back(var ? make_bound_var(kp, lhi, false, true) : make_bound(kp, lhi, L, false, true));
+      bounds.push_back(var ? make_bound_var(kp, lhi, false, true, W) : make_bound(kp, lhi, L, false, true));
       kp += lhi;
     }
   }
@@ -815,13 +819,16 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   }
   ra.deeper = d_bounds;
   ra.n_deeper = jd->n_deeper;
-  if (var && ((jd->range_lo && jd->range_lo_len > kVarMaxLen) || (jd->range_hi && jd->range_hi_len > kVarMaxLen)))
-    return fail(LUDA_UNSUPPORTED, "key-range bound longer than 71 bytes");
+  if (var && ((jd->range_lo && jd->range_lo_len > var_maxlen<W>()) ||
+              (jd->range_hi && jd->range_hi_len > var_maxlen<W>()))) {
+    if (W == kVarW) return kRetryLong;
+    return fail(LUDA_UNSUPPORTED, "key-range bound longer than 255 bytes");
+  }
   if (jd->range_lo)
-    ra.range_lo = var ? make_bound_var(jd->range_lo, jd->range_lo_len, true, true)
+    ra.range_lo = var ? make_bound_var(jd->range_lo, jd->range_lo_len, true, true, W)
                       : make_bound(jd->range_lo, jd->range_lo_len, L, true, true);
   if (jd->range_hi)
-    ra.range_hi = var ? make_bound_var(jd->range_hi, jd->range_hi_len, false, false)
+    ra.range_hi = var ? make_bound_var(jd->range_hi, jd->range_hi_len, false, false, W)
                       : make_bound(jd->range_hi, jd->range_hi_len, L, false, false);
   ra.resolve = true;
   // runs in merge-priority order; a run with a violated file seam is split into per-file runs
@@ -1311,7 +1318,14 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
       var = true;
     }
   }
-  if (var) rc = compact_w<kVarW>(st, scratch, jd, res, 8 * kVarW + 8, nblk, bt, d_fbb, pev, true);
+  if (var) {
+    rc = compact_w<kVarW>(st, scratch, jd, res, 8 * kVarW + 8, nblk, bt, d_fbb, pev, true);
+    if (rc == kRetryLong) {
+      luda_job_release(res);
+      memset(res, 0, sizeof(*res));
+      rc = compact_w<kVarWLong>(st, scratch, jd, res, 8 * kVarWLong + 8, nblk, bt, d_fbb, pev, true);
+    }
+  }
   {
     const int crc_rc = deferred_crc_check();  // a filter / index CRC error outranks every later error
     if (crc_rc) rc = crc_rc;

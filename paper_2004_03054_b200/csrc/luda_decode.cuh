@@ -48,7 +48,7 @@ enum BlockCode : uint32_t {
   B_TRAILING = 7,       // trailing garbage in block entries
   B_KEYLEN = 8,         // (unsupported) key length differs from the job's K
   B_VALUE_BIG = 9,      // (unsupported) value length >= 2^24 or arena offset >= 2^40
-  B_KEYLONG = 10,       // (unsupported) user key longer than kVarMaxLen (71) bytes
+  B_KEYLONG = 10,       // (unsupported) user key longer than the var record holds (71 / 255 bytes)
 };
 
 // Paired warps: a PARSE warp (producer + walk + records) and a CRC warp share
@@ -647,7 +647,7 @@ __device__ uint64_t dec_var_block(const DecodeArgs<W>& a, uint32_t b, uint64_t a
             break;
           }
           const uint64_t ke = sh + u;
-          if (ke < 8 || ke - 8 > kVarMaxLen) unsup = unsup ? unsup : (uint32_t)B_KEYLONG;
+          if (ke < 8 || ke - 8 > var_maxlen<W>()) unsup = unsup ? unsup : (uint32_t)B_KEYLONG;
           if (vl > kMaxValueLen) unsup = unsup ? unsup : (uint32_t)B_VALUE_BIG;
           if (!unsup) {
             for (uint32_t j = 0; j < (uint32_t)u; ++j) kbuf[sh + j] = d[pos + j];

@@ -757,7 +757,7 @@ struct MetaArgs {
   const uint64_t* scratch_off; // per SST word offset into scratch (or ~0)
   uint8_t* sst_keys;           // [nsst][2][key_slot]
   uint32_t* sst_key_len;       // [nsst][2] internal key lengths
-  uint32_t key_slot;           // bytes per key slot (K, or 8 kVarW + 8 for var jobs)
+  uint32_t key_slot;           // bytes per key slot (K, or 8 W + 8 for var jobs)
   bool var;
   const uint64_t* blk_ipos;    // var jobs: index-entry offsets (luda_plan.cuh), else nullptr
 };

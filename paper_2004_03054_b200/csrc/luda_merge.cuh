@@ -6,10 +6,10 @@
 // Version.covers_below is false — SPEC D12, version.py:122-128).
 //
 // Runs are merged pairwise by MERGE PATH: a partition kernel places every
-// kMergeTile-output tile boundary on the merge diagonal by binary search (ties
+// merge_tile_n<W>()-output tile boundary on the merge diagonal by binary search (ties
 // go to the earlier run, so the merge is stable like heapq.merge over runs in
 // priority order); each CTA loads its A and B slices into shared memory,
-// every thread merges kMergeItems outputs after a local diagonal search, and
+// every thread merges merge_items<W>() outputs after a local diagonal search, and
 // the merged permutation is written back coalesced. The last pass fuses
 // version resolution: keep flags (new user key, tombstone rule, optional key
 // range) are scanned across the CTA and the tile's survivors are written
@@ -30,11 +30,19 @@ namespace luda {
 #define LUDA_MERGE_ITEMS 6
 #endif
 constexpr int kMergeThreads = LUDA_MERGE_THREADS;
-constexpr int kMergeItems = LUDA_MERGE_ITEMS;
-constexpr int kMergeTile = kMergeThreads * kMergeItems;
+// Outputs per thread: fewer for the long var records so a tile still fits
+// shared memory (272-byte records).
+template <int W>
+__host__ __device__ constexpr int merge_items() {
+  return W > kVarW ? 2 : LUDA_MERGE_ITEMS;
+}
+template <int W>
+__host__ __device__ constexpr int merge_tile_n() {
+  return kMergeThreads * merge_items<W>();
+}
 
 struct KeyBound {
-  uint64_t k[kVarW];
+  uint64_t k[kVarWLong];
   uint32_t incl;
   uint32_t present;
 };
@@ -186,7 +194,7 @@ __global__ void merge_partition_kernel(RunView<W> A, uint64_t na, RunView<W> B, 
   const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t t = warp_mode ? gt >> 5 : gt;
   if (t > ntiles) return;  // warp-uniform in warp mode
-  uint64_t diag = t * (uint64_t)kMergeTile;
+  uint64_t diag = t * (uint64_t)merge_tile_n<W>();
   if (diag > na + nb) diag = na + nb;
   const uint64_t a = warp_mode ? merge_split_warp(A, na, B, nb, diag) : merge_split(A, na, B, nb, diag);
   if (!warp_mode || (threadIdx.x & 31u) == 0) {
@@ -227,7 +235,7 @@ struct MergeArgs {
   unsigned long long* err_order;    // min(position in decoded array of the later element)
   // resolve pass only
   ResolveArgs ra;
-  uint32_t* tile_cnt;     // resolve pass: survivors of each tile, written at out + tile * kMergeTile
+  uint32_t* tile_cnt;     // resolve pass: survivors of each tile, written at out + tile * merge_tile_n<W>()
 };
 
 // Shared-memory tile layout: 16 bytes of padding after every 8 records. A
@@ -248,7 +256,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* Sb = smem_raw;
   auto SR = [&](uint32_t i) -> const Rec<W>& { return *reinterpret_cast<const Rec<W>*>(Sb + mrg_off<W>(i)); };
-  uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + mrg_bytes<W>(kMergeTile));
+  uint16_t* perm = reinterpret_cast<uint16_t*>(smem_raw + mrg_bytes<W>(merge_tile_n<W>()));
   uint16_t* comp = perm;  // the resolve pass compacts from registers into the same array
   __shared__ uint32_t s_warp[kMergeThreads / 32];
   __shared__ unsigned long long s_base;
@@ -256,8 +264,8 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   const uint32_t tid = threadIdx.x;
   const uint64_t tile = blockIdx.x;
   if (tile >= m.ntiles) return;
-  const uint64_t d0 = tile * kMergeTile;
-  const uint64_t d1 = (d0 + kMergeTile < m.na + m.nb) ? d0 + kMergeTile : m.na + m.nb;
+  const uint64_t d0 = tile * merge_tile_n<W>();
+  const uint64_t d1 = (d0 + merge_tile_n<W>() < m.na + m.nb) ? d0 + merge_tile_n<W>() : m.na + m.nb;
   uint64_t a0 = m.split[tile], a1 = m.split[tile + 1];
   uint64_t b0 = d0 - a0, b1 = d1 - a1;
   if (a1 < a0 || b1 < b0) {
@@ -303,10 +311,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     if (nb_t > 0 && b0 > 0 && rec_cmp(m.B.at_near(b0 - 1, sb), SR(na_t)) >= 0)
       atomicMin(m.err_order, (unsigned long long)(m.b_run_base + b0));
   }
-  // ---- per-thread merge of kMergeItems outputs (heads kept in registers) ----
-  const uint32_t p0 = tid * kMergeItems;
+  // ---- per-thread merge of merge_items<W>() outputs (heads kept in registers) ----
+  const uint32_t p0 = tid * merge_items<W>();
   uint32_t keep_bits = 0, cnt = 0;
-  uint16_t my_perm[kMergeItems];
+  uint16_t my_perm[merge_items<W>()];
   if (p0 < nt) {
     uint32_t lo = p0 > nb_t ? p0 - nb_t : 0;
     uint32_t hi = p0 < na_t ? p0 : na_t;
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
       }
     }
 #pragma unroll
-    for (int k = 0; k < kMergeItems; ++k) {
+    for (int k = 0; k < merge_items<W>(); ++k) {
       const uint32_t p = p0 + k;
       if (p < nt) {
         bool takeA;
@@ -397,7 +405,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     return;
   }
   // ---- CTA exclusive scan of keep counts; the tile's survivors go to its own
-  // segment (out + tile * kMergeTile) and merge_densify_kernel packs the
+  // segment (out + tile * merge_tile_n<W>()) and merge_densify_kernel packs the
   // segments once every count is known — no look-back between tiles ----
   const uint32_t lane = lane_id(), wid = tid >> 5;
   const uint32_t incl = warp_incl_scan<uint32_t>(cnt);
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
     if (lane < kMergeThreads / 32) s_warp[lane] = vi - v;
     const uint32_t total = __shfl_sync(0xFFFFFFFFu, vi, 31);
     if (lane == 0) {
-      s_base = tile * (uint64_t)kMergeTile;
+      s_base = tile * (uint64_t)merge_tile_n<W>();
       s_total = total;
       m.tile_cnt[tile] = total;
     }
@@ -417,7 +425,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
   __syncthreads();
   uint32_t w = s_warp[wid] + incl - cnt;
 #pragma unroll
-  for (int k = 0; k < kMergeItems; ++k)
+  for (int k = 0; k < merge_items<W>(); ++k)
     if (keep_bits & (1u << k)) comp[w++] = my_perm[k];
   __syncthreads();
   {
@@ -437,14 +445,14 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(MergeArgs<W> m) {
 }
 
 // Packs the resolve pass's tile segments: tile t's cnt survivors (at
-// seg + t * kMergeTile) to out + lo[t] (lo: exclusive scan of the counts).
+// seg + t * merge_tile_n<W>()) to out + lo[t] (lo: exclusive scan of the counts).
 template <int W>
 __global__ void __launch_bounds__(256) merge_densify_kernel(const Rec<W>* seg, const uint64_t* lo, uint64_t ntiles,
                                                             Rec<W>* out) {
   const uint64_t t = blockIdx.x;
   if (t >= ntiles) return;
   const uint64_t base = lo[t], cnt = lo[t + 1] - base;
-  const Rec<W>* src = seg + t * (uint64_t)kMergeTile;
+  const Rec<W>* src = seg + t * (uint64_t)merge_tile_n<W>();
   constexpr int R16 = sizeof(Rec<W>) / 16;
   if (R16 * 16 == sizeof(Rec<W>) && (base * sizeof(Rec<W>)) % 16 == 0) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src);

@@ -91,14 +91,19 @@ __device__ __forceinline__ uint32_t ikey_lcp(const Rec<W>& a, const Rec<W>& b, u
 // and its LENGTH in the last byte (byte 71 = low byte of k[8]). For keys of
 // length <= 71, padded bytes then length is exactly Python's bytes order
 // (keys.py:60-63): when the padded bytes agree, the shorter key is a prefix of
-// the longer one and sorts first.
+// the longer one and sorts first. A var job with a user key of 72..255 bytes
+// runs again with W = kVarWLong records (255 key bytes + the length byte).
 constexpr int kVarW = 9;
-constexpr uint32_t kVarMaxLen = 8 * kVarW - 1;  // 71
+constexpr int kVarWLong = 32;
+constexpr uint32_t kVarMaxLen = 8 * kVarW - 1;          // 71
+constexpr uint32_t kVarMaxLenLong = 8 * kVarWLong - 1;  // 255
 
-// Var records are exactly the W = kVarW instantiations (fixed-length jobs use
-// W <= 4), so the var paths compile out of the fixed kernels.
+// Var records are exactly the W = kVarW / kVarWLong instantiations (fixed-length
+// jobs use W <= 4), so the var paths compile out of the fixed kernels.
 template <int W>
-__host__ __device__ constexpr bool is_var() { return W == kVarW; }
+__host__ __device__ constexpr bool is_var() { return W == kVarW || W == kVarWLong; }
+template <int W>
+__host__ __device__ constexpr uint32_t var_maxlen() { return 8 * W - 1; }
 
 template <int W>
 __device__ __forceinline__ uint32_t rec_ulen(const Rec<W>& r, bool var, uint32_t L) {

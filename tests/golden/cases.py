@@ -89,6 +89,13 @@ VARKEY_CASES = [
     ("fixed1", lambda: jobgen.c4(n_per_file=200, files=4, seed=0x41, klen=1, vlen=50), {}),
     ("fixed9_ri2", lambda: jobgen.c3(n=2000, seed=0x09, klen=9, sst_target=32 * 1024),
      dict(sst_size_target=40 * 1024, restart_interval=2)),
+] + [
+    # user keys past the 71-byte var record: the long records (kVarWLong, <= 255 bytes)
+    (f"varkey_long{s}", (lambda s=s: jobgen.varkey(200 + s, max_len=[120, 200, 255][s % 3], n_space=300)),
+     dict(sst_size_target=[16, 64][s % 2] * 1024, restart_interval=[16, 4][s % 2]))
+    for s in range(6)
+] + [
+    ("fixed100", lambda: jobgen.c3(n=1500, seed=0x100, klen=100, sst_target=48 * 1024), dict(sst_size_target=64 * 1024)),
 ]
 
 ALL_CASES = ALL_CASES + VARKEY_CASES

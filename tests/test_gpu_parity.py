@@ -412,16 +412,48 @@ def test_index_keys_one_length_data_keys_mixed(dev):
     assert [(g[1], g[2]) for g in got] == [(w[1], w[2]) for w in want]
 
 
-def test_user_keys_longer_than_71_bytes_unsupported(dev):
+@pytest.mark.parametrize("klen", [72, 80, 200, 255])
+def test_user_keys_longer_than_71_bytes(dev, klen):
+    """Keys past the 71-byte var record re-run on the long records (<= 255
+    bytes), byte-identical to the oracle."""
+    from paper_2004_03054_b200.compaction import compact_files
+    rng = random.Random(0x72 + klen)
+    pairs = sorted(((O.make_ikey(rng.randbytes(klen), i + 1, O.KIND_PUT), b"v" * (i % 7)) for i in range(300)),
+                   key=lambda kv: O.order_key(kv[0]))
+    f = O.build_table(pairs, block_size=1024)
+    short = O.build_table([(O.make_ikey(b"\x01" * 5, 900, O.KIND_PUT), b"s")])  # mixed lengths in the job
+    want = O.reference_compact([short, f], sst_size_target=64 * 1024)
+    from paper_2004_03054_b200.config import StoreConfig
+    got = compact_files(dev, [short, f], [], source_level=0, config=StoreConfig(sst_size_target=64 * 1024))
+    assert [g[0] for g in got] == [w[0] for w in want]
+    assert [(g[1], g[2]) for g in got] == [(w[1], w[2]) for w in want]
+
+
+def test_user_keys_longer_than_255_bytes_unsupported(dev):
     from paper_2004_03054_b200 import UnsupportedInputError
     from paper_2004_03054_b200.compaction import compact_files
-    rng = random.Random(0x72)
-    pairs = sorted(((O.make_ikey(rng.randbytes(80), i + 1, O.KIND_PUT), b"v") for i in range(50)),
+    rng = random.Random(0x73)
+    pairs = sorted(((O.make_ikey(rng.randbytes(300), i + 1, O.KIND_PUT), b"v") for i in range(50)),
                    key=lambda kv: O.order_key(kv[0]))
     f = O.build_table(pairs)
     O.reference_compact([f])  # the reference accepts them
     with pytest.raises(UnsupportedInputError):
         compact_files(dev, [f], [], source_level=0)
+
+
+@pytest.mark.parametrize("ext", [b"\x00", b"\xff"])
+def test_long_var_key_prefix_extension(dev, ext):
+    """Prefix / extension pairs on the long records (lengths 72..254)."""
+    from paper_2004_03054_b200.compaction import compact_files
+    from paper_2004_03054_b200.config import StoreConfig
+    base = bytes((i * 7 + 1) & 0xFF for i in range(260))
+    for L in list(range(70, 90)) + [120, 127, 128, 129, 200, 247, 248, 253]:
+        keys = [base[:L], base[:L] + ext]
+        pairs = [(O.make_ikey(k, 100 + i, O.KIND_PUT), b"v" * 7) for i, k in enumerate(keys)]
+        f = O.build_table(pairs + [(O.make_ikey(b"\xff" * 3, 1, O.KIND_PUT), b"z")], sst_size_target=1 << 20)
+        want = O.reference_compact([f], sst_size_target=1 << 20)
+        got = compact_files(dev, [f], [], source_level=0, config=StoreConfig(sst_size_target=1 << 20))
+        assert [g[0] for g in got] == [w[0] for w in want], f"L={L}"
 
 
 def test_crc_error_outranks_later_data_errors(dev):
