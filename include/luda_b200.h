@@ -156,6 +156,16 @@ int luda_build_from_sorted(const uint8_t* dev_user_keys, uint32_t user_key_len,
                            uint32_t bits_per_key, uint64_t sst_size_target,
                            luda_job_result* result, void* stream);
 
+/* As luda_build_from_sorted for user keys of mixed lengths (any length <=
+ * 255 bytes, max_key_len = the longest): key i = dev_user_keys[key_off[i] ..
+ * + key_len[i]] (device arrays). The generic-length records of the compaction
+ * path; L0 flush of a memtable whose keys differ in length. */
+int luda_build_from_sorted_var(const uint8_t* dev_user_keys, const uint64_t* dev_key_off,
+                               const uint32_t* dev_key_len, uint32_t max_key_len, const uint64_t* dev_trailers,
+                               const uint8_t* dev_values, const uint64_t* dev_value_off,
+                               const uint32_t* dev_value_len, uint64_t n, uint32_t block_size,
+                               uint32_t restart_interval, uint32_t bits_per_key, uint64_t sst_size_target,
+                               luda_job_result* result, void* stream);
 /* As luda_build_from_sorted, but cut an output SST every `entries_per_file`
  * entries (the last SST may hold fewer; sst_size_target is then unused):
  * synthesises input levels whose file boundaries are known in advance

@@ -890,10 +890,58 @@ __global__ void records_from_arrays_kernel(const uint8_t* keys, uint32_t L, cons
   out[i] = r;
 }
 
+// Var records (luda_rec.cuh) from flat arrays of keys of any length <= 8W-1:
+// key i = keys[koff[i] .. + klen[i]], zero padded, its length in byte 8W-1.
+template <int W>
+__global__ void records_from_var_arrays_kernel(const uint8_t* keys, const uint64_t* koff, const uint32_t* klen,
+                                               const uint64_t* trailers, const uint64_t* voff, const uint32_t* vlen,
+                                               uint64_t n, Rec<W>* out, unsigned long long* bad) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t* k = keys + koff[i];
+  const uint32_t L = klen[i];
+  Rec<W> r;
+  for (int j = 0; j < W; ++j) {
+    uint64_t v = 0;
+    for (int b = 0; b < 8; ++b) {
+      const uint32_t idx = 8 * j + b;
+      v = (v << 8) | (idx < L ? k[idx] : 0u);
+    }
+    r.k[j] = v;
+  }
+  r.k[W - 1] |= L;  // byte 8W-1: always padding (L <= 8W-1)
+  r.t = ~trailers[i];
+  if (vlen[i] > kMaxValueLen || voff[i] > kMaxValueOff) atomicMin(bad, 0ull);
+  r.h = handle_pack(voff[i], vlen[i]);
+  out[i] = r;
+}
+
 template <int W>
 __global__ void check_sorted_kernel(const Rec<W>* r, uint64_t n, unsigned long long* bad) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1;
   if (i < n && rec_cmp(r[i - 1], r[i]) >= 0) atomicMin(bad, (unsigned long long)i);
+}
+
+template <int W>
+int build_var_w(cudaStream_t st, Scratch& scratch, const uint8_t* keys, const uint64_t* koff, const uint32_t* klen,
+                const uint64_t* tr, const uint8_t* values, const uint64_t* voff, const uint32_t* vlen, uint64_t n,
+                const EmitParams& ep, luda_job_result* res) {
+  GET(R, Rec<W>, n, false);
+  GET(bad, unsigned long long, 1, false);
+  CK(cudaMemsetAsync(bad, 0xFF, 8, st));
+  const unsigned g = (unsigned)((n + 255) / 256);
+  records_from_var_arrays_kernel<W><<<g, 256, 0, st>>>(keys, koff, klen, tr, voff, vlen, n, R, bad);
+  ++g_launches;
+  check_sorted_kernel<W><<<g, 256, 0, st>>>(R, n, bad);
+  ++g_launches;
+  unsigned long long hb = 0;
+  CK(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
+  int rc = sync(st);
+  if (rc) return rc;
+  if (hb == 0) return fail(LUDA_UNSUPPORTED, "value too large for the b200 record handle");
+  if (hb != ~0ull) return fail(LUDA_ORDERING, "keys not strictly ascending");
+  res->n_in = n;
+  return plan_and_emit<W>(st, scratch, R, n, values, ep, res, nullptr);
 }
 
 template <int W>
@@ -1140,6 +1188,30 @@ int luda_build_files_from_sorted(const uint8_t* keys, uint32_t L, const uint64_t
     case 2: rc = build_w<2>(st, scratch, keys, L, trailers, values, voff, vlen, n, ep, res); break;
     case 3: rc = build_w<3>(st, scratch, keys, L, trailers, values, voff, vlen, n, ep, res); break;
     default: rc = build_w<4>(st, scratch, keys, L, trailers, values, voff, vlen, n, ep, res); break;
+  }
+  if (rc) luda_job_release(res);
+  return rc;
+}
+
+int luda_build_from_sorted_var(const uint8_t* keys, const uint64_t* key_off, const uint32_t* key_len,
+                               uint32_t max_key_len, const uint64_t* trailers, const uint8_t* values,
+                               const uint64_t* voff, const uint32_t* vlen, uint64_t n, uint32_t block_size,
+                               uint32_t restart_interval, uint32_t bits_per_key, uint64_t sst_size_target,
+                               luda_job_result* res, void* stream) {
+  if (g_device < 0) return fail(LUDA_DEVICE, "luda_init not called");
+  std::lock_guard<std::mutex> lock(g_job_mu);
+  memset(res, 0, sizeof(*res));
+  if (max_key_len > kVarMaxLenLong) return fail(LUDA_UNSUPPORTED, "user keys longer than 255 bytes");
+  if (restart_interval < 1) return fail(LUDA_DEVICE, "restart_interval must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch scratch(st);
+  EmitParams ep{8 * kVarW + 8, block_size, restart_interval, bits_per_key, sst_size_target, 4, 0, true};
+  int rc;
+  if (max_key_len <= kVarMaxLen) {
+    rc = build_var_w<kVarW>(st, scratch, keys, key_off, key_len, trailers, values, voff, vlen, n, ep, res);
+  } else {
+    ep.K = 8 * kVarWLong + 8;
+    rc = build_var_w<kVarWLong>(st, scratch, keys, key_off, key_len, trailers, values, voff, vlen, n, ep, res);
   }
   if (rc) luda_job_release(res);
   return rc;

@@ -14,16 +14,16 @@ import struct
 import numpy as np
 
 from . import _native
-from .errors import UnsupportedInputError
 
 _TR = struct.Struct("<Q")
 
 
 class DeviceArrays:
-    """Device copies of flat key / trailer / value arrays (luda_region_alloc)."""
+    """Device copies of flat key / trailer / value arrays (luda_region_alloc).
+    ``key_lens`` (generic-length keys): per-key user-key lengths."""
 
     def __init__(self, L, keys: bytes, trailers: np.ndarray, values: bytes, voff: np.ndarray, vlen: np.ndarray,
-                 stream):
+                 stream, key_lens=None):
         self.L = _native.load()
         self.ptrs = []
         self.n = len(trailers)
@@ -33,6 +33,15 @@ class DeviceArrays:
         self.voff = self._put(voff.astype(np.uint64).tobytes(), stream)
         self.vlen = self._put(vlen.astype(np.uint32).tobytes(), stream)
         self.klen = L
+        self.max_key_len = 0
+        if key_lens is not None:
+            kl = np.asarray(key_lens, dtype=np.uint32)
+            ko = np.zeros(len(kl), dtype=np.uint64)
+            if len(kl) > 1:
+                ko[1:] = np.cumsum(kl[:-1], dtype=np.uint64)
+            self.key_off = self._put(ko.tobytes(), stream)
+            self.key_len = self._put(kl.tobytes(), stream)
+            self.max_key_len = int(kl.max()) if len(kl) else 0
 
     def _put(self, data: bytes, stream):
         p = ctypes.c_void_p()
@@ -51,12 +60,16 @@ class DeviceArrays:
 
 
 def pack_pairs(pairs):
-    """(ikey, value) list → (L, keys, trailers, values, voff, vlen)."""
+    """(ikey, value) list → (L, keys, trailers, values, voff, vlen); L = None
+    when the user keys differ in length or are longer than 32 bytes (the
+    generic-length builder; keys then carry their own offsets / lengths)."""
     if not pairs:
         raise ValueError("cannot build an empty table")
     L = len(pairs[0][0]) - 8
-    if any(len(k) - 8 != L for k, _ in pairs):
-        raise UnsupportedInputError("keys of differing lengths are not supported by the b200 fast path")
+    if any(len(k) < 8 for k, _ in pairs):
+        raise ValueError("internal keys are at least 8 bytes (keys.py:39)")
+    if L > 32 or any(len(k) - 8 != L for k, _ in pairs):
+        L = None
     keys = b"".join(k[:-8] for k, _ in pairs)
     trailers = np.array([_TR.unpack_from(k, len(k) - 8)[0] for k, _ in pairs], dtype=np.uint64)
     vlen = np.array([len(v) for _, v in pairs], dtype=np.uint32)
@@ -72,6 +85,12 @@ def build_from_device(arrs: DeviceArrays, *, stream, block_size=4096, restart_in
     """Run luda_build_from_sorted; returns the (device-owned) JobResult."""
     L = _native.load()
     res = _native.JobResult()
+    if arrs.klen is None:  # generic-length keys
+        _native.check(L.luda_build_from_sorted_var(arrs.keys, arrs.key_off, arrs.key_len, arrs.max_key_len,
+                                                   arrs.trailers, arrs.values, arrs.voff, arrs.vlen, arrs.n,
+                                                   block_size, restart_interval, bits_per_key, sst_size_target,
+                                                   ctypes.byref(res), stream))
+        return res
     _native.check(L.luda_build_from_sorted(arrs.keys, arrs.klen, arrs.trailers, arrs.values, arrs.voff, arrs.vlen,
                                            arrs.n, block_size, restart_interval, bits_per_key, sst_size_target,
                                            ctypes.byref(res), stream))
@@ -104,7 +123,8 @@ def build_ssts(pairs, *, device_ordinal=0, block_size=4096, restart_interval=16,
     L = _native.lib(device_ordinal)
     s = ctypes.c_void_p()
     _native.check(L.luda_stream_create(ctypes.byref(s)))
-    arrs = DeviceArrays(*pack_pairs(pairs), s.value)
+    packed = pack_pairs(pairs)
+    arrs = DeviceArrays(*packed, s.value, key_lens=[len(k) - 8 for k, _ in pairs] if packed[0] is None else None)
     try:
         res = build_from_device(arrs, stream=s.value, block_size=block_size, restart_interval=restart_interval,
                                 bits_per_key=bits_per_key, sst_size_target=sst_size_target)

@@ -168,6 +168,26 @@ def test_flush_builder_matches_oracle(native):
         assert [(g[1], g[2]) for g in got] == [(w[1], w[2]) for w in want]
 
 
+@pytest.mark.parametrize("max_len", [64, 200])
+def test_flush_builder_generic_key_lengths(native, max_len):
+    """The L0 flush builder for a memtable whose user keys differ in length
+    (0..max_len bytes, prefix-rich; several versions per key) and for fixed
+    keys longer than 32 bytes: byte-identical to SstBuilder."""
+    from paper_2004_03054_b200.flush import build_ssts
+    rng = random.Random(max_len)
+    job = jobgen.varkey(max_len, max_len=max_len, n_space=600, n_files=3)
+    pairs = sorted((kv for r in job.lower for kv in r.pairs), key=lambda kv: O.order_key(kv[0]))
+    for cfg in (dict(sst_size_target=16 * 1024), dict(sst_size_target=2**31, block_size=1024, restart_interval=3)):
+        want = O.build_tables_split(pairs, **cfg)
+        got = build_ssts(pairs, **cfg)
+        assert [g[0] for g in got] == [w[0] for w in want]
+        assert [(g[1], g[2]) for g in got] == [(w[1], w[2]) for w in want]
+    fixed = sorted(((O.make_ikey(rng.randbytes(48), i + 1, O.KIND_PUT), rng.randbytes(50)) for i in range(2000)),
+                   key=lambda kv: O.order_key(kv[0]))
+    want = O.build_tables_split(fixed, sst_size_target=32 * 1024)
+    assert [g[0] for g in build_ssts(fixed, sst_size_target=32 * 1024)] == [w[0] for w in want]
+
+
 def _corrupt_case():
     job = jobgen.c3(n=2000, seed=5, sst_target=32 * 1024)
     lower, upper = jobgen.materialize(job)
