@@ -21,7 +21,7 @@ import ctypes
 
 from . import _native, errors
 
-KEY_CAP = 256  # bytes reserved per found key (longer keys raise UnsupportedInputError)
+KEY_CAP = 264  # bytes reserved per found internal key: user keys up to 256 bytes (longer: UnsupportedInputError)
 
 # luda_read.cuh GetStatus → reference exception class
 _ERR = {2: errors.FormatError, 3: errors.CorruptionError, 4: errors.FormatError, 5: errors.FormatError,

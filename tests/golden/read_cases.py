@@ -97,6 +97,13 @@ def build(name, builder=O.build_tables_split):
         lower, _ = _files(jobgen.c4(n_per_file=700, files=3), builder)
         qs = [(t, q) for t, f in enumerate(lower) for q in _queries(rng, _user_keys(f), 200, klen=24)]
         return dict(files=lower, mode="table", queries=qs)
+    if name == "varkey_long":
+        job = jobgen.varkey(77, max_len=250, n_space=300)
+        for r in job.lower:
+            r.sst_target = 24 * 1024
+        lower, _ = _files(job, builder)
+        qs = [(t, q) for t, f in enumerate(lower) for q in _queries(rng, _user_keys(f), 150)]
+        return dict(files=lower, mode="table", queries=qs)
     if name.startswith("varkey"):
         job = jobgen.varkey(int(name[6:]), max_len=64)
         for r in job.lower:
@@ -200,8 +207,8 @@ def _malformed():
     return bytes(data), qs
 
 
-READ_CASES = ["c3_tables", "ri4_bs1024", "c4_tables", "varkey0", "varkey1", "values_4k_12k", "bpk1", "corrupt",
-              "store", "malformed"]
+READ_CASES = ["c3_tables", "ri4_bs1024", "c4_tables", "varkey0", "varkey1", "varkey_long", "values_4k_12k", "bpk1",
+              "corrupt", "store", "malformed"]
 
 
 def outcome(fn):
