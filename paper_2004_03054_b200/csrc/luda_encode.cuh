@@ -451,6 +451,7 @@ struct EncLane {
   uint32_t s, hv, esz, off, win, wpre, soff;
   uint64_t voff;
   uint32_t vl;
+  uint32_t kl;         // internal key length of the entry (the job's K, or per record for var jobs)
   bool fast;
 };
 
@@ -470,7 +471,10 @@ __device__ __forceinline__ void enc_load(const EncodeArgs<W>& a, uint32_t k, Enc
 template <int W>
 __device__ __forceinline__ void enc_layout(const EncodeArgs<W>& a, EncLane<W>& e) {
   const uint32_t lane = lane_id();
-  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage && a.K < 128 && !is_var<W>();
+  // var records of <= 71-byte keys (W = kVarW) take the fast path with a key
+  // length per lane (internal keys <= 79 bytes: one-byte shared / unshared
+  // varints, as put_prefix_words needs); the long records stay generic
+  e.fast = e.valid && e.cnt <= 32 && e.size <= (uint32_t)kEncStage && a.K < 128 && W != kVarWLong;
   if (!e.fast) return;
   const uint32_t K = a.K, L = K - 8;
   const bool act = lane < e.cnt;
@@ -481,12 +485,14 @@ __device__ __forceinline__ void enc_layout(const EncodeArgs<W>& a, EncLane<W>& e
   e.s = 0;
   e.hv = e.esz = e.vl = 0;
   e.voff = 0;
+  e.kl = K;
   if (act) {
-    if (lane % a.ri != 0) e.s = ikey_lcp(pr, e.r, L);
+    if (is_var<W>()) e.kl = rec_ulen(e.r, true, 0) + 8;
+    if (lane % a.ri != 0) e.s = ikey_lcp_any(pr, e.r, is_var<W>(), L);
     e.vl = handle_len(e.r.h);
     e.voff = handle_off(e.r.h);
-    e.hv = varint_size(e.s) + varint_size(K - e.s) + varint_size(e.vl);
-    e.esz = e.hv + (K - e.s) + e.vl;
+    e.hv = varint_size(e.s) + varint_size(e.kl - e.s) + varint_size(e.vl);
+    e.esz = e.hv + (e.kl - e.s) + e.vl;
   }
   const uint32_t incl = warp_incl_scan<uint32_t>(e.esz);
   e.off = incl - e.esz;
@@ -544,7 +550,7 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   uint8_t* sbase = wbuf + kEncPre;
   uint8_t* dst = sbase + (e.out_off & 15);
   uint32_t first = 0;
-  if (lane < e.cnt) first = put_prefix_words<W>(dst + e.off, e.r, L, e.s, e.vl, e.hv);
+  if (lane < e.cnt) first = put_prefix_words<W>(dst + e.off, e.r, e.kl - 8, e.s, e.vl, e.hv);
   __syncwarp();
   if (lane < e.cnt) {
     put_prefix_first(dst + e.off, first);
@@ -562,7 +568,7 @@ __device__ __forceinline__ void enc_assemble(const EncodeArgs<W>& a, const EncLa
   // Blocks of few, large values (cnt <= 16) share each value among G = 32/2^ceil(log2 cnt) lanes.
   const uint32_t lgc = e.cnt <= 1 ? 0u : 32u - __clz(e.cnt - 1u);
   const uint32_t G = 32u >> lgc;
-  const uint32_t vdst = (uint32_t)(e.out_off & 15u) + e.off + e.hv + (K - e.s);
+  const uint32_t vdst = (uint32_t)(e.out_off & 15u) + e.off + e.hv + (e.kl - e.s);
   if (G == 1) {
     if (!LUDA_ABLATE(a, 4) && lane < e.cnt) value_copy16(sbase, stg, vdst, soff, e.vl, 0u, false, 0u, false);
   } else {
