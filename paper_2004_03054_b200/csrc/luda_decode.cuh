@@ -405,15 +405,29 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
     w = act ? ld_u32_any(d + pos) : 0u;
     return act;
   };
-  auto bad_of = [&](uint32_t w, uint32_t j) -> uint32_t {
+  // Canonical header (1-byte shared / unshared, 1-2 byte value length), restart
+  // entries unshared, and the key length: the job's K, or for var records
+  // (generic-length keys) 8..8W+7 bytes with shared <= the previous key's
+  // length (decode_data_block's "truncated block entry" check). pk: the
+  // previous entry's key length (lane - 1, same interval when j > 0).
+  auto bad_of = [&](uint32_t w, uint32_t j, uint32_t pk) -> uint32_t {
     const uint32_t s = w & 0xFFu, u = prmt(w, 0u, 0x4441u), two = (w >> 23) & 1u;
-    return (w & 0x8080u) | (two & (w >> 31)) | ((s + u) ^ K) | (j == 0 ? s : 0u);
+    uint32_t klen_bad;
+    if (is_var<W>()) klen_bad = (s + u < 8u) | (s + u - 8u > var_maxlen<W>()) | (j > 0 && s > pk);
+    else klen_bad = (s + u) ^ K;
+    return (w & 0x8080u) | (two & (w >> 31)) | klen_bad | (j == 0 ? s : 0u);
+  };
+  auto prev_klen = [&](uint32_t w, bool act) -> uint32_t {  // all lanes call
+    const uint32_t ku = act ? (w & 0xFFu) + prmt(w, 0u, 0x4441u) : 0u;
+    return is_var<W>() ? __shfl_up_sync(0xFFFFFFFFu, ku, 1) : 0u;
   };
   if (nchunks > 1) {  // validate every chunk before the first record is written
     uint32_t bad = 0;
     for (uint32_t q = 0; q < nchunks; ++q) {
       uint32_t pos, w, j;
-      if (slot(q, pos, w, j)) bad |= bad_of(w, j);
+      const bool act = slot(q, pos, w, j);
+      const uint32_t pk = prev_klen(w, act);
+      if (act) bad |= bad_of(w, j, pk);
     }
     if (__any_sync(0xFFFFFFFFu, bad != 0)) return false;
   }
@@ -422,7 +436,10 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
     uint32_t pos, w, j;
     const bool act = slot(q, pos, w, j);
     DEC_T(4);
-    if (nchunks == 1 && __any_sync(0xFFFFFFFFu, act && bad_of(w, j) != 0)) return false;
+    if (nchunks == 1) {
+      const uint32_t pk = prev_klen(w, act);
+      if (__any_sync(0xFFFFFFFFu, act && bad_of(w, j, pk) != 0)) return false;
+    }
     DEC_T(5);
     const uint32_t s = act ? (w & 0xFFu) : 0u;
     const uint32_t two = (w >> 23) & 1u;
@@ -473,8 +490,15 @@ __device__ __forceinline__ bool dec_fast_records(const DecodeArgs<W>& a, const D
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, act);
     if (act) {
       Rec<W> r;
-      words_to_rec<W, NW>(fixed, L, r);
-      r.h = handle_pack(st.addr + kpos + (K - s), vl);
+      const uint32_t u = prmt(w, 0u, 0x4441u);  // unshared (== K - s on the fixed path)
+      if (is_var<W>()) {
+        const uint32_t Lr = s + u - 8u;
+        words_to_rec<W, NW>(fixed, Lr, r);
+        r.k[W - 1] |= Lr;  // the length byte (byte 8W-1 is padding: Lr <= 8W-1)
+      } else {
+        words_to_rec<W, NW>(fixed, L, r);
+      }
+      r.h = handle_pack(st.addr + kpos + u, vl);
       a.out[e0 + __popc(m & lt)] = r;
     }
     e0 += __popc(m);
@@ -793,7 +817,19 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       uint64_t n = 0;
       if (is_var<W>()) {
         const uint8_t* d = mt.staged ? ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15) : gp;
-        n = dec_var_block<W>(a, b, mt.addr, mt.len, d, seg0 + cnt, seg1, ps.entries);
+        bool fast = false;
+        if (W == kVarW && mt.staged) {
+          // the fixed path's positions walk + lane-per-entry records, with a
+          // key length per entry; anything outside its envelope (or an error)
+          // goes through the exact sequential walk below
+          DecState stt = dec_phase1<W, true>(a, b, mt.addr, mt.len, d, slots);
+          if (stt.mode == 1 && !stt.code && !stt.restart_bad && seg0 + cnt + stt.n <= seg1 &&
+              dec_fast_records<W>(a, stt, seg0 + cnt, d, reinterpret_cast<const uint32_t*>(slots), smem_u32(d))) {
+            n = stt.n;
+            fast = true;
+          }
+        }
+        if (!fast) n = dec_var_block<W>(a, b, mt.addr, mt.len, d, seg0 + cnt, seg1, ps.entries);
       } else if (!LUDA_ABLATE(a, 4)) {
         if (mt.staged) {
           const uint8_t* d = ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15);
