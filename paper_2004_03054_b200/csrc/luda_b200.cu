@@ -1309,7 +1309,7 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   GET(cstored, uint32_t, 2ull * nf, false);
   GET(ccrc, uint32_t, 2ull * nf, false);
   ParseArgs pa{jd->arena, d_faddr, d_fsize, nf, info, caddr, clen, cstored};
-  parse_files_a<<<(nf * 32 + 255) / 256, 256, 0, st>>>(pa);
+  parse_files_a<<<(nf * 32 + kParseAThreads - 1) / kParseAThreads, kParseAThreads, 0, st>>>(pa);
   ++g_launches;
   CK(cudaGetLastError());
   // Filter / index CRCs on the side stream, concurrently with the block table

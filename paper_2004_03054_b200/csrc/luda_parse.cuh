@@ -75,26 +75,128 @@ __device__ __forceinline__ int varint_read(const uint8_t* buf, uint64_t n, uint6
   }
 }
 
-// Sequential decode_index_block walk. Emits entries through `emit(i, off, len)`.
+// decode_index_block's sequential walk (sst.py:79-102), by a whole warp
+// through a shared-memory window: the lanes load kIdxWin bytes at the current
+// entry (coalesced 16-byte granules; a granule holding any payload byte lies
+// inside the file's allocation). Lane 0 then chains through the window — for the
+// common entry (1-byte varint, entry inside the window and the body) one
+// dependent shared-memory byte load per entry — and lists where each entry's
+// (off, len) sits; the lanes read and emit those in parallel. Any other entry
+// goes through the exact general step (multi-byte varints, errors; off/len
+// past the window read from global memory). Checks in the reference's order:
+// varint (truncated / too long), entry bounds, then trailing bytes. All lanes
+// get the return value / klen (0xFFFFFFFF when the key lengths differ).
+constexpr uint32_t kIdxWin = 4096;
+constexpr uint32_t kIdxList = kIdxWin / 9 + 1;
+struct IdxWalkSmem {
+  uint8_t win[kIdxWin + 16];
+  uint32_t list[kIdxList];  // (entry - first entry of the window) << 16 | window offset of off/len
+};
 template <typename Emit>
-__device__ int index_walk(const uint8_t* body, uint64_t end, uint32_t n, uint32_t& klen_out, Emit emit) {
+__device__ int index_walk_warp(const uint8_t* body, uint64_t end, uint32_t n, uint32_t& klen_out, IdxWalkSmem& sm,
+                               Emit emit) {
+  const uint32_t lane = lane_id();
+  const uint64_t pay = end + 4;  // varints may read into the count (payload = body ∥ count)
   uint64_t pos = 0;
-  uint32_t klen0 = 0xFFFFFFFEu;
-  for (uint32_t i = 0; i < n; ++i) {
-    uint64_t kl;
-    int r = varint_read(body, end + 4, pos, kl);  // payload = body ∥ count
-    if (r == 1) return F_IDX_VARINT_TRUNC;
-    if (r == 2) return F_IDX_VARINT_LONG;
-    if (kl > end || pos + kl + 8 > end) return F_IDX_TRUNC;
-    if (klen0 == 0xFFFFFFFEu) klen0 = (uint32_t)kl;
-    else if (klen0 != (uint32_t)kl) klen0 = 0xFFFFFFFFu;
-    pos += kl;
-    emit(i, ld_u32_le(body + pos), ld_u32_le(body + pos + 4));
-    pos += 8;
+  uint32_t i = 0, klen0 = 0xFFFFFFFEu;
+  int code = F_OK;
+  uint8_t* const win = sm.win;
+  while (true) {
+    const uint32_t go = __shfl_sync(0xFFFFFFFFu, (uint32_t)(i < n && code == F_OK), 0);
+    if (!go) break;
+    // window [A0, A0 + kIdxWin) in absolute addresses, A0 16-aligned at/below
+    // the entry; all of a lane's loads are issued before the first store
+    const uintptr_t A0 = reinterpret_cast<uintptr_t>(body + pos) & ~uintptr_t(15);
+    const uintptr_t Aend = reinterpret_cast<uintptr_t>(body + pay);
+    {
+      constexpr int kPer = kIdxWin / 16 / 32;
+      uint4 v[kPer];
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) {
+        const uintptr_t ad = A0 + 16ull * (lane + 32u * t);
+        v[t] = ad < Aend ? *reinterpret_cast<const uint4*>(ad) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int t = 0; t < kPer; ++t) reinterpret_cast<uint4*>(win)[lane + 32u * t] = v[t];
+    }
+    __syncwarp();
+    const uint32_t i0 = i;
+    uint32_t nl = 0;
+    if (lane == 0) {
+      const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(body + pos) & 15u);
+      const uint64_t wb = pos - mis;  // body offset of window byte 0 (wraps below 0 at the first entry)
+      const uint64_t wlim = pos + (kIdxWin - mis);
+      const bool whole = wlim >= pay;
+      // fast entries end inside the window and the body (the reference bound)
+      const uint64_t capb = wlim < end ? wlim : end;
+      const uint32_t qcap = capb >= pos ? (uint32_t)(capb - pos) + mis : mis;
+      uint32_t q = mis;
+      auto at = [&](uint64_t p) -> uint32_t { return win[p - wb]; };
+      while (i < n) {
+        const uint32_t b = win[q];
+        if (b < 0x80u && q + 9u + b <= qcap) {
+          if (klen0 == 0xFFFFFFFEu) klen0 = b;
+          else if (klen0 != b) klen0 = 0xFFFFFFFFu;
+          sm.list[nl++] = ((i - i0) << 16) | (q + 1u + b);
+          q += 9u + b;
+          ++i;
+          continue;
+        }
+        pos = wb + q;
+        if (!(whole || pos + 10 <= wlim)) break;  // next window
+        uint64_t kl = 0;
+        int shift = 0;
+        bool big = false;
+        int r = -1;
+        while (r < 0) {
+          if (pos >= pay) { r = 1; break; }
+          const uint32_t c = at(pos++);
+          const uint64_t part = (uint64_t)(c & 0x7F);
+          if (shift == 63 && part > 1) big = true;
+          if (shift < 64) kl |= part << shift;
+          if (!(c & 0x80)) { r = 0; break; }
+          shift += 7;
+          if (shift > 63) r = 2;
+        }
+        if (big) kl = ~0ull;
+        if (r == 1) { code = F_IDX_VARINT_TRUNC; break; }
+        if (r == 2) { code = F_IDX_VARINT_LONG; break; }
+        if (kl > end || pos + kl + 8 > end) { code = F_IDX_TRUNC; break; }
+        if (klen0 == 0xFFFFFFFEu) klen0 = (uint32_t)kl;
+        else if (klen0 != (uint32_t)kl) klen0 = 0xFFFFFFFFu;
+        pos += kl;
+        uint32_t off, len;
+        if (pos + 8 <= wlim) {
+          off = at(pos) | (at(pos + 1) << 8) | (at(pos + 2) << 16) | (at(pos + 3) << 24);
+          len = at(pos + 4) | (at(pos + 5) << 8) | (at(pos + 6) << 16) | (at(pos + 7) << 24);
+        } else {
+          off = ld_u32_le(body + pos);
+          len = ld_u32_le(body + pos + 4);
+        }
+        emit(i, off, len);
+        pos += 8;
+        ++i;
+        if (pos >= wlim) break;
+        q = (uint32_t)(pos - wb);
+      }
+      if (code == F_OK && pos < wb + q) pos = wb + q;  // left the loop on the fast path
+    }
+    nl = __shfl_sync(0xFFFFFFFFu, nl, 0);
+    __syncwarp();
+    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(win);
+    for (uint32_t k = lane; k < nl; k += 32) {
+      const uint32_t e = sm.list[k], o = e & 0xFFFFu, sh = (o & 3u) * 8u;
+      const uint32_t x = w32[o >> 2], y = w32[(o >> 2) + 1], z = w32[(o >> 2) + 2];
+      emit(i0 + (e >> 16), __funnelshift_r(x, y, sh), __funnelshift_r(y, z, sh));
+    }
+    __syncwarp();
+    pos = __shfl_sync(0xFFFFFFFFu, pos, 0);
+    i = __shfl_sync(0xFFFFFFFFu, i, 0);
+    code = __shfl_sync(0xFFFFFFFFu, code, 0);
   }
-  if (pos != end) return F_IDX_TRAILING;
-  klen_out = klen0;
-  return F_OK;
+  if (code == F_OK && pos != end) code = F_IDX_TRAILING;
+  klen_out = __shfl_sync(0xFFFFFFFFu, klen0, 0);
+  return code;
 }
 
 // Fixed-stride fast path: every entry is a 1-byte varint klen == K0.
@@ -125,7 +227,9 @@ struct ParseArgs {
 };
 
 // Stage A: warp per file.
-__global__ void parse_files_a(ParseArgs a) {
+constexpr uint32_t kParseAThreads = 128;
+__global__ void __launch_bounds__(kParseAThreads) parse_files_a(ParseArgs a) {
+  __shared__ __align__(16) IdxWalkSmem s_win[kParseAThreads / 32];
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = lane_id();
   if (warp >= a.nfiles) return;
@@ -160,10 +264,9 @@ __global__ void parse_files_a(ParseArgs a) {
       fi.klen = K0;
       fi.stride = 1;
     } else {
-      uint32_t code = 0, kl = 0;
-      if (lane == 0) code = index_walk(body, end, n, kl, [](uint32_t, uint32_t, uint32_t) {});
-      code = __shfl_sync(0xFFFFFFFFu, code, 0);
-      kl = __shfl_sync(0xFFFFFFFFu, kl, 0);
+      uint32_t kl = 0;
+      const uint32_t code = (uint32_t)index_walk_warp(body, end, n, kl, s_win[threadIdx.x >> 5],
+                                                      [](uint32_t, uint32_t, uint32_t) {});
       fi.icode = code;
       fi.nblocks = code ? 0 : n;
       fi.klen = (n == 0) ? 0xFFFFFFFEu : kl;
@@ -368,9 +471,10 @@ __global__ void __launch_bounds__(kParseThreads) parse_files_c(ParseArgs a, cons
       const uint8_t* e = body + (uint64_t)i * E + 1 + K0;
       put(i, ld_u32_le(e), ld_u32_le(e + 4));
     }
-  } else if (blockIdx.y == 0 && threadIdx.x == 0) {
+  } else if (blockIdx.y == 0 && threadIdx.x < 32) {
+    __shared__ __align__(16) IdxWalkSmem s_win;
     uint32_t kl;
-    index_walk(body, end, n, kl, put);
+    index_walk_warp(body, end, n, kl, s_win, put);
   }
 }
 

@@ -563,3 +563,100 @@ def test_varkey_randomized_configs(dev):
         if [g[0] for g in got] != [w[0] for w in want] or [g[1:] for g in got] != [w[1:] for w in want]:
             bad.append((s, cfg))
     assert not bad, bad[:5]
+
+
+def _var_many_blocks(klen_fn, n=3000, seed=0x91):
+    rng = random.Random(seed)
+    keys = sorted({rng.randbytes(klen_fn(rng)) for _ in range(n)})
+    pairs = sorted(((O.make_ikey(k, i + 1, O.KIND_PUT), b"v" * (i % 5)) for i, k in enumerate(keys)),
+                   key=lambda kv: O.order_key(kv[0]))
+    return O.build_table(pairs, block_size=256)
+
+
+def _reseal_index(f: bytes, mutate) -> bytes:
+    """Mutate the index payload (entries ∥ count) and recompute its CRC so the
+    damage reaches decode_index_block (sst.py:79-102) instead of the CRC check."""
+    import struct
+    foff, flen, ioff, ilen, magic = O.FOOTER.unpack_from(f, len(f) - O.FOOTER_SIZE)
+    payload = bytearray(f[ioff:ioff + ilen - 4])
+    mutate(payload)
+    out = bytearray(f[:ioff]) + payload + struct.pack("<I", zlib.crc32(bytes(payload)))
+    ilen2 = len(payload) + 4
+    foff2 = foff if foff < ioff else foff + (ilen2 - ilen)
+    return bytes(out) + bytes(f[ioff + ilen:len(f) - O.FOOTER_SIZE]) + O.FOOTER.pack(foff2, flen, ioff, ilen2, magic)
+
+
+def _index_entry_starts(payload):
+    import struct
+    n = struct.unpack_from("<I", payload, len(payload) - 4)[0]
+    pos, starts = 0, []
+    for _ in range(n):
+        starts.append(pos)
+        kl, pos = O.varint_read(payload, pos)
+        pos += kl + 8
+    return starts
+
+
+@pytest.mark.parametrize("damage", ["count_minus", "count_plus", "klen_big", "klen_cont", "klen_long_varint",
+                                    "klen_short", "count_ff"])
+def test_index_parse_errors_multi_window(dev, damage):
+    """decode_index_block errors (varint truncated / too long, truncated entry,
+    trailing bytes) at entries far past the first staged window of the warp
+    walk, on a mixed-length index (no fixed stride): same exception class and
+    message as the reference's Table.__init__."""
+    import struct
+    from paper_2004_03054_b200.compaction import compact_files
+    f = _var_many_blocks(lambda r: r.randint(8, 60))
+
+    def mut(p):
+        starts = _index_entry_starts(p)
+        n = len(starts)
+        late = starts[int(n * 0.8)]
+        if damage == "count_minus":
+            struct.pack_into("<I", p, len(p) - 4, n - 1)
+        elif damage == "count_plus":
+            struct.pack_into("<I", p, len(p) - 4, n + 1)
+        elif damage == "klen_big":
+            p[late] = 0x7F
+        elif damage == "klen_cont":
+            p[late] = p[late] | 0x80
+        elif damage == "klen_long_varint":
+            p[late:late + 11] = b"\xff" * 11
+        elif damage == "klen_short":
+            p[late] = max(0, p[late] - 3)
+        elif damage == "count_ff":  # the walk runs into the count: varint truncated
+            struct.pack_into("<I", p, len(p) - 4, 0xFFFFFFFF)
+    g = _reseal_index(f, mut)
+    with pytest.raises(Exception) as want:
+        O.reference_compact([g])
+    with pytest.raises(Exception) as got:
+        compact_files(dev, [g], [], source_level=0)
+    assert type(got.value).__name__ == type(want.value).__name__
+    assert str(got.value) == str(want.value)
+
+
+@pytest.mark.parametrize("klen", [1000, 2100, 5000])
+def test_index_keys_longer_than_the_walk_window(dev, klen):
+    """Index entries whose keys exceed the warp walk's 2 KB window parse
+    (off/len read past the window); the job is then unsupported (keys > 255 B)."""
+    from paper_2004_03054_b200 import UnsupportedInputError
+    from paper_2004_03054_b200.compaction import compact_files
+    rng = random.Random(klen)
+    pairs = sorted(((O.make_ikey(rng.randbytes(klen), i + 1, O.KIND_PUT), b"v") for i in range(40)),
+                   key=lambda kv: O.order_key(kv[0]))
+    f = O.build_table(pairs, block_size=256)
+    O.reference_compact([f])
+    with pytest.raises(UnsupportedInputError):
+        compact_files(dev, [f], [], source_level=0)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_var_many_blocks_multi_window_index(dev, seed):
+    """A mixed-length job whose indexes span many walk windows: byte-identical."""
+    from paper_2004_03054_b200.compaction import compact_files
+    from paper_2004_03054_b200.config import StoreConfig
+    a = _var_many_blocks(lambda r: r.randint(8, 70), seed=seed)
+    b = _var_many_blocks(lambda r: r.choice([8, 9, 40, 70, 71]), n=2000, seed=seed + 100)
+    want = O.reference_compact([a, b], sst_size_target=128 * 1024)
+    got = compact_files(dev, [a, b], [], source_level=0, config=StoreConfig(sst_size_target=128 * 1024))
+    assert [g[0] for g in got] == [w[0] for w in want]
