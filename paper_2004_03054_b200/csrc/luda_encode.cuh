@@ -768,22 +768,28 @@ struct MetaArgs {
   const uint64_t* blk_ipos;    // var jobs: index-entry offsets (luda_plan.cuh), else nullptr
 };
 
-// Bloom hash h = crc32(user key) (bloom.py:28-29): 4-byte words of the key
-// through the slicing-by-2 update, the tail bytewise.
+// Bloom hash h = crc32(user key) (bloom.py:28-29): the L/4 whole 4-byte words
+// of the key through the slicing-by-2 update, then the L%4 tail bytes of the
+// next word. wmax: a warp-uniform bound on L/4 (var records: the warp's
+// longest key, so short keys do not walk all 2W predicated words).
 template <int W>
-__device__ __forceinline__ uint32_t user_key_crc(const Rec<W>& r, uint32_t L, const CrcLane& tl) {
+__device__ __forceinline__ uint32_t key_word_be(const Rec<W>& r, int w) {
+  return (uint32_t)(r.k[w >> 1] >> ((w & 1) ? 0 : 32));
+}
+template <int W>
+__device__ __forceinline__ uint32_t user_key_crc(const Rec<W>& r, uint32_t L, const CrcLane& tl,
+                                                 uint32_t wmax = 2 * W) {
   uint32_t c = 0xFFFFFFFFu;
+  const uint32_t nw = L >> 2;
 #pragma unroll
   for (int w = 0; w < 2 * W; ++w) {
-    if ((uint32_t)(4 * w + 4) <= L) {
-      const uint32_t be = (uint32_t)(r.k[w >> 1] >> ((w & 1) ? 0 : 32));
-      c = crc_word(c, bswap32(be), tl);
-    }
+    if (is_var<W>() && (uint32_t)w >= wmax) break;
+    if ((uint32_t)w < nw) c = crc_word(c, bswap32(key_word_be<W>(r, w)), tl);
   }
+  uint32_t tw = 0;  // the word holding the tail bytes (static indices: the record stays in registers)
 #pragma unroll
-  for (int j = 0; j < 8 * W; ++j)  // static indices: the record stays in registers
-    if ((uint32_t)j >= (L & ~3u) && (uint32_t)j < L)
-      c = crc_byte(c, (uint32_t)(r.k[j >> 3] >> (56 - 8 * (j & 7))) & 0xFFu, tl);
+  for (int w = 0; w < 2 * W; ++w) tw = ((uint32_t)w == nw) ? key_word_be<W>(r, w) : tw;
+  for (uint32_t t = 0; t < (L & 3u); ++t) c = crc_byte(c, (tw >> (24 - 8 * t)) & 0xFFu, tl);
   return ~c;
 }
 
@@ -836,7 +842,11 @@ __global__ void __launch_bounds__(kMetaThreads, 1) sst_meta_kernel(MetaArgs<W> a
         // together (ILP) before any probe
         uint32_t h[meta_unroll<W>()];
 #pragma unroll
-        for (int u = 0; u < meta_unroll<W>(); ++u) h[u] = user_key_crc<W>(r[u], rec_ulen(r[u], is_var<W>(), L), tl);
+        for (int u = 0; u < meta_unroll<W>(); ++u) {
+          const uint32_t Lu = rec_ulen(r[u], is_var<W>(), L);
+          const uint32_t wmax = is_var<W>() ? __reduce_max_sync(__activemask(), Lu >> 2) : 2 * W;
+          h[u] = user_key_crc<W>(r[u], Lu, tl, wmax);
+        }
 #pragma unroll
         for (int u = 0; u < meta_unroll<W>(); ++u) {
           if (e0 + (uint64_t)u * kMetaThreads < e_end) {
