@@ -537,11 +537,17 @@ int plan_and_emit(cudaStream_t st, Scratch& scratch, const Rec<W>* S, uint64_t n
   GET(jmp, uint32_t, n, false);
   GET(bsz, uint32_t, n, false);
   GET(ctl, unsigned int, 4, true);  // jmax, overflow, jmax_sst
-  BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1, p.file_entries, p.var};
-  const size_t jsm = (2ull * (kJumpTile + halo) + 1) * 4;
-  CK(cudaFuncSetAttribute(block_jump_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jsm));
+  // kJumpTile survivors per CTA; small jobs (c2: ~22 K survivors) use smaller
+  // tiles so that >= 2 CTAs per SM still run (the halo is re-read per tile)
+  const uint64_t fill = (n + 2ull * g_num_sms - 1) / (2ull * g_num_sms);
+  const uint32_t jtile = (uint32_t)std::min<uint64_t>(
+      kJumpTile, std::max<uint64_t>(kJumpThreads, (fill + kJumpThreads - 1) / kJumpThreads * kJumpThreads));
+  BlockJumpArgs<W> ja{S, n, p.K, p.block_size, p.ri, halo, jmp, bsz, ctl, ctl + 1, p.file_entries, p.var, jtile};
+  const size_t jsm = (2ull * (jtile + halo) + 1) * 4;
+  CK(cudaFuncSetAttribute(block_jump_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)((2ull * (kJumpTile + 8192) + 1) * 4)));
   KT_START(2, st);
-  block_jump_kernel<W><<<(unsigned)((n + kJumpTile - 1) / kJumpTile), kJumpThreads, jsm, st>>>(ja);
+  block_jump_kernel<W><<<(unsigned)((n + jtile - 1) / jtile), kJumpThreads, jsm, st>>>(ja);
   ++g_launches;
   KT_STOP(2, st);
   CK(cudaGetLastError());

@@ -752,6 +752,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
   const uint32_t p = warp % kDecPairs;
   const bool parse = warp < kDecPairs;
   DecPairSmem& ps = pairs[p];
+#ifdef LUDA_DEC_CTA_TIMES  // per-CTA start/end timestamps (experiment builds: profiles/cta_times.py)
+  uint64_t t_start = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   crc_smem_init(cs);
   constexpr int kLeadChunks = kDecLead / 16;
   for (uint32_t i = threadIdx.x; i < kDecPairs * kDecNSlot * kLeadChunks; i += blockDim.x) {
@@ -886,6 +890,16 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       if (lane == 0) mbar_arrive(&ps.empty[s]);
     }
   }
+#ifdef LUDA_DEC_CTA_TIMES
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t_end;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("CTAT %u %u %llu %llu\n", blockIdx.x, smid, (unsigned long long)t_start, (unsigned long long)t_end);
+  }
+#endif
 }
 
 // Segment starts (logical record index): exclusive scan of the segment

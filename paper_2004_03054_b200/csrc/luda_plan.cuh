@@ -52,6 +52,7 @@ struct BlockJumpArgs {
   unsigned int* overflow;
   uint64_t file_entries;  // > 0: a block never crosses a multiple of this (file-cut builds)
   bool var;               // generic-length keys: K per record (luda_rec.cuh)
+  uint32_t tile;          // survivors per CTA (<= kJumpTile; smaller for small jobs)
 };
 
 // Block size if a block started at local index i held n entries:
@@ -64,11 +65,12 @@ struct BlockJumpArgs {
 template <int W>
 __global__ void __launch_bounds__(kJumpThreads) block_jump_kernel(BlockJumpArgs<W> a) {
   extern __shared__ __align__(16) uint32_t sz[];  // PB[span+1], D[span]
-  const uint32_t span = kJumpTile + a.halo;
+  const uint32_t tile = a.tile;
+  const uint32_t span = tile + a.halo;
   uint32_t* PB = sz;
   uint32_t* D = sz + span + 1;
   __shared__ uint32_t s_warp[kJumpThreads / 32];
-  const uint64_t t0 = (uint64_t)blockIdx.x * kJumpTile;
+  const uint64_t t0 = (uint64_t)blockIdx.x * tile;
   const uint32_t K = a.K, L = K - 8, vK = varint_size(K);
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
   // sizes → D (full - compressed) and a CTA-wide exclusive scan PB of compressed sizes
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(kJumpThreads) block_jump_kernel(BlockJumpArgs<
   __syncthreads();
   const uint32_t ri = a.ri, bs = a.block_size;
   uint32_t mymax = 0;
-  for (uint32_t i = threadIdx.x; i < (uint32_t)kJumpTile; i += kJumpThreads) {
+  for (uint32_t i = threadIdx.x; i < tile; i += kJumpThreads) {
     const uint64_t j = t0 + i;
     if (j >= a.n) break;
     uint64_t rem64 = a.n - j;
