@@ -721,7 +721,12 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   // capacity comes from the records-per-input-byte ratio of earlier jobs
   // (first job: 1 record per 48 bytes); a job whose largest segment does not
   // fit is decoded again with the exact capacity.
-  const uint32_t nw = (uint32_t)g_num_sms * kDecPairs;  // record segments (one per warp pair)
+  // record segments = block chunks handed to the decode pairs dynamically
+  // (kDecChunksPerPair per pair on big jobs; one per pair, as long as a
+  // chunk would hold >= 8 blocks, on small ones)
+  const uint32_t npairs = (uint32_t)g_num_sms * kDecPairs;
+  const uint32_t nw = std::max<uint32_t>(
+      1u, std::min<uint32_t>(nblk, std::max<uint32_t>(npairs, std::min<uint32_t>(npairs * kDecChunksPerPair, nblk / 8))));
   uint64_t blk_bytes = 0;
   for (uint32_t f = 0; f < jd->n_files; ++f) blk_bytes += jd->file_len[f];
   static double s_ratio = 1.0 / 48.0;
@@ -730,6 +735,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   GET(d_count, uint64_t, nw, false);
   GET(d_lo, uint64_t, nw + 1, false);
   GET(d_max, uint64_t, 1, false);
+  GET(d_ctr, unsigned int, 1, false);
   // file seams of every multi-file run, checked (with the file bases) right
   // after the decode, before any merge pass
   std::vector<uint32_t> run_first(jd->run_first_file, jd->run_first_file + jd->n_runs + 1);
@@ -745,12 +751,13 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
     if (!X) return fail(LUDA_DEVICE, "device allocation failed (records)");
     CK(cudaMemsetAsync(errs, 0xFF, 16, st));
     CK(cudaMemsetAsync(d_max, 0, 8, st));
+    CK(cudaMemsetAsync(d_ctr, 0, 4, st));
 #ifdef LUDA_ABLATION
     static const uint32_t s_dbg = getenv("LUDA_DEC_DBG") ? (uint32_t)atoi(getenv("LUDA_DEC_DBG")) : 0u;
 #else
     const uint32_t s_dbg = 0;
 #endif
-    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, errs, errs + 1, s_dbg, var};
+    DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, nw, d_ctr, errs, errs + 1, s_dbg, var};
     KT_START(0, st);
     decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
     ++g_launches;
@@ -1331,6 +1338,9 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   CK(cudaMemcpyAsync(dc.h, ccrc, 8ull * nf, cudaMemcpyDeviceToHost, dc.side));
   CK(cudaMemcpyAsync(dc.h + 2 * nf, cstored, 8ull * nf, cudaMemcpyDeviceToHost, dc.side));
   CK(cudaEventRecord(dc.done, dc.side));
+#ifdef LUDA_SERIAL_SIDE_CRC  // experiment: the main stream waits for the side-stream CRCs
+  CK(cudaStreamWaitEvent(st, dc.done, 0));
+#endif
   std::vector<FileInfo>& hinfo = dc.info;
   CK(cudaMemcpyAsync(hinfo.data(), info, sizeof(FileInfo) * nf, cudaMemcpyDeviceToHost, st));
   rc = sync(st);

@@ -59,6 +59,10 @@ enum BlockCode : uint32_t {
 #endif
 constexpr int kDecPairs = LUDA_DEC_PAIRS;
 constexpr int kDecWarps = 2 * kDecPairs;
+#ifndef LUDA_DEC_CHUNKS
+#define LUDA_DEC_CHUNKS 4
+#endif
+constexpr uint32_t kDecChunksPerPair = LUDA_DEC_CHUNKS;  // block chunks (record segments) per pair, on average
 constexpr int kDecNSlot = 2;                     // staging slots per pair (1 block in flight)
 constexpr int kDecLead = 48;                     // zero lead before the TMA window (never written by TMA)
 constexpr int kDecStage = 4352;                  // TMA window capacity
@@ -70,6 +74,8 @@ struct DecSlotMeta {
   uint64_t addr;  // arena offset of the block
   uint32_t len;   // block length
   uint32_t staged;
+  uint32_t blk;   // block index (0xFFFFFFFF: end of the pair's sequence)
+  uint32_t chunk; // record segment the block belongs to
 };
 struct DecPairSmem {
   uint8_t slot[kDecNSlot][kDecSlot];
@@ -97,10 +103,12 @@ struct DecodeArgs {
   BlockTable bt;
   uint32_t nblk;
   uint32_t K;               // internal key length of the job
-  Rec<W>* out;              // segmented: warp w writes out[w * seg_cap ...]
+  Rec<W>* out;              // segmented: chunk c's records at out[c * seg_cap ...]
   uint64_t seg_cap;         // records per warp segment
   uint32_t* blk_local;      // out [nblk]: block's first record index within its warp segment
-  uint64_t* seg_count;      // out [nwarps]: records of each warp segment (may exceed seg_cap → rerun)
+  uint64_t* seg_count;      // out [nseg]: records of each segment (may exceed seg_cap → rerun)
+  uint32_t nseg;            // record segments = block chunks
+  unsigned int* chunk_ctr;  // chunk counter (zeroed before the launch)
   unsigned long long* err_ref;
   unsigned long long* err_unsup;
   uint32_t dbg;             // ablation switches (LUDA_ABLATION builds only)
@@ -770,34 +778,66 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
     }
   }
   __syncthreads();
-  // The pair's contiguous block range; its records form one segment.
-  const uint32_t np = gridDim.x * kDecPairs;
-  const uint32_t g = blockIdx.x * kDecPairs + p;
-  const uint32_t b0 = seg_first_block(g, a.nblk, np), b1 = seg_first_block(g + 1, a.nblk, np);
-  const uint32_t nb = b1 - b0;
+  // Work distribution: the blocks are cut into a.nseg contiguous chunks (the
+  // record segments); each pair takes chunks from a global counter, in
+  // order, and its blocks run through the pair's slot pipeline as one
+  // sequence (a chunk never straddles a pipeline restart). Dynamic chunks
+  // keep every SM busy to the end even when a CTA starts late or a chunk
+  // decodes slower than another (static per-pair ranges measured a 2x
+  // step when one CTA could not be placed until another had finished).
   if (parse) {
-    // Producer: TMA of local block k into slot k % 3 once both consumers
-    // released it. Block-table entries are fetched 32 blocks at a time (lane
-    // j holds block kb + j) so no global load sits on the per-block path.
+    // Producer cursor: chunk pc, its blocks [pb, pe). Block-table entries are
+    // fetched 32 blocks at a time (lane j holds block kb + j) so no global
+    // load sits on the per-block path.
+    uint32_t pc = 0, pb = 0, pe = 0;
     uint32_t kb = 0xFFFFFFFFu;
     uint64_t t_addr = 0;
     uint32_t t_len = 0;
-    auto issue = [&](uint32_t k) {
-      if (kb == 0xFFFFFFFFu || k >= kb + 32) {
-        kb = k;
-        const uint32_t bj = b0 + k + lane;
-        t_addr = bj < b1 ? a.bt.addr[bj] : 0;
-        t_len = bj < b1 ? a.bt.len[bj] : 0;
+    uint32_t total = 0xFFFFFFFFu;  // pipeline length, known once the chunks ran out
+    auto next_block = [&](uint32_t& b, uint32_t& c) -> bool {  // warp-uniform
+      while (pb >= pe) {
+#ifdef LUDA_DEC_STATIC_CHUNKS  // experiment: chunk g, g + np, ... (no counter)
+        const uint32_t nc = pe == 0 ? blockIdx.x * kDecPairs + p : pc + gridDim.x * kDecPairs;
+        pe = 1;
+#else
+        uint32_t nc = 0;
+        if (lane == 0) nc = atomicAdd(a.chunk_ctr, 1u);
+        nc = __shfl_sync(0xFFFFFFFFu, nc, 0);
+#endif
+        if (nc >= a.nseg) return false;
+        pc = nc;
+        pb = seg_first_block(nc, a.nblk, a.nseg);
+        pe = seg_first_block(nc + 1, a.nblk, a.nseg);
+        if (pb >= pe && lane == 0) a.seg_count[nc] = 0;  // empty chunk (nblk < nseg)
       }
-      const uint64_t addr = __shfl_sync(0xFFFFFFFFu, t_addr, k - kb);
-      const uint32_t len = __shfl_sync(0xFFFFFFFFu, t_len, k - kb);
+      b = pb++;
+      c = pc;
+      return true;
+    };
+    auto issue = [&](uint32_t k) {
+      const uint32_t s = k % kDecNSlot;
+      uint32_t bj = 0, c = 0;
+      const bool have = next_block(bj, c);
+      if (have && (kb == 0xFFFFFFFFu || bj < kb || bj >= kb + 32)) {
+        kb = bj;
+        const uint32_t bl = bj + lane;
+        t_addr = bl < a.nblk ? a.bt.addr[bl] : 0;
+        t_len = bl < a.nblk ? a.bt.len[bl] : 0;
+      }
+      const uint64_t addr = __shfl_sync(0xFFFFFFFFu, t_addr, (bj - kb) & 31u);
+      const uint32_t len = __shfl_sync(0xFFFFFFFFu, t_len, (bj - kb) & 31u);
+      if (!have) total = k;
       if (lane == 0) {
-        const uint32_t s = k % kDecNSlot;
         if (k >= kDecNSlot) mbar_wait(&ps.empty[s], ((k - kDecNSlot) / kDecNSlot) & 1u);
+        if (!have) {  // end marker for the CRC warp
+          ps.meta[s] = DecSlotMeta{0, 0, 0, 0xFFFFFFFFu, 0};
+          mbar_arrive(&ps.full[s]);
+          return;
+        }
         const uint8_t* gp = a.arena + addr;
         const uint32_t win = dec_window(gp, len);
         const bool st = len >= 12 && win <= (uint32_t)kDecStage;
-        ps.meta[s] = DecSlotMeta{addr, len, st ? 1u : 0u};
+        ps.meta[s] = DecSlotMeta{addr, len, st ? 1u : 0u, bj, c};
         if (st) {
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&ps.full[s], win);
@@ -808,14 +848,25 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
         }
       }
     };
-    for (uint32_t k = 0; k < nb && k < (uint32_t)kDecNSlot; ++k) issue(k);
     DecSlot* slots = reinterpret_cast<DecSlot*>(ps.entries);
-    const uint64_t seg0 = (uint64_t)g * a.seg_cap, seg1 = seg0 + a.seg_cap;
-    uint64_t cnt = 0;
-    for (uint32_t k = 0; k < nb; ++k) {
-      const uint32_t s = k % kDecNSlot, b = b0 + k;
+    uint32_t cur = 0xFFFFFFFFu, issued = 0;
+    uint64_t seg0 = 0, seg1 = 0, cnt = 0;
+    for (uint32_t k = 0;; ++k) {
+      // keep kDecNSlot blocks in flight (one issue site: the kernel is
+      // instruction-cache sensitive)
+      while (issued < k + kDecNSlot && total == 0xFFFFFFFFu) issue(issued++);
+      if (k >= total) break;
+      const uint32_t s = k % kDecNSlot;
       mbar_wait(&ps.full[s], (k / kDecNSlot) & 1u);
       const DecSlotMeta mt = ps.meta[s];
+      const uint32_t b = mt.blk;
+      if (mt.chunk != cur) {
+        if (cur != 0xFFFFFFFFu && lane == 0) a.seg_count[cur] = cnt;
+        cur = mt.chunk;
+        seg0 = (uint64_t)cur * a.seg_cap;
+        seg1 = seg0 + a.seg_cap;
+        cnt = 0;
+      }
       const uint8_t* gp = a.arena + mt.addr;
       if (lane == 0) a.blk_local[b] = (uint32_t)cnt;
       uint64_t n = 0;
@@ -850,15 +901,17 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       fence_proxy_async_smem();  // this lane's generic slot accesses before the next TMA into it
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps.empty[s]);
-      if (k + kDecNSlot < nb) issue(k + kDecNSlot);
     }
-    if (lane == 0) a.seg_count[g] = cnt;
+    if (cur != 0xFFFFFFFFu && lane == 0) a.seg_count[cur] = cnt;
   } else {
-    // CRC warp: verify every block of the range (reference: before parsing)
-    for (uint32_t k = 0; k < nb; ++k) {
-      const uint32_t s = k % kDecNSlot, b = b0 + k;
+    // CRC warp: verify every block of the pair's sequence (reference: before
+    // parsing), up to the producer's end marker
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t s = k % kDecNSlot;
       mbar_wait(&ps.full[s], (k / kDecNSlot) & 1u);
       const DecSlotMeta mt = ps.meta[s];
+      if (mt.blk == 0xFFFFFFFFu) break;
+      const uint32_t b = mt.blk;
       const bool st_ok = mt.staged != 0;
       const uint32_t len = mt.len;
       if (len >= 12 && !LUDA_ABLATE(a, 1)) {
