@@ -1370,6 +1370,7 @@ int luda_compact(const luda_job_desc* jd, luda_job_result* res, void* stream) {
   }
   const uint32_t nblk = fbb[nf];
   if (nblk == 0) return deferred_crc_check();  // no data blocks: empty output
+  if (nblk >= kDecEnd) return fail(LUDA_UNSUPPORTED, "more than 2^31 - 1 data blocks in one job");
   // Fixed-K records when every index key has one length <= 32 bytes; else
   // (mixed lengths, longer keys) the generic-length "var" records.
   bool var = mixed || K < 8 || K - 8 > 32;

@@ -55,7 +55,7 @@ enum BlockCode : uint32_t {
 // a pair of staging slots; both consume every block of the pair's contiguous
 // block range concurrently (the CRC never modifies bytes the parse warp reads).
 #ifndef LUDA_DEC_PAIRS
-#define LUDA_DEC_PAIRS 14
+#define LUDA_DEC_PAIRS 12
 #endif
 constexpr int kDecPairs = LUDA_DEC_PAIRS;
 constexpr int kDecWarps = 2 * kDecPairs;
@@ -63,7 +63,10 @@ constexpr int kDecWarps = 2 * kDecPairs;
 #define LUDA_DEC_CHUNKS 4
 #endif
 constexpr uint32_t kDecChunksPerPair = LUDA_DEC_CHUNKS;  // block chunks (record segments) per pair, on average
-constexpr int kDecNSlot = 2;                     // staging slots per pair (1 block in flight)
+#ifndef LUDA_DEC_NSLOT
+#define LUDA_DEC_NSLOT 2
+#endif
+constexpr int kDecNSlot = LUDA_DEC_NSLOT;        // staging slots per pair (NSLOT - 1 blocks in flight)
 constexpr int kDecLead = 48;                     // zero lead before the TMA window (never written by TMA)
 constexpr int kDecStage = 4352;                  // TMA window capacity
 constexpr int kDecSlot = kDecLead + kDecStage;   // bytes per staging slot
@@ -73,10 +76,11 @@ constexpr int kDecBig = kGroup + 192;            // CTA staging for CRC passes o
 struct DecSlotMeta {
   uint64_t addr;  // arena offset of the block
   uint32_t len;   // block length
-  uint32_t staged;
-  uint32_t blk;   // block index (0xFFFFFFFF: end of the pair's sequence)
-  uint32_t chunk; // record segment the block belongs to
+  uint32_t tag;   // block index | staged << 31 (kDecEnd: end of the pair's sequence)
+  __device__ __forceinline__ uint32_t blk() const { return tag & 0x7FFFFFFFu; }
+  __device__ __forceinline__ bool staged() const { return tag >> 31; }
 };
+constexpr uint32_t kDecEnd = 0x7FFFFFFFu;  // (jobs have fewer blocks: luda_compact checks)
 struct DecPairSmem {
   uint8_t slot[kDecNSlot][kDecSlot];
   uint64_t full[kDecNSlot], empty[kDecNSlot];
@@ -830,14 +834,14 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       if (lane == 0) {
         if (k >= kDecNSlot) mbar_wait(&ps.empty[s], ((k - kDecNSlot) / kDecNSlot) & 1u);
         if (!have) {  // end marker for the CRC warp
-          ps.meta[s] = DecSlotMeta{0, 0, 0, 0xFFFFFFFFu, 0};
+          ps.meta[s] = DecSlotMeta{0, 0, kDecEnd};
           mbar_arrive(&ps.full[s]);
           return;
         }
         const uint8_t* gp = a.arena + addr;
         const uint32_t win = dec_window(gp, len);
         const bool st = len >= 12 && win <= (uint32_t)kDecStage;
-        ps.meta[s] = DecSlotMeta{addr, len, st ? 1u : 0u, bj, c};
+        ps.meta[s] = DecSlotMeta{addr, len, bj | (st ? 0x80000000u : 0u)};
         if (st) {
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&ps.full[s], win);
@@ -849,7 +853,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       }
     };
     DecSlot* slots = reinterpret_cast<DecSlot*>(ps.entries);
-    uint32_t cur = 0xFFFFFFFFu, issued = 0;
+    uint32_t cur = 0xFFFFFFFFu, cur_end = 0, issued = 0;
     uint64_t seg0 = 0, seg1 = 0, cnt = 0;
     for (uint32_t k = 0;; ++k) {
       // keep kDecNSlot blocks in flight (one issue site: the kernel is
@@ -859,10 +863,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       const uint32_t s = k % kDecNSlot;
       mbar_wait(&ps.full[s], (k / kDecNSlot) & 1u);
       const DecSlotMeta mt = ps.meta[s];
-      const uint32_t b = mt.blk;
-      if (mt.chunk != cur) {
+      const uint32_t b = mt.blk();
+      if (b >= cur_end) {  // the pair's next chunk (its blocks follow each other within a chunk)
         if (cur != 0xFFFFFFFFu && lane == 0) a.seg_count[cur] = cnt;
-        cur = mt.chunk;
+        cur = seg_of_block(b, a.nblk, a.nseg);
+        cur_end = seg_first_block(cur + 1, a.nblk, a.nseg);
         seg0 = (uint64_t)cur * a.seg_cap;
         seg1 = seg0 + a.seg_cap;
         cnt = 0;
@@ -871,9 +876,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       if (lane == 0) a.blk_local[b] = (uint32_t)cnt;
       uint64_t n = 0;
       if (is_var<W>()) {
-        const uint8_t* d = mt.staged ? ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15) : gp;
+        const uint8_t* d = mt.staged() ? ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15) : gp;
         bool fast = false;
-        if (W == kVarW && mt.staged) {
+        if (W == kVarW && mt.staged()) {
           // the fixed path's positions walk + lane-per-entry records, with a
           // key length per entry; anything outside its envelope (or an error)
           // goes through the exact sequential walk below
@@ -886,7 +891,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
         }
         if (!fast) n = dec_var_block<W>(a, b, mt.addr, mt.len, d, seg0 + cnt, seg1, ps.entries);
       } else if (!LUDA_ABLATE(a, 4)) {
-        if (mt.staged) {
+        if (mt.staged()) {
           const uint8_t* d = ps.slot[s] + kDecLead + (reinterpret_cast<uintptr_t>(gp) & 15);
           DecState stt = dec_phase1<W, true>(a, b, mt.addr, mt.len, d, slots);
           dec_phase2<W, true>(a, b, stt, seg0 + cnt, seg1, d, slots);
@@ -910,9 +915,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 1) decode_kernel(DecodeArgs<W>
       const uint32_t s = k % kDecNSlot;
       mbar_wait(&ps.full[s], (k / kDecNSlot) & 1u);
       const DecSlotMeta mt = ps.meta[s];
-      if (mt.blk == 0xFFFFFFFFu) break;
-      const uint32_t b = mt.blk;
-      const bool st_ok = mt.staged != 0;
+      if (mt.tag == kDecEnd) break;
+      const uint32_t b = mt.blk();
+      const bool st_ok = mt.staged();
       const uint32_t len = mt.len;
       if (len >= 12 && !LUDA_ABLATE(a, 1)) {
         const uint8_t* gp = a.arena + mt.addr;
