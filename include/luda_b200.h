@@ -50,7 +50,11 @@ int luda_abi_version(void);
  * span fewer than 2 tiles per SM, never below the longest jump. Outputs do not depend on it;
  * the parity tests set it to 32 so that small jobs exercise the planner's
  * multi-tile / multi-group composition. */
-enum luda_option { LUDA_OPT_PLANNER_TILE = 1 };
+/* LUDA_OPT_DEC_CTAS: decode CTAs (0 = one per SM) and LUDA_OPT_DEC_SEGS: block
+ * chunks handed out to the decode pairs (0 = automatic). Outputs do not depend
+ * on them; the parity tests use 1 CTA and one block per chunk so that small
+ * jobs exercise the pairs' chunk switching. */
+enum luda_option { LUDA_OPT_PLANNER_TILE = 1, LUDA_OPT_DEC_CTAS = 2, LUDA_OPT_DEC_SEGS = 3 };
 int luda_set_option(int option, int64_t value);
 
 /* ---- regions: device arena + pinned host staging ------------------------ */

@@ -202,6 +202,8 @@ def lib(device_ordinal: int = 0):
 
 
 OPT_PLANNER_TILE = 1  # include/luda_b200.h enum luda_option
+OPT_DEC_CTAS = 2
+OPT_DEC_SEGS = 3
 
 
 def sst_key_pairs(res):

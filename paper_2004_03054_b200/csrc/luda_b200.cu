@@ -46,6 +46,8 @@ thread_local int64_t g_err_off = -1;
 int g_device = -1;
 int g_num_sms = 148;
 uint32_t g_planner_tile = 8192;  // LUDA_OPT_PLANNER_TILE
+uint32_t g_dec_ctas = 0;         // LUDA_OPT_DEC_CTAS (0: one per SM)
+uint32_t g_dec_segs = 0;         // LUDA_OPT_DEC_SEGS (0: automatic)
 
 int fail(int status, const std::string& msg, int64_t off = -1) {
   g_err = msg;
@@ -724,9 +726,12 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
   // record segments = block chunks handed to the decode pairs dynamically
   // (kDecChunksPerPair per pair on big jobs; one per pair, as long as a
   // chunk would hold >= 8 blocks, on small ones)
-  const uint32_t npairs = (uint32_t)g_num_sms * kDecPairs;
+  const uint32_t dec_ctas = g_dec_ctas ? std::min<uint32_t>(g_dec_ctas, (uint32_t)g_num_sms) : (uint32_t)g_num_sms;
+  const uint32_t npairs = dec_ctas * kDecPairs;
   const uint32_t nw = std::max<uint32_t>(
-      1u, std::min<uint32_t>(nblk, std::max<uint32_t>(npairs, std::min<uint32_t>(npairs * kDecChunksPerPair, nblk / 8))));
+      1u, std::min<uint32_t>(nblk, g_dec_segs ? g_dec_segs
+                                              : std::max<uint32_t>(npairs, std::min<uint32_t>(npairs * kDecChunksPerPair,
+                                                                                              nblk / 8))));
   uint64_t blk_bytes = 0;
   for (uint32_t f = 0; f < jd->n_files; ++f) blk_bytes += jd->file_len[f];
   static double s_ratio = 1.0 / 48.0;
@@ -759,7 +764,7 @@ int compact_w(cudaStream_t st, Scratch& scratch, const luda_job_desc* jd, luda_j
 #endif
     DecodeArgs<W> da{jd->arena, bt, nblk, K, X, seg_cap, d_local, d_count, nw, d_ctr, errs, errs + 1, s_dbg, var};
     KT_START(0, st);
-    decode_kernel<W><<<g_num_sms, kDecWarps * 32, dsm, st>>>(da);
+    decode_kernel<W><<<dec_ctas, kDecWarps * 32, dsm, st>>>(da);
     ++g_launches;
     KT_STOP(0, st);
     CK(cudaGetLastError());
@@ -990,6 +995,14 @@ int luda_set_option(int option, int64_t value) {
     case LUDA_OPT_PLANNER_TILE:
       if (value < 32 || value > (1 << 20)) return fail(LUDA_DEVICE, "planner tile must be in [32, 2^20]");
       g_planner_tile = (uint32_t)value;
+      return LUDA_OK;
+    case LUDA_OPT_DEC_CTAS:
+      if (value < 0 || value > (1 << 16)) return fail(LUDA_DEVICE, "decode CTAs must be in [0, 2^16]");
+      g_dec_ctas = (uint32_t)value;
+      return LUDA_OK;
+    case LUDA_OPT_DEC_SEGS:
+      if (value < 0 || value > (1 << 24)) return fail(LUDA_DEVICE, "decode chunks must be in [0, 2^24]");
+      g_dec_segs = (uint32_t)value;
       return LUDA_OK;
     default:
       return fail(LUDA_DEVICE, "unknown option");

@@ -23,7 +23,7 @@ def main():
     for i in range(steps):
         r = bench.compact_once(L, desc, st)
         dec.append(r.k_ms[0])
-        print(f"step {i} decode {r.k_ms[0]:.3f} merge {r.k_ms[1]:.3f} encode {r.k_ms[3]:.3f} "
+        print(f"step {i} decode {r.k_ms[0]:.3f} merge {r.k_ms[1]:.3f} encode {r.k_ms[3]:.3f} meta {r.k_ms[4]:.3f} "
               f"phases {sum(r.t_ms[:5]):.3f}", flush=True)
         L.luda_job_release(ctypes.byref(r))
     print("decode min %.3f max %.3f mean %.3f" % (min(dec), max(dec), sum(dec) / len(dec)))

@@ -149,6 +149,25 @@ def test_compaction_multitile_planner(dev, small_planner_tiles, name):
     check_case(dev, name)
 
 
+@pytest.fixture(params=[(1, 1 << 24), (1, 3), (2, 7)], ids=["1cta-1blk", "1cta-3chunks", "2cta-7chunks"])
+def decode_chunks(request, native):
+    """Decode work distribution forced small (LUDA_OPT_DEC_CTAS / _SEGS): one
+    CTA with one block per chunk makes each of its 12 pairs switch chunks
+    many times on a small job; 3 or 7 long chunks leave most pairs idle."""
+    from paper_2004_03054_b200 import _native
+    ctas, segs = request.param
+    _native.check(native.luda_set_option(_native.OPT_DEC_CTAS, ctas))
+    _native.check(native.luda_set_option(_native.OPT_DEC_SEGS, segs))
+    yield
+    _native.check(native.luda_set_option(_native.OPT_DEC_CTAS, 0))
+    _native.check(native.luda_set_option(_native.OPT_DEC_SEGS, 0))
+
+
+@pytest.mark.parametrize("name", [n for n, _, _ in CASES + EDGE_CASES + VARKEY_CASES[:6] + SPEC_A1_CASES[:12]])
+def test_compaction_decode_chunking(dev, decode_chunks, name):
+    check_case(dev, name)
+
+
 def test_flush_builder_matches_oracle(native):
     from paper_2004_03054_b200.flush import build_ssts
     rng = random.Random(11)
